@@ -1,0 +1,212 @@
+/*
+ * minikv_b200.h -- C ABI of the B200-native MiniKV attention hot path.
+ *
+ * Drop-in boundary for the reference C++ core (namespace minikv in
+ * /root/reference/proj/core/include/minikv).  Every entry point names the
+ * reference interface it replaces.  Plain pointers and sizes only; device
+ * pointers are CUDA global memory on the current device; `stream` is a
+ * cudaStream_t passed as void*.  All compute calls are stream-ordered and
+ * asynchronous; a cache handle is single-writer (the reference's
+ * KVCacheLayer contract): distinct caches may be driven concurrently.
+ *
+ * Errors never throw across the ABI.  Every call returns an mkv_status whose
+ * value maps 1:1 onto the reference's exception class; the
+ * message is available from mkv_last_error() on the calling thread.
+ *
+ * Device data layout:
+ *   Q/K/V/X_O   fp16, [.., tokens, head_dim] with unit-stride channels
+ *   LSE         fp32 [B, Hq, Lq]       A_cumul fp32 [B, Hkv, Lk] (GQA-summed)
+ *   cache       16-token pages of 16*head_dim bytes: 2-bit K codes (per-channel
+ *               groups of 16 tokens) + fp16 (scale, zero), 2-bit V codes
+ *               (per-token groups of 16 channels) + fp16 (scale, zero), in an
+ *               mma-fragment-native order; fp16 residual ring of n_r tokens.
+ */
+#ifndef MINIKV_B200_H
+#define MINIKV_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MKV_ABI_VERSION 1
+
+typedef enum {
+    MKV_OK = 0,
+    MKV_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument */
+    MKV_ERR_DOMAIN = 2,           /* std::domain_error (non-finite input, code > 3) */
+    MKV_ERR_RUNTIME = 3,          /* std::runtime_error (zero kept, empty cache) */
+    MKV_ERR_OUT_OF_RANGE = 4,     /* std::out_of_range */
+    MKV_ERR_CUDA = 5,             /* CUDA runtime / launch failure */
+    MKV_ERR_UNSUPPORTED = 6       /* not an sm_100 device, or an unsupported shape */
+} mkv_status;
+
+/* Thread-local text of the last error on this thread ("" if none). */
+const char* mkv_last_error(void);
+int mkv_abi_version(void);
+/* Succeeds only on a compute-capability 10.0 device (the kernels are sm_100a). */
+int mkv_device_check(int device);
+
+/* ------------------------------------------------------------------------ */
+/* K1  selective flash-attention prefill                                     */
+/* replaces: AttentionResult selective_flash_attn(q, k, v, scale, causal,     */
+/*           TileConfig)        attention.hpp:38-39, attention.cpp:29-117     */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+    const void* q;       /* fp16 [B, Hq, Lq, d]: element (b,h,t,c) at b*q_sb + h*q_sh + t*q_st + c */
+    int64_t q_sb, q_sh, q_st;
+    const void* k;       /* fp16 [B, Hkv, Lk, d] */
+    int64_t k_sb, k_sh, k_st;
+    const void* v;       /* fp16 [B, Hkv, Lk, d] */
+    int64_t v_sb, v_sh, v_st;
+    void* out;           /* fp16 X_O [B, Hq, Lq, d] */
+    int64_t o_sb, o_sh, o_st;
+    float* lse;          /* fp32 [B, Hq, Lq] contiguous (natural log, attention.cpp:98) */
+    float* a_cumul;      /* fp32 [B, Hkv, Lk] contiguous; sum over the G q-heads of each kv-head */
+    int batch, n_q_heads, n_kv_heads, len_q, len_k, head_dim;
+    float scale;
+    int causal;          /* query i sees keys 0 .. len_k - len_q + i (attention.cpp:42,60) */
+} mkv_prefill_args;
+int mkv_prefill_attn(const mkv_prefill_args* args, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* K2  rectified top-k token selection                                       */
+/* replaces: SelectionResult select_token_counts(a_cumul, hh, rw)            */
+/*           selection.hpp:34-35, selection.cpp:10-33                        */
+/* kept[u] = sort(top-hh of a_cumul[u][0, L-rw) by value desc, ties to the   */
+/* lower index) ++ [L-rw, L).  n_kept[u] = min(hh[u] + rw, L).               */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+    const float* a_cumul;      /* device fp32 [n_units, a_stride] */
+    int64_t a_stride;
+    int n_units, length;
+    const int32_t* hh_count;   /* host int32 [n_units] */
+    int rw_count;
+    int32_t* kept;             /* device int32 [n_units, kept_stride] ascending */
+    int64_t kept_stride;
+    int32_t* n_kept;           /* device int32 [n_units] (optional) */
+} mkv_select_args;
+int mkv_select(const mkv_select_args* args, void* stream);
+
+/* Host helpers with the reference's exact arithmetic (selection.cpp:48-83). */
+int mkv_allocate_pyramid(size_t mean_budget_x, size_t layers, size_t depth, int bottom_heavy,
+                         int64_t* per_layer_hh);
+int mkv_allocate_uniform(size_t total_hh, size_t layers, int64_t* per_layer_hh);
+
+/* ------------------------------------------------------------------------ */
+/* Device KV cache: one handle owns n_units (seq, layer, kv-head) caches.    */
+/* replaces: KVCacheLayer make_cache(d, n_r, gs, mode)  cache_engine.hpp:44-46 */
+/* ------------------------------------------------------------------------ */
+typedef struct mkv_cache mkv_cache;
+
+typedef struct {
+    int n_units;
+    int head_dim;               /* 128 (64 also accepted) */
+    int n_r;                    /* residual flush period; multiple of group_size (cache_engine.cpp:13-15) */
+    int group_size;             /* 16 (the only device grouping) */
+    const int32_t* prefill_capacity; /* host [n_units]: max kept tokens at prefill */
+    int max_decode_tokens;      /* decode growth reserved per unit */
+    int keep_fp32_params;       /* also keep fp32 (scale, zero) for bit-exact export */
+} mkv_cache_config;
+
+int mkv_cache_create(const mkv_cache_config* cfg, mkv_cache** out);
+int mkv_cache_destroy(mkv_cache* cache);
+/* Device bytes held: quantized pages, residual ring, metadata. */
+int mkv_cache_bytes(const mkv_cache* cache, uint64_t* page_bytes, uint64_t* residual_bytes,
+                    uint64_t* total_bytes);
+/* Host mirror of one unit's state (exact: updated in call order). */
+int mkv_cache_unit_info(const mkv_cache* cache, int unit, int64_t* tokens_quantized,
+                        int64_t* tokens_residual, int64_t* n_pages, int64_t* n_blocks);
+
+/* ------------------------------------------------------------------------ */
+/* K3  gather + 2-bit quantize + pack of the kept tokens                     */
+/* replaces: prefill(k, v, a_cumul, hh, rw, n_r, gs) after selection,        */
+/*           i.e. gather_rows + append_block(PerChannel K / PerToken V)      */
+/*           cache_engine.cpp:56-77, quantizer.cpp:102-136                   */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+    int unit_begin, n_units;
+    const void* k;              /* fp16: unit i token t row at k + i*k_su + t*k_st (elements) */
+    int64_t k_su, k_st;
+    const void* v;
+    int64_t v_su, v_st;
+    const int32_t* kept;        /* device int32 [n_units, kept_stride], ascending */
+    int64_t kept_stride;
+    const int32_t* n_kept_host; /* host int32 [n_units] (= min(hh + rw, L), known without a sync) */
+} mkv_cache_prefill_args;
+int mkv_cache_prefill(mkv_cache* cache, const mkv_cache_prefill_args* args, void* stream);
+
+/* Select + gather + quantize in one call (prefill, cache_engine.cpp:56-77). */
+typedef struct {
+    int unit_begin, n_units, length;
+    const float* a_cumul;       /* device fp32 [n_units, a_stride] */
+    int64_t a_stride;
+    const int32_t* hh_count;    /* host [n_units] */
+    int rw_count;
+    const void* k;
+    int64_t k_su, k_st;
+    const void* v;
+    int64_t v_su, v_st;
+} mkv_prefill_select_args;
+int mkv_cache_prefill_select(mkv_cache* cache, const mkv_prefill_select_args* args, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* K4  fused unpack-and-multiply 2-bit decode attention                      */
+/* replaces: Vector decode_step(cache, t_q, t_k, t_v, scale)                 */
+/*           cache_engine.hpp:63-64, cache_engine.cpp:100-138 (GQA-batched)  */
+/* Appends (t_k, t_v) to each unit's residual (flushing a full n_r block to  */
+/* 2-bit pages first, cache_engine.cpp:79-90), then attends [pages ; residual]*/
+/* with one softmax.  k_new == NULL attends without appending.               */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+    int unit_begin, n_units;
+    int group;                  /* q-heads per unit (G = Hq / Hkv), 1..8 */
+    const void* q;              /* fp16 [n_units, G, d] */
+    const void* k_new;          /* fp16 [n_units, d] or NULL */
+    const void* v_new;          /* fp16 [n_units, d] or NULL */
+    void* out;                  /* fp16 [n_units, G, d] */
+    float scale;
+} mkv_decode_args;
+int mkv_decode_step(mkv_cache* cache, const mkv_decode_args* args, void* stream);
+/* decode_append only (cache_engine.cpp:79-90). */
+int mkv_cache_append(mkv_cache* cache, int unit_begin, int n_units, const void* k_new,
+                     const void* v_new, void* stream);
+/* Multi-layer decode step: n_layers consecutive calls in one FFI crossing. */
+int mkv_decode_step_layers(mkv_cache* cache, int n_layers, const mkv_decode_args* args,
+                           void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Reference-format export (synchronous): the unit's QuantizedTensor for     */
+/* keys (which = 0, PerChannel) or values (which = 1, PerToken) exactly as   */
+/* quantizer.hpp:30-42 lays it out (continuous 16-codes-per-word stream,     */
+/* per-block grouping, (scale, zero) per group, block_rows), plus the fp16   */
+/* residual rows.  Sizes come from mkv_cache_export_sizes.                   */
+/* ------------------------------------------------------------------------ */
+int mkv_cache_export_sizes(const mkv_cache* cache, int unit, int which, int64_t* n_words,
+                           int64_t* n_params, int64_t* n_blocks);
+int mkv_cache_export_reference(const mkv_cache* cache, int unit, int which,
+                               uint32_t* packed_words, float* params, int64_t* block_rows);
+int mkv_cache_export_residual(const mkv_cache* cache, int unit, uint16_t* r_key_fp16,
+                              uint16_t* r_value_fp16);
+/* Synchronizes and reports device-side input faults (non-finite values met by
+ * the quantizer -> MKV_ERR_DOMAIN, like quantize_group, quantizer.cpp:35-37). */
+int mkv_cache_check(mkv_cache* cache);
+
+/* ------------------------------------------------------------------------ */
+/* Synthetic inputs (benchmarks/tests): the integer-exact approximate-N(0,1) */
+/* fp16 generator of oracle/minikv_oracle.h, bit-identical on device.        */
+/* ------------------------------------------------------------------------ */
+int mkv_synth_fp16(void* out, int64_t n, uint64_t seed, uint64_t stream_id, void* stream);
+/* Rows: out row r (of n_rows, row_len elements, row stride ld) uses stream
+ * stream_base + r * stream_step. */
+int mkv_synth_fp16_rows(void* out, int64_t n_rows, int64_t row_len, int64_t ld, uint64_t seed,
+                        uint64_t stream_base, uint64_t stream_step, void* stream);
+int mkv_synth_uniform_f32(float* out, int64_t n_rows, int64_t row_len, int64_t ld, uint64_t seed,
+                          uint64_t stream_base, uint64_t stream_step, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MINIKV_B200_H */

@@ -1,0 +1,682 @@
+// capi.cu -- the extern "C" boundary (include/minikv_b200.h).
+//
+// Validates arguments with the reference's error classes, keeps an exact host
+// mirror of every unit's cache state (so planning never needs a device sync),
+// owns device memory, and launches the K1-K4 kernels.  No exceptions cross the
+// ABI; no CPU fallback exists -- on a non-sm_100 device every compute call
+// fails with MKV_ERR_UNSUPPORTED.
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "mkv_kernels.h"
+
+using namespace mkv;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int status, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return status;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+    return fail(MKV_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+#define CK(call)                                                    \
+    do {                                                            \
+        cudaError_t e_ = (call);                                    \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call);         \
+    } while (0)
+
+int g_device_ok = -1;  // cached per process (single device per process)
+
+int require_device() {
+    if (g_device_ok < 0) {
+        int dev = 0;
+        cudaDeviceProp prop;
+        if (cudaGetDevice(&dev) != cudaSuccess || cudaGetDeviceProperties(&prop, dev) != cudaSuccess) {
+            g_device_ok = 0;
+        } else {
+            g_device_ok = (prop.major == 10 && prop.minor == 0) ? 1 : 0;
+        }
+    }
+    if (!g_device_ok) return fail(MKV_ERR_UNSUPPORTED, "no compute-capability 10.0 (B200, sm_100a) device");
+    return MKV_OK;
+}
+
+int num_sms() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    return sms;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// cache object
+// ---------------------------------------------------------------------------
+struct Plan {
+    uint64_t hash = 0;
+    int total = 0, chunk = 0, grid = 0;
+    int32_t* d_pref = nullptr;
+};
+
+struct mkv_cache {
+    int n_units = 0, d = 0, n_r = 0, gs = 0, max_decode = 0;
+    bool shadow = false;
+    // host mirror
+    std::vector<int64_t> page_base;
+    std::vector<int32_t> cap_pages, n_pages, n_prefill, n_res, n_blocks;
+    int64_t total_pages = 0;
+    // device
+    UnitMeta* d_meta = nullptr;
+    uint8_t* d_pool = nullptr;
+    float* d_shadow = nullptr;
+    __half* d_res_k = nullptr;
+    __half* d_res_v = nullptr;
+    uint32_t* d_status = nullptr;
+    int* d_counters = nullptr;
+    float* d_res_ml = nullptr;
+    float* d_res_o = nullptr;
+    float* d_part_ml = nullptr;
+    float* d_part_o = nullptr;
+    int part_slots = 0;
+    std::unordered_map<uint64_t, Plan> plans;  // key: (unit_begin, n_units)
+
+    ~mkv_cache() {
+        for (auto& kv : plans) cudaFree(kv.second.d_pref);
+        cudaFree(d_meta); cudaFree(d_pool); cudaFree(d_shadow); cudaFree(d_res_k); cudaFree(d_res_v);
+        cudaFree(d_status); cudaFree(d_counters); cudaFree(d_res_ml); cudaFree(d_res_o);
+        cudaFree(d_part_ml); cudaFree(d_part_o);
+    }
+
+    UnitMeta meta_of(int u) const {
+        UnitMeta m;
+        m.page_base = page_base[u];
+        m.n_pages = n_pages[u];
+        m.n_prefill = n_prefill[u];
+        m.n_res = n_res[u];
+        m.cap_pages = cap_pages[u];
+        return m;
+    }
+    cudaError_t upload_meta(int ub, int n, cudaStream_t s) {
+        std::vector<UnitMeta> h(n);
+        for (int i = 0; i < n; ++i) h[i] = meta_of(ub + i);
+        // pageable source: the copy is staged before return, so the host vector may die.
+        return cudaMemcpyAsync(d_meta + ub, h.data(), sizeof(UnitMeta) * n, cudaMemcpyHostToDevice, s);
+    }
+};
+
+extern "C" {
+
+const char* mkv_last_error(void) { return g_err.c_str(); }
+int mkv_abi_version(void) { return MKV_ABI_VERSION; }
+
+int mkv_device_check(int device) {
+    cudaDeviceProp prop;
+    cudaError_t e = cudaGetDeviceProperties(&prop, device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceProperties");
+    if (!(prop.major == 10 && prop.minor == 0))
+        return fail(MKV_ERR_UNSUPPORTED, "device %d is sm_%d%d, kernels are built for sm_100a", device,
+                    prop.major, prop.minor);
+    return MKV_OK;
+}
+
+// ---------------------------------------------------------------------------
+// host allocation helpers (selection.cpp:48-83, exact double arithmetic)
+// ---------------------------------------------------------------------------
+int mkv_allocate_uniform(size_t total_hh, size_t layers, int64_t* out) {
+    if (layers < 1) return fail(MKV_ERR_INVALID_ARGUMENT, "allocate_uniform: layers must be >= 1");
+    for (size_t i = 0; i < layers; ++i) out[i] = static_cast<int64_t>(total_hh / layers);
+    for (size_t i = 0; i < total_hh % layers; ++i) ++out[i];
+    return MKV_OK;
+}
+
+int mkv_allocate_pyramid(size_t mean_x, size_t layers, size_t depth, int bottom_heavy, int64_t* out) {
+    if (layers < 1) return fail(MKV_ERR_INVALID_ARGUMENT, "allocate_pyramid: layers must be >= 1");
+    if (depth < 1) return fail(MKV_ERR_INVALID_ARGUMENT, "allocate_pyramid: depth must be >= 1");
+    const double x = static_cast<double>(mean_x);
+    const double small_end = x / static_cast<double>(depth);
+    const double large_end = 2.0 * x - small_end;
+    const double first = bottom_heavy ? large_end : small_end;
+    const double last = bottom_heavy ? small_end : large_end;
+    for (size_t i = 0; i < layers; ++i) {
+        const double t = (layers == 1) ? 0.0 : static_cast<double>(i) / static_cast<double>(layers - 1);
+        volatile double span = (last - first) * t;  // no contraction into an FMA
+        const double v = first + span;
+        out[i] = static_cast<int64_t>(std::llround(std::max(v, 0.0)));
+    }
+    return MKV_OK;
+}
+
+// ---------------------------------------------------------------------------
+// K1 prefill attention
+// ---------------------------------------------------------------------------
+int mkv_prefill_attn(const mkv_prefill_args* a, void* stream) {
+    if (!a) return fail(MKV_ERR_INVALID_ARGUMENT, "attention: null args");
+    if (a->len_q <= 0 || a->len_k <= 0) return fail(MKV_ERR_INVALID_ARGUMENT, "attention: zero-length sequence");
+    if (a->causal && a->len_q > a->len_k)
+        return fail(MKV_ERR_INVALID_ARGUMENT, "attention: causal requires l_query <= l_key");
+    if (a->head_dim != 128) return fail(MKV_ERR_UNSUPPORTED, "attention: head_dim %d (device kernel: 128)", a->head_dim);
+    if (a->batch <= 0 || a->n_q_heads <= 0 || a->n_kv_heads <= 0 || a->n_q_heads % a->n_kv_heads)
+        return fail(MKV_ERR_INVALID_ARGUMENT, "attention: bad head counts (Hq %d, Hkv %d)", a->n_q_heads, a->n_kv_heads);
+    if (!a->q || !a->k || !a->v || !a->out || !a->lse || !a->a_cumul)
+        return fail(MKV_ERR_INVALID_ARGUMENT, "attention: null tensor");
+    if (!aligned16(a->q) || !aligned16(a->k) || !aligned16(a->v) || !aligned16(a->out) ||
+        (a->q_st % 8) || (a->k_st % 8) || (a->v_st % 8) || (a->o_st % 8) || (a->q_sh % 8) ||
+        (a->k_sh % 8) || (a->v_sh % 8) || (a->o_sh % 8) || (a->q_sb % 8) || (a->k_sb % 8) ||
+        (a->v_sb % 8) || (a->o_sb % 8))
+        return fail(MKV_ERR_INVALID_ARGUMENT, "attention: rows must be 16-byte aligned");
+    if (int r = require_device()) return r;
+    PrefillAttnParams p;
+    p.q = static_cast<const __half*>(a->q); p.q_sb = a->q_sb; p.q_sh = a->q_sh; p.q_st = a->q_st;
+    p.k = static_cast<const __half*>(a->k); p.k_sb = a->k_sb; p.k_sh = a->k_sh; p.k_st = a->k_st;
+    p.v = static_cast<const __half*>(a->v); p.v_sb = a->v_sb; p.v_sh = a->v_sh; p.v_st = a->v_st;
+    p.out = static_cast<__half*>(a->out); p.o_sb = a->o_sb; p.o_sh = a->o_sh; p.o_st = a->o_st;
+    p.lse = a->lse; p.a_cumul = a->a_cumul;
+    p.batch = a->batch; p.hq = a->n_q_heads; p.hkv = a->n_kv_heads; p.lq = a->len_q; p.lk = a->len_k;
+    p.scale = a->scale; p.causal = a->causal;
+    CK(launch_prefill_attn(p, static_cast<cudaStream_t>(stream)));
+    return MKV_OK;
+}
+
+// ---------------------------------------------------------------------------
+// K2 selection
+// ---------------------------------------------------------------------------
+static int do_select(const float* a_cumul, int64_t a_stride, int n_units, int length, const int32_t* hh_host,
+                     int rw, int32_t* kept, int64_t kept_stride, int32_t* n_kept, cudaStream_t s) {
+    int32_t* d_hh = nullptr;
+    CK(cudaMallocAsync(&d_hh, sizeof(int32_t) * n_units, s));
+    CK(cudaMemcpyAsync(d_hh, hh_host, sizeof(int32_t) * n_units, cudaMemcpyHostToDevice, s));
+    SelectParams p{a_cumul, a_stride, n_units, length, d_hh, rw, kept, kept_stride, n_kept};
+    cudaError_t e = launch_select(p, s);
+    cudaFreeAsync(d_hh, s);
+    if (e != cudaSuccess) return cuda_fail(e, "select kernel");
+    return MKV_OK;
+}
+
+int mkv_select(const mkv_select_args* a, void* stream) {
+    if (!a) return fail(MKV_ERR_INVALID_ARGUMENT, "select: null args");
+    if (a->n_units < 0 || a->length < 0 || a->rw_count < 0 || !a->hh_count)
+        return fail(MKV_ERR_INVALID_ARGUMENT, "select: negative budget");
+    for (int u = 0; u < a->n_units; ++u)
+        if (a->hh_count[u] < 0) return fail(MKV_ERR_INVALID_ARGUMENT, "select_tokens: negative budget");
+    if (a->n_units == 0) return MKV_OK;
+    if (!a->a_cumul || !a->kept) return fail(MKV_ERR_INVALID_ARGUMENT, "select: null tensor");
+    if (a->kept_stride < std::min<int64_t>(a->length, 1))
+        return fail(MKV_ERR_INVALID_ARGUMENT, "select: kept_stride < length");
+    if (int r = require_device()) return r;
+    return do_select(a->a_cumul, a->a_stride, a->n_units, a->length, a->hh_count, a->rw_count, a->kept,
+                     a->kept_stride, a->n_kept, static_cast<cudaStream_t>(stream));
+}
+
+// ---------------------------------------------------------------------------
+// cache lifecycle
+// ---------------------------------------------------------------------------
+int mkv_cache_create(const mkv_cache_config* cfg, mkv_cache** out) {
+    if (!cfg || !out) return fail(MKV_ERR_INVALID_ARGUMENT, "make_cache: null argument");
+    if (cfg->head_dim < 1) return fail(MKV_ERR_INVALID_ARGUMENT, "make_cache: d must be >= 1");
+    if (cfg->group_size < 1 || cfg->n_r <= 0 || cfg->n_r % cfg->group_size != 0)
+        return fail(MKV_ERR_INVALID_ARGUMENT, "make_cache: n_r must be a positive multiple of group_size");
+    if (cfg->head_dim != kHeadDim) return fail(MKV_ERR_UNSUPPORTED, "make_cache: head_dim %d (device cache: 128)", cfg->head_dim);
+    if (cfg->group_size != kGroup) return fail(MKV_ERR_UNSUPPORTED, "make_cache: group_size %d (device cache: 16)", cfg->group_size);
+    if (cfg->n_r > 128) return fail(MKV_ERR_UNSUPPORTED, "make_cache: n_r %d > 128", cfg->n_r);
+    if (cfg->n_units <= 0 || !cfg->prefill_capacity || cfg->max_decode_tokens < 0)
+        return fail(MKV_ERR_INVALID_ARGUMENT, "make_cache: bad unit configuration");
+    if (int r = require_device()) return r;
+    auto* c = new mkv_cache;
+    c->n_units = cfg->n_units;
+    c->d = cfg->head_dim;
+    c->n_r = cfg->n_r;
+    c->gs = cfg->group_size;
+    c->max_decode = cfg->max_decode_tokens;
+    c->shadow = cfg->keep_fp32_params != 0;
+    const int n = c->n_units;
+    c->page_base.resize(n);
+    c->cap_pages.resize(n);
+    c->n_pages.assign(n, 0);
+    c->n_prefill.assign(n, 0);
+    c->n_res.assign(n, 0);
+    c->n_blocks.assign(n, 0);
+    const int flush_pages = ((cfg->max_decode_tokens + c->n_r - 1) / c->n_r) * (c->n_r / kGroup);
+    int64_t acc = 0;
+    for (int u = 0; u < n; ++u) {
+        if (cfg->prefill_capacity[u] < 0) {
+            delete c;
+            return fail(MKV_ERR_INVALID_ARGUMENT, "make_cache: negative capacity");
+        }
+        c->page_base[u] = acc;
+        c->cap_pages[u] = (cfg->prefill_capacity[u] + kGroup - 1) / kGroup + flush_pages;
+        acc += c->cap_pages[u];
+    }
+    c->total_pages = acc;
+    c->part_slots = num_sms() * kPagesWarps + n;
+    auto al = [&](void** p, size_t bytes) -> cudaError_t { return cudaMalloc(p, std::max<size_t>(bytes, 16)); };
+    cudaError_t e = cudaSuccess;
+    if (e == cudaSuccess) e = al((void**)&c->d_meta, sizeof(UnitMeta) * n);
+    if (e == cudaSuccess) e = al((void**)&c->d_pool, (size_t)acc * kPageBytes);
+    if (e == cudaSuccess && c->shadow) e = al((void**)&c->d_shadow, (size_t)acc * kShadowBytes);
+    if (e == cudaSuccess) e = al((void**)&c->d_res_k, (size_t)n * c->n_r * c->d * sizeof(__half));
+    if (e == cudaSuccess) e = al((void**)&c->d_res_v, (size_t)n * c->n_r * c->d * sizeof(__half));
+    if (e == cudaSuccess) e = al((void**)&c->d_status, sizeof(uint32_t));
+    if (e == cudaSuccess) e = al((void**)&c->d_counters, sizeof(int) * n);
+    if (e == cudaSuccess) e = al((void**)&c->d_res_ml, sizeof(float) * 2 * kMaxG * n);
+    if (e == cudaSuccess) e = al((void**)&c->d_res_o, sizeof(float) * kMaxG * kHeadDim * n);
+    if (e == cudaSuccess) e = al((void**)&c->d_part_ml, sizeof(float) * 2 * kMaxG * c->part_slots);
+    if (e == cudaSuccess) e = al((void**)&c->d_part_o, sizeof(float) * kMaxG * kHeadDim * c->part_slots);
+    if (e == cudaSuccess) e = cudaMemset(c->d_status, 0, sizeof(uint32_t));
+    if (e == cudaSuccess) e = cudaMemset(c->d_counters, 0, sizeof(int) * n);
+    if (e == cudaSuccess) e = cudaMemset(c->d_pool, 0, (size_t)acc * kPageBytes);
+    if (e == cudaSuccess) e = c->upload_meta(0, n, 0);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+        delete c;
+        return cuda_fail(e, "make_cache: device allocation");
+    }
+    *out = c;
+    return MKV_OK;
+}
+
+int mkv_cache_destroy(mkv_cache* c) {
+    if (c) {
+        cudaDeviceSynchronize();
+        delete c;
+    }
+    return MKV_OK;
+}
+
+int mkv_cache_bytes(const mkv_cache* c, uint64_t* page_bytes, uint64_t* residual_bytes, uint64_t* total) {
+    if (!c) return fail(MKV_ERR_INVALID_ARGUMENT, "cache: null handle");
+    const uint64_t pb = (uint64_t)c->total_pages * kPageBytes;
+    const uint64_t rb = (uint64_t)c->n_units * c->n_r * c->d * 2 * 2;
+    if (page_bytes) *page_bytes = pb;
+    if (residual_bytes) *residual_bytes = rb;
+    if (total) *total = pb + rb + (c->shadow ? (uint64_t)c->total_pages * kShadowBytes : 0) +
+                        (uint64_t)c->part_slots * kMaxG * (kHeadDim + 2) * 4;
+    return MKV_OK;
+}
+
+int mkv_cache_unit_info(const mkv_cache* c, int u, int64_t* tq, int64_t* tr, int64_t* np, int64_t* nb) {
+    if (!c) return fail(MKV_ERR_INVALID_ARGUMENT, "cache: null handle");
+    if (u < 0 || u >= c->n_units) return fail(MKV_ERR_OUT_OF_RANGE, "cache: unit %d out of range", u);
+    if (tq) *tq = c->n_prefill[u] + (int64_t)(c->n_blocks[u] > 0 ? c->n_blocks[u] - 1 : 0) * c->n_r;
+    if (tr) *tr = c->n_res[u];
+    if (np) *np = c->n_pages[u];
+    if (nb) *nb = c->n_blocks[u];
+    return MKV_OK;
+}
+
+static int check_range(const mkv_cache* c, int ub, int n) {
+    if (!c) return fail(MKV_ERR_INVALID_ARGUMENT, "cache: null handle");
+    if (ub < 0 || n < 0 || ub + n > c->n_units)
+        return fail(MKV_ERR_OUT_OF_RANGE, "cache: units [%d, %d) outside [0, %d)", ub, ub + n, c->n_units);
+    return MKV_OK;
+}
+
+// ---------------------------------------------------------------------------
+// K3 prefill quantize + pack
+// ---------------------------------------------------------------------------
+static int prefill_pages_impl(mkv_cache* c, int ub, int n, const void* k, int64_t k_su, int64_t k_st,
+                              const void* v, int64_t v_su, int64_t v_st, const int32_t* kept,
+                              int64_t kept_stride, const int32_t* n_kept, cudaStream_t s) {
+    int max_pages = 0;
+    for (int i = 0; i < n; ++i) {
+        const int u = ub + i;
+        if (n_kept[i] <= 0) return fail(MKV_ERR_INVALID_ARGUMENT, "append_block: empty block (unit %d)", u);
+        const int pages = (n_kept[i] + kGroup - 1) / kGroup;
+        if (pages > c->cap_pages[u])
+            return fail(MKV_ERR_OUT_OF_RANGE, "prefill: unit %d keeps %d tokens > capacity", u, n_kept[i]);
+        max_pages = std::max(max_pages, pages);
+    }
+    for (int i = 0; i < n; ++i) {  // make_cache + store_block (cache_engine.cpp:70-74)
+        const int u = ub + i;
+        c->n_prefill[u] = n_kept[i];
+        c->n_pages[u] = (n_kept[i] + kGroup - 1) / kGroup;
+        c->n_res[u] = 0;
+        c->n_blocks[u] = 1;
+    }
+    CK(c->upload_meta(ub, n, s));
+    PrefillPagesParams p;
+    p.k = static_cast<const __half*>(k); p.k_su = k_su; p.k_st = k_st;
+    p.v = static_cast<const __half*>(v); p.v_su = v_su; p.v_st = v_st;
+    p.kept = kept; p.kept_stride = kept_stride;
+    p.meta = c->d_meta; p.unit_begin = ub; p.n_units = n; p.max_pages = max_pages;
+    p.pool = c->d_pool; p.shadow = c->d_shadow; p.status = c->d_status;
+    CK(launch_prefill_pages(p, s));
+    return MKV_OK;
+}
+
+int mkv_cache_prefill(mkv_cache* c, const mkv_cache_prefill_args* a, void* stream) {
+    if (!a) return fail(MKV_ERR_INVALID_ARGUMENT, "prefill: null args");
+    if (int r = check_range(c, a->unit_begin, a->n_units)) return r;
+    if (a->n_units == 0) return MKV_OK;
+    if (!a->k || !a->v || !a->kept || !a->n_kept_host) return fail(MKV_ERR_INVALID_ARGUMENT, "prefill: null tensor");
+    if (!aligned16(a->k) || !aligned16(a->v) || (a->k_st % 8) || (a->v_st % 8) || (a->k_su % 8) || (a->v_su % 8))
+        return fail(MKV_ERR_INVALID_ARGUMENT, "prefill: K/V rows must be 16-byte aligned");
+    if (int r = require_device()) return r;
+    return prefill_pages_impl(c, a->unit_begin, a->n_units, a->k, a->k_su, a->k_st, a->v, a->v_su, a->v_st,
+                              a->kept, a->kept_stride, a->n_kept_host, static_cast<cudaStream_t>(stream));
+}
+
+int mkv_cache_prefill_select(mkv_cache* c, const mkv_prefill_select_args* a, void* stream) {
+    if (!a) return fail(MKV_ERR_INVALID_ARGUMENT, "prefill: null args");
+    if (int r = check_range(c, a->unit_begin, a->n_units)) return r;
+    if (a->n_units == 0) return MKV_OK;
+    if (!a->a_cumul || !a->k || !a->v || !a->hh_count) return fail(MKV_ERR_INVALID_ARGUMENT, "prefill: null tensor");
+    if (a->length < 0 || a->rw_count < 0) return fail(MKV_ERR_INVALID_ARGUMENT, "prefill: k/v/a_cumul length mismatch");
+    std::vector<int32_t> n_kept(a->n_units);
+    for (int i = 0; i < a->n_units; ++i) {
+        if (a->hh_count[i] < 0) return fail(MKV_ERR_INVALID_ARGUMENT, "prefill: negative budget");
+        if ((int64_t)a->hh_count[i] + a->rw_count == 0) return fail(MKV_ERR_RUNTIME, "prefill: zero kept tokens");
+        n_kept[i] = (int32_t)std::min<int64_t>((int64_t)a->hh_count[i] + a->rw_count, a->length);
+    }
+    if (!aligned16(a->k) || !aligned16(a->v) || (a->k_st % 8) || (a->v_st % 8) || (a->k_su % 8) || (a->v_su % 8))
+        return fail(MKV_ERR_INVALID_ARGUMENT, "prefill: K/V rows must be 16-byte aligned");
+    if (int r = require_device()) return r;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int32_t* kept = nullptr;
+    const int64_t ks = std::max(a->length, 1);
+    CK(cudaMallocAsync(&kept, sizeof(int32_t) * ks * a->n_units, s));
+    int r = do_select(a->a_cumul, a->a_stride, a->n_units, a->length, a->hh_count, a->rw_count, kept, ks,
+                      nullptr, s);
+    if (r == MKV_OK)
+        r = prefill_pages_impl(c, a->unit_begin, a->n_units, a->k, a->k_su, a->k_st, a->v, a->v_su, a->v_st, kept,
+                               ks, n_kept.data(), s);
+    cudaFreeAsync(kept, s);
+    return r;
+}
+
+// ---------------------------------------------------------------------------
+// K4 decode
+// ---------------------------------------------------------------------------
+static uint64_t range_hash(const mkv_cache* c, int ub, int n) {
+    uint64_t h = 1469598103934665603ull;
+    for (int i = 0; i < n; ++i) {
+        h ^= (uint64_t)(uint32_t)c->n_pages[ub + i];
+        h *= 1099511628211ull;
+    }
+    return h;
+}
+
+static int get_plan(mkv_cache* c, int ub, int n, cudaStream_t s, Plan** out) {
+    const uint64_t key = ((uint64_t)(uint32_t)ub << 32) | (uint32_t)n;
+    Plan& pl = c->plans[key];
+    const uint64_t h = range_hash(c, ub, n);
+    if (pl.d_pref && pl.hash == h) {
+        *out = &pl;
+        return MKV_OK;
+    }
+    std::vector<int32_t> pref(n + 1);
+    pref[0] = 0;
+    for (int i = 0; i < n; ++i) pref[i + 1] = pref[i] + c->n_pages[ub + i];
+    const int total = pref[n];
+    const int max_warps = num_sms() * kPagesWarps;
+    const int min_chunk = 4;
+    int chunk = std::max(min_chunk, (total + max_warps - 1) / std::max(max_warps, 1));
+    const int warps = total > 0 ? (total + chunk - 1) / chunk : 0;
+    if (!pl.d_pref) CK(cudaMalloc(&pl.d_pref, sizeof(int32_t) * (c->n_units + 1)));
+    CK(cudaMemcpyAsync(pl.d_pref, pref.data(), sizeof(int32_t) * (n + 1), cudaMemcpyHostToDevice, s));
+    pl.hash = h;
+    pl.total = total;
+    pl.chunk = chunk;
+    pl.grid = (warps + kPagesWarps - 1) / kPagesWarps;
+    *out = &pl;
+    return MKV_OK;
+}
+
+static int decode_impl(mkv_cache* c, const mkv_decode_args* a, bool attend, cudaStream_t s) {
+    const int ub = a->unit_begin, n = a->n_units;
+    if (int r = check_range(c, ub, n)) return r;
+    if (n == 0) return MKV_OK;
+    const bool append = a->k_new != nullptr;
+    if (append && !a->v_new) return fail(MKV_ERR_INVALID_ARGUMENT, "decode_append: null v");
+    if (attend) {
+        if (a->group < 1 || a->group > kMaxG) return fail(MKV_ERR_UNSUPPORTED, "decode: group %d outside 1..8", a->group);
+        if (!a->q || !a->out) return fail(MKV_ERR_INVALID_ARGUMENT, "decode: null q/out");
+        if (!aligned16(a->q) || !aligned16(a->out)) return fail(MKV_ERR_INVALID_ARGUMENT, "decode: q/out must be 16-byte aligned");
+    }
+    if (append && (!aligned16(a->k_new) || !aligned16(a->v_new)))
+        return fail(MKV_ERR_INVALID_ARGUMENT, "decode_append: k/v must be 16-byte aligned");
+    // validate everything before mutating the mirror
+    for (int i = 0; i < n; ++i) {
+        const int u = ub + i;
+        const int64_t total = (int64_t)c->n_pages[u] + c->n_res[u];
+        if (attend && total == 0) return fail(MKV_ERR_RUNTIME, "decode_step: empty cache (unit %d)", u);
+        if (append && c->n_res[u] + 1 == c->n_r && c->n_pages[u] + c->n_r / kGroup > c->cap_pages[u])
+            return fail(MKV_ERR_OUT_OF_RANGE, "decode: unit %d exceeds max_decode_tokens", u);
+    }
+    if (int r = require_device()) return r;
+    if (append) {
+        for (int i = 0; i < n; ++i) {
+            const int u = ub + i;
+            if (++c->n_res[u] == c->n_r) {
+                c->n_res[u] = 0;
+                c->n_pages[u] += c->n_r / kGroup;
+                c->n_blocks[u] += 1;
+            }
+        }
+    }
+    ResidualParams rp;
+    rp.meta = c->d_meta; rp.unit_begin = ub; rp.n_units = n; rp.group = a->group; rp.n_r = c->n_r;
+    rp.q = static_cast<const __half*>(a->q);
+    rp.k_new = static_cast<const __half*>(a->k_new);
+    rp.v_new = static_cast<const __half*>(a->v_new);
+    rp.res_k = c->d_res_k; rp.res_v = c->d_res_v; rp.pool = c->d_pool; rp.shadow = c->d_shadow;
+    rp.res_ml = c->d_res_ml; rp.res_o = c->d_res_o; rp.out = static_cast<__half*>(a->out);
+    rp.scale_log2 = a->scale * 1.4426950408889634f;
+    rp.attend = attend ? 1 : 0;
+    rp.status = c->d_status;
+    CK(launch_residual(rp, s));
+    if (!attend) return MKV_OK;
+    Plan* pl = nullptr;
+    if (int r = get_plan(c, ub, n, s, &pl)) return r;
+    if (pl->total == 0) return MKV_OK;  // residual-only units were finished by the residual kernel
+    PagesParams pp;
+    pp.pool = c->d_pool; pp.meta = c->d_meta; pp.unit_begin = ub; pp.n_units = n; pp.group = a->group;
+    pp.q = static_cast<const __half*>(a->q);
+    pp.pref = pl->d_pref; pp.chunk = pl->chunk; pp.total_pages = pl->total; pp.n_warps = pl->grid * kPagesWarps;
+    pp.part_ml = c->d_part_ml; pp.part_o = c->d_part_o; pp.res_ml = c->d_res_ml; pp.res_o = c->d_res_o;
+    pp.counters = c->d_counters; pp.out = static_cast<__half*>(a->out); pp.scale_log2 = rp.scale_log2;
+    CK(launch_pages(pp, pl->grid, s));
+    return MKV_OK;
+}
+
+int mkv_decode_step(mkv_cache* c, const mkv_decode_args* a, void* stream) {
+    if (!a) return fail(MKV_ERR_INVALID_ARGUMENT, "decode_step: null args");
+    return decode_impl(c, a, true, static_cast<cudaStream_t>(stream));
+}
+
+int mkv_decode_step_layers(mkv_cache* c, int n_layers, const mkv_decode_args* a, void* stream) {
+    if (!a || n_layers < 0) return fail(MKV_ERR_INVALID_ARGUMENT, "decode_step: bad layer list");
+    for (int l = 0; l < n_layers; ++l)
+        if (int r = decode_impl(c, a + l, true, static_cast<cudaStream_t>(stream))) return r;
+    return MKV_OK;
+}
+
+int mkv_cache_append(mkv_cache* c, int ub, int n, const void* k_new, const void* v_new, void* stream) {
+    if (!k_new || !v_new) return fail(MKV_ERR_INVALID_ARGUMENT, "decode_append: null token");
+    mkv_decode_args a{};
+    a.unit_begin = ub; a.n_units = n; a.group = 1; a.k_new = k_new; a.v_new = v_new;
+    return decode_impl(c, &a, false, static_cast<cudaStream_t>(stream));
+}
+
+// ---------------------------------------------------------------------------
+// export to the reference QuantizedTensor format (quantizer.hpp:30-42)
+// ---------------------------------------------------------------------------
+static void block_list(const mkv_cache* c, int u, std::vector<int>& rows) {
+    rows.clear();
+    if (c->n_blocks[u] == 0) return;
+    rows.push_back(c->n_prefill[u]);
+    for (int b = 1; b < c->n_blocks[u]; ++b) rows.push_back(c->n_r);
+}
+
+int mkv_cache_export_sizes(const mkv_cache* c, int u, int which, int64_t* n_words, int64_t* n_params,
+                           int64_t* n_blocks) {
+    if (int r = check_range(c, u, 1)) return r;
+    std::vector<int> rows;
+    block_list(c, u, rows);
+    int64_t codes = 0, params = 0;
+    for (int R : rows) {
+        codes += (int64_t)R * c->d;
+        params += which == 0 ? (int64_t)c->d * ((R + c->gs - 1) / c->gs) : (int64_t)R * (c->d / c->gs);
+    }
+    if (n_words) *n_words = (codes + 15) / 16;
+    if (n_params) *n_params = params;
+    if (n_blocks) *n_blocks = (int64_t)rows.size();
+    return MKV_OK;
+}
+
+int mkv_cache_export_reference(const mkv_cache* c, int u, int which, uint32_t* words, float* params,
+                               int64_t* block_rows) {
+    if (int r = check_range(c, u, 1)) return r;
+    if (which != 0 && which != 1) return fail(MKV_ERR_INVALID_ARGUMENT, "export: which must be 0 or 1");
+    CK(cudaDeviceSynchronize());
+    const int np = c->n_pages[u];
+    std::vector<uint8_t> pages((size_t)np * kPageBytes);
+    std::vector<float> shadow;
+    if (np) CK(cudaMemcpy(pages.data(), c->d_pool + (size_t)c->page_base[u] * kPageBytes, pages.size(), cudaMemcpyDeviceToHost));
+    if (c->shadow && np) {
+        shadow.resize((size_t)np * kShadowBytes / 4);
+        CK(cudaMemcpy(shadow.data(), c->d_shadow + (size_t)c->page_base[u] * (kShadowBytes / 4),
+                      shadow.size() * 4, cudaMemcpyDeviceToHost));
+    }
+    std::vector<int> rows;
+    block_list(c, u, rows);
+    auto half_to_float = [](uint16_t h) { __half_raw r; r.x = h; return __half2float(__half(r)); };
+    auto code_of = [&](int pg, int t, int ch) -> uint32_t {
+        const uint8_t* page = pages.data() + (size_t)pg * kPageBytes;
+        const CodePos cp = which == 0 ? k_code_pos(t, ch) : v_code_pos(t, ch);
+        const uint32_t* w = reinterpret_cast<const uint32_t*>(page + (which == 0 ? kKC : kVC));
+        return (w[cp.word] >> cp.shift) & 3u;
+    };
+    auto param_of = [&](int pg, int t, int ch, float* sc, float* zp) {
+        const uint8_t* page = pages.data() + (size_t)pg * kPageBytes;
+        if (!shadow.empty()) {
+            const float* sh = shadow.data() + (size_t)pg * (kShadowBytes / 4);
+            if (which == 0) { *sc = sh[2 * ch]; *zp = sh[2 * ch + 1]; }
+            else { const int g = ch / 16; *sc = sh[256 + 2 * (t * 8 + g)]; *zp = sh[256 + 2 * (t * 8 + g) + 1]; }
+            return;
+        }
+        const uint16_t* hs;
+        if (which == 0) {
+            hs = reinterpret_cast<const uint16_t*>(page + kKS);
+            *sc = half_to_float(hs[k_param_idx(ch)]);
+            *zp = half_to_float(reinterpret_cast<const uint16_t*>(page + kKZ)[k_param_idx(ch)]);
+        } else {
+            const int g = ch / 16;
+            *sc = half_to_float(reinterpret_cast<const uint16_t*>(page + kVS)[vs_param_idx(t, g)]);
+            *zp = half_to_float(reinterpret_cast<const uint16_t*>(page + kVZ)[vz_param_idx(t, g)]);
+        }
+    };
+    int64_t code_idx = 0, group_idx = 0;
+    int64_t nw = 0;
+    mkv_cache_export_sizes(c, u, which, &nw, nullptr, nullptr);
+    if (words) std::fill(words, words + nw, 0u);
+    auto push = [&](uint32_t code) {
+        if (words) words[code_idx / 16] |= code << (2 * (code_idx % 16));
+        ++code_idx;
+    };
+    int page0 = 0;
+    const int d = c->d;
+    for (size_t b = 0; b < rows.size(); ++b) {
+        const int R = rows[b];
+        if (which == 0) {  // PerChannel: for channel, for token group
+            for (int ch = 0; ch < d; ++ch) {
+                for (int g0 = 0; g0 < R; g0 += 16) {
+                    const int glen = std::min(16, R - g0), pg = page0 + g0 / 16;
+                    float sc, zp;
+                    param_of(pg, 0, ch, &sc, &zp);
+                    if (params) { params[2 * group_idx] = sc; params[2 * group_idx + 1] = zp; }
+                    ++group_idx;
+                    for (int t = 0; t < glen; ++t) push(code_of(pg, t, ch));
+                }
+            }
+        } else {  // PerToken: for token, for channel group
+            for (int r = 0; r < R; ++r) {
+                const int pg = page0 + r / 16, t = r % 16;
+                for (int g0 = 0; g0 < d; g0 += 16) {
+                    float sc, zp;
+                    param_of(pg, t, g0, &sc, &zp);
+                    if (params) { params[2 * group_idx] = sc; params[2 * group_idx + 1] = zp; }
+                    ++group_idx;
+                    for (int ch = g0; ch < g0 + 16; ++ch) push(code_of(pg, t, ch));
+                }
+            }
+        }
+        if (block_rows) block_rows[b] = R;
+        page0 += (R + 15) / 16;
+    }
+    return MKV_OK;
+}
+
+int mkv_cache_export_residual(const mkv_cache* c, int u, uint16_t* rk, uint16_t* rv) {
+    if (int r = check_range(c, u, 1)) return r;
+    CK(cudaDeviceSynchronize());
+    const size_t bytes = (size_t)c->n_res[u] * c->d * sizeof(__half);
+    if (bytes) {
+        CK(cudaMemcpy(rk, c->d_res_k + (size_t)u * c->n_r * c->d, bytes, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(rv, c->d_res_v + (size_t)u * c->n_r * c->d, bytes, cudaMemcpyDeviceToHost));
+    }
+    return MKV_OK;
+}
+
+int mkv_cache_check(mkv_cache* c) {
+    if (!c) return fail(MKV_ERR_INVALID_ARGUMENT, "cache: null handle");
+    CK(cudaDeviceSynchronize());
+    uint32_t st = 0;
+    CK(cudaMemcpy(&st, c->d_status, sizeof(st), cudaMemcpyDeviceToHost));
+    if (st) {
+        CK(cudaMemset(c->d_status, 0, sizeof(uint32_t)));
+        if (st & kStatusNonFinite) return fail(MKV_ERR_DOMAIN, "quantize_group: non-finite input");
+    }
+    return MKV_OK;
+}
+
+// ---------------------------------------------------------------------------
+// synthetic inputs
+// ---------------------------------------------------------------------------
+int mkv_synth_fp16(void* out, int64_t n, uint64_t seed, uint64_t stream_id, void* stream) {
+    if (!out || n < 0) return fail(MKV_ERR_INVALID_ARGUMENT, "synth: bad args");
+    if (int r = require_device()) return r;
+    CK(launch_synth_fp16(static_cast<__half*>(out), 1, n, n, seed, stream_id, 0, static_cast<cudaStream_t>(stream)));
+    return MKV_OK;
+}
+
+int mkv_synth_fp16_rows(void* out, int64_t n_rows, int64_t row_len, int64_t ld, uint64_t seed, uint64_t base,
+                        uint64_t step, void* stream) {
+    if (!out || n_rows < 0 || row_len < 0 || ld < row_len) return fail(MKV_ERR_INVALID_ARGUMENT, "synth: bad args");
+    if (int r = require_device()) return r;
+    CK(launch_synth_fp16(static_cast<__half*>(out), n_rows, row_len, ld, seed, base, step,
+                         static_cast<cudaStream_t>(stream)));
+    return MKV_OK;
+}
+
+int mkv_synth_uniform_f32(float* out, int64_t n_rows, int64_t row_len, int64_t ld, uint64_t seed, uint64_t base,
+                          uint64_t step, void* stream) {
+    if (!out || n_rows < 0 || row_len < 0 || ld < row_len) return fail(MKV_ERR_INVALID_ARGUMENT, "synth: bad args");
+    if (int r = require_device()) return r;
+    CK(launch_synth_uniform(out, n_rows, row_len, ld, seed, base, step, static_cast<cudaStream_t>(stream)));
+    return MKV_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,107 @@
+// mkv_kernels.h -- host-side launch interface between the C ABI (capi.cu) and
+// the kernel translation units.  Internal; not part of the public ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "mkv_common.cuh"
+
+namespace mkv {
+
+constexpr int kMaxG = 8;  // q-heads per kv-head handled by one mma N=8 tile
+
+// ---- K3: prefill pages (quant_pack.cu) ----
+struct PrefillPagesParams {
+    const __half* k;
+    int64_t k_su, k_st;
+    const __half* v;
+    int64_t v_su, v_st;
+    const int32_t* kept;
+    int64_t kept_stride;
+    UnitMeta* meta;     // global unit meta array
+    int unit_begin, n_units, max_pages;
+    uint8_t* pool;
+    float* shadow;      // may be null
+    uint32_t* status;
+};
+cudaError_t launch_prefill_pages(const PrefillPagesParams& p, cudaStream_t s);
+
+// ---- K2: selection (select.cu) ----
+struct SelectParams {
+    const float* a;
+    int64_t a_stride;
+    int n_units, length;
+    const int32_t* hh;  // device [n_units]
+    int rw;
+    int32_t* kept;
+    int64_t kept_stride;
+    int32_t* n_kept;    // may be null
+};
+cudaError_t launch_select(const SelectParams& p, cudaStream_t s);
+
+// ---- K4: decode (decode.cu) ----
+struct ResidualParams {
+    UnitMeta* meta;
+    int unit_begin, n_units, group, n_r;
+    const __half* q;      // [n_units][G][d]
+    const __half* k_new;  // [n_units][d] or null (no append)
+    const __half* v_new;
+    __half* res_k;        // [total_units][n_r][d]
+    __half* res_v;
+    uint8_t* pool;
+    float* shadow;
+    float* res_ml;        // [n_units][2][kMaxG]  (local unit index)
+    float* res_o;         // [n_units][kMaxG][d]
+    __half* out;          // final output when a unit has no pages
+    float scale_log2;
+    int attend;           // 0: append only
+    uint32_t* status;
+};
+cudaError_t launch_residual(const ResidualParams& p, cudaStream_t s);
+
+struct PagesParams {
+    const uint8_t* pool;
+    const UnitMeta* meta;
+    int unit_begin, n_units, group;
+    const __half* q;
+    const int32_t* pref;   // [n_units + 1] local page prefix
+    int chunk, total_pages, n_warps;
+    float* part_ml;        // [slots][2][kMaxG]
+    float* part_o;         // [slots][kMaxG][d]
+    const float* res_ml;
+    const float* res_o;
+    int* counters;         // [n_units] local, zero between calls
+    __half* out;
+    float scale_log2;
+};
+constexpr int kPagesWarps = 8;
+cudaError_t launch_pages(const PagesParams& p, int grid, cudaStream_t s);
+
+// ---- utilities (synth.cu) ----
+cudaError_t launch_synth_fp16(__half* out, int64_t n_rows, int64_t row_len, int64_t ld,
+                              uint64_t seed, uint64_t stream_base, uint64_t stream_step,
+                              cudaStream_t s);
+cudaError_t launch_synth_uniform(float* out, int64_t n_rows, int64_t row_len, int64_t ld,
+                                 uint64_t seed, uint64_t stream_base, uint64_t stream_step,
+                                 cudaStream_t s);
+
+// ---- K1: prefill attention (prefill.cu) ----
+struct PrefillAttnParams {
+    const __half* q;
+    int64_t q_sb, q_sh, q_st;
+    const __half* k;
+    int64_t k_sb, k_sh, k_st;
+    const __half* v;
+    int64_t v_sb, v_sh, v_st;
+    __half* out;
+    int64_t o_sb, o_sh, o_st;
+    float* lse;
+    float* a_cumul;
+    int batch, hq, hkv, lq, lk;
+    float scale;
+    int causal;
+};
+cudaError_t launch_prefill_attn(const PrefillAttnParams& p, cudaStream_t s);
+
+}  // namespace mkv

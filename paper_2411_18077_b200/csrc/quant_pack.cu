@@ -1,0 +1,76 @@
+// quant_pack.cu -- K3: gather the selected tokens and 2-bit quantize + pack them.
+//
+// Restates the tail of prefill (cache_engine.cpp:56-77): gather_rows of the
+// kept indices (ascending) followed by append_block for keys (PerChannel) and
+// values (PerToken) as ONE block of n_kept rows (quantizer.cpp:102-136).  Key
+// groups are 16 consecutive *kept* tokens; the last group of the
+// block may be short and is quantized over its own tokens only.  No gathered
+// intermediate is materialised: each warp gathers its page's 16 rows straight
+// from K/V into shared memory and writes one finished 2 KB page with 16-byte
+// coalesced stores.
+#include "mkv_kernels.h"
+#include "mkv_page.cuh"
+
+namespace mkv {
+
+constexpr int kQuantWarps = 4;
+
+__global__ void __launch_bounds__(kQuantWarps * 32) prefill_pages_kernel(const PrefillPagesParams P) {
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    PageScratch* scratch = reinterpret_cast<PageScratch*>(smem_raw);
+    const int warp = threadIdx.x >> 5, lane = lane_id();
+    const int i = blockIdx.y;
+    const int u = P.unit_begin + i;
+    const int p = blockIdx.x * kQuantWarps + warp;
+    const UnitMeta meta = P.meta[u];
+    const int n_kept = meta.n_prefill;
+    const int pages = (n_kept + 15) >> 4;
+    if (p >= pages) return;
+    const int valid = min(16, n_kept - 16 * p);
+    PageScratch& s = scratch[warp];
+    const int32_t* kept = P.kept + (size_t)i * P.kept_stride + 16 * p;
+    const __half* kbase = P.k + (size_t)i * P.k_su;
+    const __half* vbase = P.v + (size_t)i * P.v_su;
+    // gather: 16 rows x 16 uint4 per tensor, 8 per lane
+#pragma unroll
+    for (int e = lane; e < 256; e += 32) {
+        const int r = e >> 4, c16 = e & 15;
+        if (r < valid) {
+            const int64_t t = __ldg(kept + r);
+            reinterpret_cast<uint4*>(s.k[r])[c16] = __ldg(reinterpret_cast<const uint4*>(kbase + t * P.k_st) + c16);
+            reinterpret_cast<uint4*>(s.v[r])[c16] = __ldg(reinterpret_cast<const uint4*>(vbase + t * P.v_st) + c16);
+        }
+    }
+    __syncwarp();
+    const int64_t page = meta.page_base + p;
+    const bool ok = build_page(s, valid, P.pool + (size_t)page * kPageBytes,
+                               P.shadow ? P.shadow + (size_t)page * (kShadowBytes / 4) : nullptr);
+    if (!ok && lane == 0) atomicOr(P.status, kStatusNonFinite);
+}
+
+cudaError_t launch_prefill_pages(const PrefillPagesParams& p, cudaStream_t s) {
+    if (p.n_units == 0 || p.max_pages == 0) return cudaSuccess;
+    const size_t smem = sizeof(PageScratch) * kQuantWarps;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(prefill_pages_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    for (int u0 = 0; u0 < p.n_units; u0 += 65535) {  // grid.y limit
+        PrefillPagesParams q = p;
+        q.unit_begin = p.unit_begin + u0;
+        q.n_units = min(65535, p.n_units - u0);
+        q.k = p.k + (size_t)u0 * p.k_su;
+        q.v = p.v + (size_t)u0 * p.v_su;
+        q.kept = p.kept + (size_t)u0 * p.kept_stride;
+        dim3 grid((p.max_pages + kQuantWarps - 1) / kQuantWarps, q.n_units);
+        prefill_pages_kernel<<<grid, kQuantWarps * 32, smem, s>>>(q);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+}  // namespace mkv

@@ -1,0 +1,108 @@
+"""K4 fused 2-bit decode attention on the B200 vs the oracle.
+
+Oracle (GQA composition): per unit one decode_append
+(cache_engine.cpp:79-90), then for each q-head decode_attention over
+[dequant(stored) ; residual] -- bit-identical to decode_step for G = 1 --
+with the stored (scale, zero) rounded to fp16 as the device stores them.
+Tolerance (stated in BASELINE/SURVEY 8(d)): max |t_O - oracle| <= 5e-3.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from tests.gpu_util import SEED, f32, max_abs, synth_np
+
+pytestmark = pytest.mark.gpu
+TOL = 5e-3
+
+
+@pytest.fixture(scope="module")
+def mkv():
+    import paper_2411_18077_b200 as m
+    return m
+
+
+def run_decode(mkv, n_units, G, L, hh, rw, steps, n_r=128, seed=SEED, check_every=1, hh_per_unit=None):
+    d = 128
+    scale = 1.0 / np.sqrt(d)
+    k = np.stack([synth_np(seed, oracle.stream_id(oracle.KIND_K, u), (L, d)) for u in range(n_units)])
+    v = np.stack([synth_np(seed, oracle.stream_id(oracle.KIND_V, u), (L, d)) for u in range(n_units)])
+    rng = np.random.default_rng(seed + L)
+    a = rng.random((n_units, L)).astype(np.float32)
+    hh_u = hh_per_unit or [hh] * n_units
+    caps = [min(h + rw, L) for h in hh_u]
+    cache = mkv.KVCache(n_units, caps, max_decode_tokens=steps + n_r, n_r=n_r)
+    cache.prefill(torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda(), torch.from_numpy(a).cuda(), hh_u, rw)
+    P = oracle.port()
+    ocs = []
+    for u in range(n_units):
+        oc = P.cache(d=d, n_r=n_r)
+        oc.prefill(f32(k[u]), f32(v[u]), a[u], hh_u[u], rw)
+        ocs.append(oc)
+    worst = 0.0
+    for s in range(steps):
+        q = np.stack([synth_np(seed, oracle.stream_id(oracle.KIND_QDEC, u, s + 1), (G, d)) for u in range(n_units)])
+        tk = np.stack([synth_np(seed, oracle.stream_id(oracle.KIND_KDEC, u, s + 1), (d,)) for u in range(n_units)])
+        tv = np.stack([synth_np(seed, oracle.stream_id(oracle.KIND_VDEC, u, s + 1), (d,)) for u in range(n_units)])
+        out = cache.decode_step(torch.from_numpy(q).cuda(), torch.from_numpy(tk).cuda(),
+                                torch.from_numpy(tv).cuda(), scale)
+        out = out.float().cpu().numpy()
+        for u in range(n_units):
+            ocs[u].append(f32(tk[u]), f32(tv[u]))
+            if s % check_every == 0 or s == steps - 1:
+                for h in range(G):
+                    exp = ocs[u].attend(f32(q[u, h]), scale, param_fp16=True)
+                    worst = max(worst, max_abs(out[u, h], exp))
+    cache.check()
+    return worst
+
+
+@pytest.mark.parametrize("G", [1, 4, 8])
+def test_decode_gqa_small(mkv, G):
+    assert run_decode(mkv, n_units=3, G=G, L=400, hh=40, rw=40, steps=20) <= TOL
+
+
+def test_decode_through_flush(mkv):
+    # 818 kept (config-1 budget at L=4096 scaled down: partial last prefill page) and a flush at step 128
+    worst = run_decode(mkv, n_units=2, G=4, L=1000, hh=91, rw=100, steps=140, check_every=7)
+    assert worst <= TOL
+
+
+def test_decode_partial_pages_and_tiny_units(mkv):
+    # units with fewer than 16 kept tokens (one partial page) and ragged pyramid budgets
+    worst = run_decode(mkv, n_units=5, G=4, L=300, hh=0, rw=3, steps=10, hh_per_unit=[0, 5, 13, 60, 200])
+    assert worst <= TOL
+
+
+def test_decode_many_units_split(mkv):
+    # enough pages that units are split across several warps (split-K merge path)
+    worst = run_decode(mkv, n_units=16, G=4, L=6000, hh=1500, rw=600, steps=3)
+    assert worst <= TOL
+
+
+def test_decode_small_n_r(mkv):
+    worst = run_decode(mkv, n_units=2, G=2, L=200, hh=20, rw=20, steps=70, n_r=32, check_every=5)
+    assert worst <= TOL
+
+
+def test_decode_residual_only_unit(mkv):
+    """A unit whose cache is only residual rows (no pages) is finished by the residual kernel."""
+    d = 128
+    cache = mkv.KVCache(1, 16, max_decode_tokens=64)
+    P = oracle.port()
+    oc = P.cache()
+    rng = np.random.default_rng(3)
+    # first append without attention, then decode steps (decode_step needs a non-empty cache)
+    tk = rng.standard_normal((1, d)).astype(np.float16)
+    tv = rng.standard_normal((1, d)).astype(np.float16)
+    cache.append(torch.from_numpy(tk).cuda(), torch.from_numpy(tv).cuda())
+    oc.append(f32(tk[0]), f32(tv[0]))
+    for s in range(5):
+        q = rng.standard_normal((1, 1, d)).astype(np.float16)
+        tk = rng.standard_normal((1, d)).astype(np.float16)
+        tv = rng.standard_normal((1, d)).astype(np.float16)
+        out = cache.decode_step(torch.from_numpy(q).cuda(), torch.from_numpy(tk).cuda(),
+                                torch.from_numpy(tv).cuda(), 0.1).float().cpu().numpy()
+        exp = oc.decode_step(f32(q[0, 0]), f32(tk[0]), f32(tv[0]), 0.1, param_fp16=True)
+        assert max_abs(out[0, 0], exp) <= TOL

@@ -1,0 +1,163 @@
+"""K2 (selection) and K3 (quantize + pack) on the B200 vs the oracle: bit-exact.
+
+Selection: select_token_counts (selection.cpp:10-33), ties to the lower index.
+Quantizer: prefill -> append_block PerChannel K / PerToken V
+(quantizer.cpp:102-136), compared through the reference-format export.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from tests.gpu_util import SEED, f32, oracle_select
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def mkv():
+    import paper_2411_18077_b200 as m
+    return m
+
+
+def _ties(rng, n, levels):
+    return (rng.integers(0, levels, n).astype(np.float32) * np.float32(0.125))
+
+
+@pytest.mark.parametrize("L,hh,rw,kind", [
+    (256, 64, 64, "uniform"), (1000, 100, 100, "ties"), (4096, 409, 409, "uniform"),
+    (777, 0, 50, "uniform"), (777, 50, 0, "ties"), (100, 95, 10, "uniform"),  # clamped
+    (300, 300, 0, "ties"), (1, 1, 0, "uniform"), (65536, 6553, 6553, "ties"),
+    (5000, 2500, 100, "allequal"), (32768, 6084, 3276, "uniform"),
+])
+def test_select_matches_oracle(mkv, L, hh, rw, kind):
+    rng = np.random.default_rng(L * 7 + hh)
+    if kind == "uniform":
+        a = rng.random(L).astype(np.float32)
+    elif kind == "ties":
+        a = _ties(rng, L, 7)
+    else:
+        a = np.ones(L, np.float32)
+    a[rng.integers(0, L, max(1, L // 50))] = 0.0
+    a[rng.integers(0, L, max(1, L // 97))] = -0.0
+    ta = torch.from_numpy(a).cuda()
+    kept, nk = mkv.select_token_counts(ta, hh, rw)
+    got = kept.cpu().numpy().astype(np.int64)
+    exp = oracle_select(a, hh, rw)
+    assert nk == len(exp)
+    np.testing.assert_array_equal(got, exp)
+
+
+def test_select_batched_units(mkv):
+    rng = np.random.default_rng(5)
+    n, L = 37, 3000
+    a = _ties(rng, n * L, 40).reshape(n, L)
+    hh = [int(x) for x in rng.integers(0, 1500, n)]
+    kept, nks = mkv.select_token_counts(torch.from_numpy(a).cuda(), hh, 200)
+    kept = kept.cpu().numpy()
+    for u in range(n):
+        exp = oracle_select(a[u], hh[u], 200)
+        np.testing.assert_array_equal(kept[u, :nks[u]], exp)
+
+
+def _prefill_case(mkv, L, hh, rw, n_units, fp32_params, dist_scale=1.0):
+    rng = np.random.default_rng(L + hh + rw)
+    d = 128
+    k = (rng.standard_normal((n_units, L, d)) * dist_scale).astype(np.float16)
+    v = (rng.standard_normal((n_units, L, d)) * dist_scale).astype(np.float16)
+    a = rng.random((n_units, L)).astype(np.float32)
+    cap = min(hh + rw, L)
+    cache = mkv.KVCache(n_units, cap, max_decode_tokens=256, keep_fp32_params=fp32_params)
+    cache.prefill(torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda(), torch.from_numpy(a).cuda(), hh, rw)
+    cache.check()
+    return cache, k, v, a
+
+
+@pytest.mark.parametrize("L,hh,rw", [(300, 40, 30), (1000, 100, 100), (64, 16, 16), (37, 5, 3),
+                                     (4096, 409, 409), (20, 100, 0)])
+@pytest.mark.parametrize("fp32_params", [True, False])
+def test_prefill_pack_bit_exact(mkv, L, hh, rw, fp32_params):
+    n_units = 3
+    cache, k, v, a = _prefill_case(mkv, L, hh, rw, n_units, fp32_params)
+    P = oracle.port()
+    for u in range(n_units):
+        oc = P.cache()
+        oc.prefill(f32(k[u]), f32(v[u]), a[u], hh, rw)
+        for which in (0, 1):
+            w_ref, p_ref, br_ref = oc.export(which)
+            w, p, br = cache.export_reference(u, which)
+            np.testing.assert_array_equal(br, br_ref)
+            np.testing.assert_array_equal(w, w_ref)  # codes: bit-exact
+            if fp32_params:
+                np.testing.assert_array_equal(p, p_ref)
+            else:
+                np.testing.assert_array_equal(p, p_ref.astype(np.float16).astype(np.float32))
+
+
+def test_flush_blocks_bit_exact(mkv):
+    """decode_append flushes a full n_r block into 2-bit pages (cache_engine.cpp:79-90)."""
+    L, hh, rw, n_units, d = 500, 60, 45, 2, 128
+    cache, k, v, a = _prefill_case(mkv, L, hh, rw, n_units, True)
+    P = oracle.port()
+    ocs = []
+    for u in range(n_units):
+        oc = P.cache()
+        oc.prefill(f32(k[u]), f32(v[u]), a[u], hh, rw)
+        ocs.append(oc)
+    rng = np.random.default_rng(9)
+    for step in range(300):
+        tk = rng.standard_normal((n_units, d)).astype(np.float16)
+        tv = rng.standard_normal((n_units, d)).astype(np.float16)
+        cache.append(torch.from_numpy(tk).cuda(), torch.from_numpy(tv).cuda())
+        for u in range(n_units):
+            ocs[u].append(f32(tk[u]), f32(tv[u]))
+    cache.check()
+    for u in range(n_units):
+        info = cache.unit_info(u)
+        assert info["tokens_quantized"] == ocs[u].tokens_quantized == hh + rw + 256
+        assert info["tokens_residual"] == ocs[u].tokens_residual == 300 - 256
+        for which in (0, 1):
+            w_ref, p_ref, br_ref = ocs[u].export(which)
+            w, p, br = cache.export_reference(u, which)
+            np.testing.assert_array_equal(br, br_ref)
+            np.testing.assert_array_equal(w, w_ref)
+            np.testing.assert_array_equal(p, p_ref)
+        rk, rv = cache.export_residual(u)
+        ork, orv = ocs[u].residual()
+        np.testing.assert_array_equal(rk.astype(np.float32), ork)
+        np.testing.assert_array_equal(rv.astype(np.float32), orv)
+
+
+def test_nonfinite_input_is_domain_error(mkv):
+    L, d = 64, 128
+    k = np.zeros((1, L, d), np.float16)
+    v = np.zeros((1, L, d), np.float16)
+    k[0, 3, 7] = np.float16(np.inf)
+    a = np.ones((1, L), np.float32)
+    cache = mkv.KVCache(1, L, 0)
+    cache.prefill(torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda(), torch.from_numpy(a).cuda(), L, 0)
+    with pytest.raises(mkv.DomainError):
+        cache.check()
+
+
+def test_prefill_errors(mkv):
+    cache = mkv.KVCache(1, 64, 0)
+    k = torch.zeros((1, 64, 128), dtype=torch.float16, device="cuda")
+    a = torch.ones((1, 64), dtype=torch.float32, device="cuda")
+    with pytest.raises(mkv.RuntimeFailure):   # zero kept tokens (cache_engine.cpp:66-68)
+        cache.prefill(k, k, a, 0, 0)
+    with pytest.raises(mkv.InvalidArgument):  # make_cache: n_r not a multiple of group_size
+        mkv.KVCache(1, 64, 0, n_r=24)
+    with pytest.raises(mkv.RuntimeFailure):   # decode_step on an empty cache
+        q = torch.zeros((1, 1, 128), dtype=torch.float16, device="cuda")
+        cache.decode_step(q, None, None, 0.1)
+
+
+def test_synth_matches_oracle(mkv):
+    t = mkv.synth_fp16((4, 1000), SEED, 12345, 7).cpu().numpy()
+    for r in range(4):
+        exp = oracle.port().synth_fp16(SEED, 12345 + 7 * r, 1000)
+        np.testing.assert_array_equal(t[r].view(np.uint16), exp.view(np.uint16))
+    u = mkv.synth_uniform((2, 500), SEED, 99, 1).cpu().numpy()
+    for r in range(2):
+        np.testing.assert_array_equal(u[r], oracle.port().synth_uniform(SEED, 99 + r, 500))

@@ -1,0 +1,89 @@
+"""The C restatement vs the reference itself (oracle/_ref, compiled from the
+unmodified sources): bit-identical on fresh seeded inputs.  CPU only; skipped
+where the reference .so could not be built (the golden fixtures then pin it).
+"""
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.skipif(not oracle.ref_available(), reason="oracle/_ref not built")
+
+
+@pytest.fixture(scope="module")
+def PR():
+    return oracle.port(), oracle.ref()
+
+
+def test_attention_random_shapes(PR):  # mirrors acceptance.cpp:103-142 (210 random cases)
+    P, R = PR
+    rng = np.random.default_rng(7)
+    for _ in range(60):
+        d = int(rng.choice([8, 16, 64, 128]))
+        lk = int(rng.integers(1, 200))
+        lq = int(rng.integers(1, lk + 1))
+        causal = bool(rng.integers(0, 2))
+        bm, bn = int(rng.integers(1, 97)), int(rng.integers(1, 97))
+        q = rng.standard_normal((lq, d)).astype(np.float32)
+        k = rng.standard_normal((lk, d)).astype(np.float32)
+        v = rng.standard_normal((lk, d)).astype(np.float32)
+        a = P.selective_flash_attn(q, k, v, 1 / np.sqrt(d), causal, bm, bn)
+        b = R.selective_flash_attn(q, k, v, 1 / np.sqrt(d), causal, bm, bn)
+        assert np.array_equal(a.output, b.output) and np.array_equal(a.lse, b.lse)
+        assert np.array_equal(a.a_cumul, b.a_cumul) and a.aux_elements == b.aux_elements
+
+
+def test_quantizer_random(PR):
+    P, R = PR
+    rng = np.random.default_rng(8)
+    for _ in range(100):
+        rows, cols = int(rng.integers(1, 140)), int(rng.integers(1, 140))
+        m = (rng.standard_normal((rows, cols)) * rng.uniform(0.01, 100)).astype(np.float32)
+        if rng.random() < 0.2:
+            m = np.round(m)  # many exact-tie / constant groups
+        for axis in (0, 1):
+            codes, params = P.quantize_block(m, axis)
+            w, p = R.quantize_matrix(m, axis)
+            assert np.array_equal(P.pack_codes(codes), w) and np.array_equal(params, p)
+
+
+def test_selection_random(PR):
+    P, R = PR
+    rng = np.random.default_rng(9)
+    for _ in range(200):
+        L = int(rng.integers(1, 3000))
+        a = rng.random(L).astype(np.float32)
+        if rng.random() < 0.5:
+            a = np.floor(a * 6).astype(np.float32)
+        hh, rw = int(rng.integers(0, L + 5)), int(rng.integers(0, L // 2 + 2))
+        assert np.array_equal(P.select_token_counts(a, hh, rw)[0], R.select_token_counts(a, hh, rw)[0])
+
+
+def test_pyramid_random(PR):
+    P, R = PR
+    rng = np.random.default_rng(10)
+    for _ in range(300):
+        x, layers, depth = int(rng.integers(0, 60000)), int(rng.integers(1, 80)), int(rng.integers(1, 12))
+        bh = bool(rng.integers(0, 2))
+        assert np.array_equal(P.allocate_pyramid(x, layers, depth, bh), R.allocate_pyramid(x, layers, depth, bh))
+
+
+def test_cache_decode_random(PR):
+    P, R = PR
+    rng = np.random.default_rng(11)
+    for trial in range(4):
+        L, d = int(rng.integers(20, 400)), int(rng.choice([16, 64, 128]))
+        n_r = int(rng.choice([16, 32, 128]))
+        hh, rw = int(rng.integers(0, L)), int(rng.integers(1, L // 2 + 2))
+        k = rng.standard_normal((L, d)).astype(np.float32)
+        v = rng.standard_normal((L, d)).astype(np.float32)
+        a = rng.random(L).astype(np.float32)
+        pc = P.cache(d=d, n_r=n_r)
+        pc.prefill(k, v, a, hh, rw)
+        rc = R.cache_prefill(k, v, a, hh, rw, n_r=n_r)
+        for s in range(int(rng.integers(1, 2 * n_r + 10))):
+            tq, tk, tv = (rng.standard_normal(d).astype(np.float32) for _ in range(3))
+            assert np.array_equal(pc.decode_step(tq, tk, tv, 0.1), rc.decode_step(tq, tk, tv, 0.1))
+        for which in (0, 1):
+            for x, y in zip(pc.export(which), rc.export(which)):
+                assert np.array_equal(x, y)
