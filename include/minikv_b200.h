@@ -173,6 +173,10 @@ int mkv_decode_step(mkv_cache* cache, const mkv_decode_args* args, void* stream)
 /* decode_append only (cache_engine.cpp:79-90). */
 int mkv_cache_append(mkv_cache* cache, int unit_begin, int n_units, const void* k_new,
                      const void* v_new, void* stream);
+/* Profiling entry: ONLY the fused page kernel of K4 (pages -> partials -> merge),
+ * reusing the residual partials of the previous mkv_decode_step on the same
+ * units.  Used by bench.py to time the dominant kernel for its roofline. */
+int mkv_decode_pages_only(mkv_cache* cache, const mkv_decode_args* args, void* stream);
 /* Multi-layer decode step: n_layers consecutive calls in one FFI crossing. */
 int mkv_decode_step_layers(mkv_cache* cache, int n_layers, const mkv_decode_args* args,
                            void* stream);

@@ -108,7 +108,7 @@ EXPORTS = [
     "mkv_prefill_attn", "mkv_select", "mkv_allocate_pyramid", "mkv_allocate_uniform",
     "mkv_cache_create", "mkv_cache_destroy", "mkv_cache_bytes", "mkv_cache_unit_info",
     "mkv_cache_prefill", "mkv_cache_prefill_select", "mkv_decode_step", "mkv_cache_append",
-    "mkv_decode_step_layers", "mkv_cache_export_sizes", "mkv_cache_export_reference",
+    "mkv_decode_step_layers", "mkv_decode_pages_only", "mkv_cache_export_sizes", "mkv_cache_export_reference",
     "mkv_cache_export_residual", "mkv_cache_check",
     "mkv_synth_fp16", "mkv_synth_fp16_rows", "mkv_synth_uniform_f32",
 ]
@@ -137,6 +137,7 @@ def lib():
     L.mkv_cache_prefill.argtypes = [vp, C.POINTER(CachePrefillArgs), vp]
     L.mkv_cache_prefill_select.argtypes = [vp, C.POINTER(PrefillSelectArgs), vp]
     L.mkv_decode_step.argtypes = [vp, C.POINTER(DecodeArgs), vp]
+    L.mkv_decode_pages_only.argtypes = [vp, C.POINTER(DecodeArgs), vp]
     L.mkv_decode_step_layers.argtypes = [vp, i32, C.POINTER(DecodeArgs), vp]
     L.mkv_cache_append.argtypes = [vp, i32, i32, vp, vp, vp]
     L.mkv_cache_export_sizes.argtypes = [vp, i32, i32] + [C.POINTER(C.c_int64)] * 3

@@ -78,7 +78,8 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 struct Plan {
     uint64_t hash = 0;
     int total = 0, chunk = 0, grid = 0;
-    int32_t* d_pref = nullptr;
+    int32_t* d_pref = nullptr;    // [n_units + 1] local page prefix, then [warps] first unit per warp
+    int32_t* d_wstart = nullptr;
 };
 
 struct mkv_cache {
@@ -95,9 +96,6 @@ struct mkv_cache {
     __half* d_res_k = nullptr;
     __half* d_res_v = nullptr;
     uint32_t* d_status = nullptr;
-    int* d_counters = nullptr;
-    float* d_res_ml = nullptr;
-    float* d_res_o = nullptr;
     float* d_part_ml = nullptr;
     float* d_part_o = nullptr;
     int part_slots = 0;
@@ -106,7 +104,7 @@ struct mkv_cache {
     ~mkv_cache() {
         for (auto& kv : plans) cudaFree(kv.second.d_pref);
         cudaFree(d_meta); cudaFree(d_pool); cudaFree(d_shadow); cudaFree(d_res_k); cudaFree(d_res_v);
-        cudaFree(d_status); cudaFree(d_counters); cudaFree(d_res_ml); cudaFree(d_res_o);
+        cudaFree(d_status);
         cudaFree(d_part_ml); cudaFree(d_part_o);
     }
 
@@ -279,13 +277,9 @@ int mkv_cache_create(const mkv_cache_config* cfg, mkv_cache** out) {
     if (e == cudaSuccess) e = al((void**)&c->d_res_k, (size_t)n * c->n_r * c->d * sizeof(__half));
     if (e == cudaSuccess) e = al((void**)&c->d_res_v, (size_t)n * c->n_r * c->d * sizeof(__half));
     if (e == cudaSuccess) e = al((void**)&c->d_status, sizeof(uint32_t));
-    if (e == cudaSuccess) e = al((void**)&c->d_counters, sizeof(int) * n);
-    if (e == cudaSuccess) e = al((void**)&c->d_res_ml, sizeof(float) * 2 * kMaxG * n);
-    if (e == cudaSuccess) e = al((void**)&c->d_res_o, sizeof(float) * kMaxG * kHeadDim * n);
     if (e == cudaSuccess) e = al((void**)&c->d_part_ml, sizeof(float) * 2 * kMaxG * c->part_slots);
     if (e == cudaSuccess) e = al((void**)&c->d_part_o, sizeof(float) * kMaxG * kHeadDim * c->part_slots);
     if (e == cudaSuccess) e = cudaMemset(c->d_status, 0, sizeof(uint32_t));
-    if (e == cudaSuccess) e = cudaMemset(c->d_counters, 0, sizeof(int) * n);
     if (e == cudaSuccess) e = cudaMemset(c->d_pool, 0, (size_t)acc * kPageBytes);
     if (e == cudaSuccess) e = c->upload_meta(0, n, 0);
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
@@ -426,22 +420,38 @@ static int get_plan(mkv_cache* c, int ub, int n, cudaStream_t s, Plan** out) {
         *out = &pl;
         return MKV_OK;
     }
-    std::vector<int32_t> pref(n + 1);
-    pref[0] = 0;
+    const int max_warps = num_sms() * kPagesWarps;
+    std::vector<int32_t> buf(n + 1 + max_warps, 0);
+    int32_t* pref = buf.data();
     for (int i = 0; i < n; ++i) pref[i + 1] = pref[i] + c->n_pages[ub + i];
     const int total = pref[n];
-    const int max_warps = num_sms() * kPagesWarps;
-    const int min_chunk = 4;
-    int chunk = std::max(min_chunk, (total + max_warps - 1) / std::max(max_warps, 1));
+    const int min_chunk = 8;
+    const int chunk = std::max(min_chunk, (total + max_warps - 1) / std::max(max_warps, 1));
     const int warps = total > 0 ? (total + chunk - 1) / chunk : 0;
-    if (!pl.d_pref) CK(cudaMalloc(&pl.d_pref, sizeof(int32_t) * (c->n_units + 1)));
-    CK(cudaMemcpyAsync(pl.d_pref, pref.data(), sizeof(int32_t) * (n + 1), cudaMemcpyHostToDevice, s));
+    int32_t* wstart = pref + n + 1;
+    for (int w = 0, i = 0; w < warps; ++w) {  // first unit with pages that contains page w*chunk
+        const int p = w * chunk;
+        while (i < n - 1 && pref[i + 1] <= p) ++i;
+        wstart[w] = i;
+    }
+    if (!pl.d_pref) CK(cudaMalloc(&pl.d_pref, sizeof(int32_t) * (c->n_units + 1 + max_warps)));
+    CK(cudaMemcpyAsync(pl.d_pref, buf.data(), sizeof(int32_t) * buf.size(), cudaMemcpyHostToDevice, s));
+    pl.d_wstart = pl.d_pref + n + 1;
     pl.hash = h;
     pl.total = total;
     pl.chunk = chunk;
     pl.grid = (warps + kPagesWarps - 1) / kPagesWarps;
     *out = &pl;
     return MKV_OK;
+}
+
+static void fill_pages_params(mkv_cache* c, const Plan* pl, const mkv_decode_args* a, PagesParams& pp) {
+    pp.pool = c->d_pool; pp.meta = c->d_meta; pp.unit_begin = a->unit_begin; pp.n_units = a->n_units;
+    pp.group = a->group; pp.q = static_cast<const __half*>(a->q);
+    pp.pref = pl->d_pref; pp.wstart = pl->d_wstart; pp.chunk = pl->chunk; pp.total_pages = pl->total;
+    pp.n_warps = pl->grid * kPagesWarps;
+    pp.part_ml = c->d_part_ml; pp.part_o = c->d_part_o;
+    pp.scale_log2 = a->scale * 1.4426950408889634f;
 }
 
 static int decode_impl(mkv_cache* c, const mkv_decode_args* a, bool attend, cudaStream_t s) {
@@ -466,6 +476,7 @@ static int decode_impl(mkv_cache* c, const mkv_decode_args* a, bool attend, cuda
             return fail(MKV_ERR_OUT_OF_RANGE, "decode: unit %d exceeds max_decode_tokens", u);
     }
     if (int r = require_device()) return r;
+    bool any_flush = false;
     if (append) {
         for (int i = 0; i < n; ++i) {
             const int u = ub + i;
@@ -473,6 +484,7 @@ static int decode_impl(mkv_cache* c, const mkv_decode_args* a, bool attend, cuda
                 c->n_res[u] = 0;
                 c->n_pages[u] += c->n_r / kGroup;
                 c->n_blocks[u] += 1;
+                any_flush = true;
             }
         }
     }
@@ -482,28 +494,45 @@ static int decode_impl(mkv_cache* c, const mkv_decode_args* a, bool attend, cuda
     rp.k_new = static_cast<const __half*>(a->k_new);
     rp.v_new = static_cast<const __half*>(a->v_new);
     rp.res_k = c->d_res_k; rp.res_v = c->d_res_v; rp.pool = c->d_pool; rp.shadow = c->d_shadow;
-    rp.res_ml = c->d_res_ml; rp.res_o = c->d_res_o; rp.out = static_cast<__half*>(a->out);
+    rp.part_ml = c->d_part_ml; rp.part_o = c->d_part_o; rp.out = static_cast<__half*>(a->out);
     rp.scale_log2 = a->scale * 1.4426950408889634f;
-    rp.attend = attend ? 1 : 0;
     rp.status = c->d_status;
-    CK(launch_residual(rp, s));
+    // flush steps (or append-only calls): append (+ quantize the full block) before the page pass
+    if (append && (any_flush || !attend)) {
+        CK(launch_append(rp, s));
+        rp.k_new = nullptr;
+        rp.v_new = nullptr;
+    }
     if (!attend) return MKV_OK;
     Plan* pl = nullptr;
     if (int r = get_plan(c, ub, n, s, &pl)) return r;
-    if (pl->total == 0) return MKV_OK;  // residual-only units were finished by the residual kernel
-    PagesParams pp;
-    pp.pool = c->d_pool; pp.meta = c->d_meta; pp.unit_begin = ub; pp.n_units = n; pp.group = a->group;
-    pp.q = static_cast<const __half*>(a->q);
-    pp.pref = pl->d_pref; pp.chunk = pl->chunk; pp.total_pages = pl->total; pp.n_warps = pl->grid * kPagesWarps;
-    pp.part_ml = c->d_part_ml; pp.part_o = c->d_part_o; pp.res_ml = c->d_res_ml; pp.res_o = c->d_res_o;
-    pp.counters = c->d_counters; pp.out = static_cast<__half*>(a->out); pp.scale_log2 = rp.scale_log2;
-    CK(launch_pages(pp, pl->grid, s));
+    if (pl->total > 0) {
+        PagesParams pp;
+        fill_pages_params(c, pl, a, pp);
+        CK(launch_pages(pp, pl->grid, s));
+    }
+    CK(launch_finish(rp, pl->d_pref, std::max(pl->chunk, 1), s));
     return MKV_OK;
 }
 
 int mkv_decode_step(mkv_cache* c, const mkv_decode_args* a, void* stream) {
     if (!a) return fail(MKV_ERR_INVALID_ARGUMENT, "decode_step: null args");
     return decode_impl(c, a, true, static_cast<cudaStream_t>(stream));
+}
+
+int mkv_decode_pages_only(mkv_cache* c, const mkv_decode_args* a, void* stream) {
+    if (!a) return fail(MKV_ERR_INVALID_ARGUMENT, "decode: null args");
+    if (int r = check_range(c, a->unit_begin, a->n_units)) return r;
+    if (a->group < 1 || a->group > kMaxG || !a->q || !a->out) return fail(MKV_ERR_INVALID_ARGUMENT, "decode: bad args");
+    if (int r = require_device()) return r;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    Plan* pl = nullptr;
+    if (int r = get_plan(c, a->unit_begin, a->n_units, s, &pl)) return r;
+    if (pl->total == 0) return MKV_OK;
+    PagesParams pp;
+    fill_pages_params(c, pl, a, pp);
+    CK(launch_pages(pp, pl->grid, s));
+    return MKV_OK;
 }
 
 int mkv_decode_step_layers(mkv_cache* c, int n_layers, const mkv_decode_args* a, void* stream) {

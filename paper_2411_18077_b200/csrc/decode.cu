@@ -5,22 +5,27 @@
 // first, cache_engine.cpp:79-90), then ONE softmax over
 // [dequant(K_q) ; R_K] and out = attn . [dequant(V_q) ; R_V].
 //
-// Two kernels per call:
-//   residual_kernel  one CTA per unit: append (+flush via the K3 page builder),
-//                    attention over the fp16 residual -> partial (m, l, o)
-//   pages_kernel     persistent, 8 warps/CTA, each warp an independent worker
-//                    over a contiguous range of the global page sequence; pages
-//                    stream HBM -> smem with cp.async.bulk (3-stage ring per
-//                    warp), are dequantized in registers and multiplied on the
-//                    tensor cores (mma.sync m16n8k16) -> per-(warp, unit)
-//                    partials; the last warp to finish a unit merges all
-//                    partials (split-K / flash-decoding combine) into out.
+// Kernels (per call = one layer's units):
+//   append_kernel  (only on steps where some unit's residual fills up)
+//                  decode_append + flush of the n_r block through the K3 page
+//                  builder, so the new pages are visible to pages_kernel.
+//   pages_kernel   persistent, 12 warps/CTA, each warp an independent worker
+//                  over a contiguous range of the global page sequence; pages
+//                  stream HBM -> smem with cp.async.bulk (2-stage ring of
+//                  4-page batches per warp), are dequantized in registers and
+//                  multiplied on the tensor cores (mma.sync m16n8k16), four
+//                  pages interleaved for ILP -> one partial (m, l, o) per
+//                  (warp, unit) segment.
+//   finish_kernel  one CTA per unit: decode_append (non-flush steps), exact
+//                  attention over the fp16 residual (mma, one warp per 16-token
+//                  tile), and the split-K merge of every partial into out.
 //
-// Dequantization never materialises fp16 K/V: the 2-bit code is extracted
-// into an fp16 *subnormal* (code * 4^s * 2^-24) with one LOP3, the per-channel
-// key scale is folded into the query fragment, the per-token value scale into
-// the probability fragment, and the zero points enter through one extra mma
-// per page (sum_c q_c z_c for keys, sum_t p_t z_t for values).  See DESIGN.md.
+// Dequantization never materialises fp16 K/V: each 2-bit code becomes an fp16
+// *subnormal* code * 4^s * 2^-24 with one LOP3 (s = kc mod 3 after a 0/6/12-bit
+// shift), the 4^-s and the per-channel key scale are folded into the query
+// fragment, the per-token value scale into the probability fragment, and the
+// zero points enter through one extra mma per page (keys: sum_c q_c z_c over a
+// 4-page batch; values: sum_t p_t z_t).  See DESIGN.md.
 #include <math.h>
 
 #include "mkv_kernels.h"
@@ -30,58 +35,38 @@ namespace mkv {
 
 namespace {
 
-constexpr int kStages = 3;
-constexpr int kBatch = 4;  // pages per bulk copy / per K-bias mma
+constexpr int kStages = 2;
+constexpr int kBatch = 4;  // pages per bulk copy / per K-bias mma / per softmax update
 constexpr float kTwo24 = 16777216.0f;
+constexpr int kQBytes = kMaxG * kHeadDim * 2;  // per-warp q staging
+constexpr int kWarpSmem = kStages * kBatch * kPageBytes + kQBytes;
 
-__device__ __forceinline__ uint4 lds128(const uint8_t* p) {
-    return *reinterpret_cast<const uint4*>(p);
-}
-__device__ __forceinline__ uint2 lds64(const uint8_t* p) {
-    return *reinterpret_cast<const uint2*>(p);
-}
+__device__ __forceinline__ uint4 lds128(const uint8_t* p) { return *reinterpret_cast<const uint4*>(p); }
+__device__ __forceinline__ uint2 lds64(const uint8_t* p) { return *reinterpret_cast<const uint2*>(p); }
 
-// Binary search: largest i in [0, n) with pref[i] <= x.
-__device__ __forceinline__ int find_unit(const int32_t* pref, int n, int x) {
-    int lo = 0, hi = n - 1;
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (__ldg(pref + mid) <= x) lo = mid; else hi = mid - 1;
-    }
-    return lo;
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+__device__ __forceinline__ float extract_scale(int k) {  // 2^24 * 4^-(k mod 3)
+    return kTwo24 * ((k % 3 == 0) ? 1.0f : ((k % 3 == 1) ? 0.25f : 0.0625f));
 }
 
-// Merge every partial of local unit i (pages partial slots + residual) into out.
-__device__ void merge_unit(const PagesParams& P, int i, int w_first, int w_last) {
-    const int lane = lane_id();
-    const int G = P.group;
-    const float* rml = P.res_ml + (size_t)i * 2 * kMaxG;
-    const float* ro = P.res_o + (size_t)i * kMaxG * kHeadDim;
-    for (int h = 0; h < G; ++h) {
-        float M = __ldcg(rml + h);
-        for (int w = w_first; w <= w_last; ++w) {
-            const float* ml = P.part_ml + (size_t)(w + i) * 2 * kMaxG;
-            M = fmaxf(M, __ldcg(ml + h));
+// q of local unit i, head gid (zero for gid >= G), staged in smem, -> B fragments
+__device__ __forceinline__ void load_q_frags(const __half* qs_smem, int G, int gid, int tig, uint32_t (&qb)[8][2],
+                                             uint32_t (&qsc)[8][2]) {
+#pragma unroll
+    for (int kc = 0; kc < 8; ++kc) {
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+            uint32_t v = 0;
+            if (gid < G) v = *reinterpret_cast<const uint32_t*>(qs_smem + gid * kHeadDim + 16 * kc + 2 * tig + 8 * p);
+            qb[kc][p] = v;
+            const float f = (kc % 3 == 0) ? 1.0f : ((kc % 3 == 1) ? 0.25f : 0.0625f);
+            qsc[kc][p] = hmul2_u32(v, pack_half2(f, f));
         }
-        const float rs = (__ldcg(rml + kMaxG + h) > 0.0f) ? fast_exp2(__ldcg(rml + h) - M) : 0.0f;
-        float L = __ldcg(rml + kMaxG + h) * rs;
-        float4 acc = __ldcg(reinterpret_cast<const float4*>(ro + h * kHeadDim) + lane);
-        acc.x *= rs; acc.y *= rs; acc.z *= rs; acc.w *= rs;
-        for (int w = w_first; w <= w_last; ++w) {
-            const float* ml = P.part_ml + (size_t)(w + i) * 2 * kMaxG;
-            const float* po = P.part_o + (size_t)(w + i) * kMaxG * kHeadDim;
-            const float sc = fast_exp2(__ldcg(ml + h) - M);
-            L += __ldcg(ml + kMaxG + h) * sc;
-            const float4 o = __ldcg(reinterpret_cast<const float4*>(po + h * kHeadDim) + lane);
-            acc.x += o.x * sc; acc.y += o.y * sc; acc.z += o.z * sc; acc.w += o.w * sc;
-        }
-        const float inv = 1.0f / L;
-        __half2 lo = __floats2half2_rn(acc.x * inv, acc.y * inv);
-        __half2 hi = __floats2half2_rn(acc.z * inv, acc.w * inv);
-        uint2 st;
-        st.x = *reinterpret_cast<uint32_t*>(&lo);
-        st.y = *reinterpret_cast<uint32_t*>(&hi);
-        reinterpret_cast<uint2*>(P.out + ((size_t)i * G + h) * kHeadDim)[lane] = st;
     }
 }
 
@@ -94,14 +79,25 @@ __global__ void __launch_bounds__(kPagesWarps * 32, 1) pages_kernel(const PagesP
     extern __shared__ __align__(128) uint8_t smem[];
     const int warp = threadIdx.x >> 5, lane = lane_id();
     const int gid = lane >> 2, tig = lane & 3;
-    uint8_t* ring = smem + (size_t)warp * kStages * kBatch * kPageBytes;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)kPagesWarps * kStages * kBatch * kPageBytes) +
-                     warp * kStages;
+    uint8_t* wsm = smem + (size_t)warp * kWarpSmem;
+    uint8_t* ring = wsm;
+    __half* qsm = reinterpret_cast<__half*>(wsm + kStages * kBatch * kPageBytes);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)kPagesWarps * kWarpSmem) + warp * kStages;
 
     const int wg = blockIdx.x * kPagesWarps + warp;
     const int start = wg * P.chunk;
     const int end = min(start + P.chunk, P.total_pages);
     if (start >= end) return;
+    const int G = P.group;
+    const int qchunks = G * kHeadDim * 2 / 16;
+
+    int ci = __ldg(P.wstart + wg);  // first unit of this warp's range (host plan)
+    auto prefetch_q = [&](int unit) {
+        const uint8_t* src = reinterpret_cast<const uint8_t*>(P.q + (size_t)unit * G * kHeadDim);
+        for (int e = lane; e < qchunks; e += 32) cp_async16(reinterpret_cast<uint8_t*>(qsm) + 16 * e, src + 16 * e);
+        cp_async_commit();
+    };
+    prefetch_q(ci);
 
     if (lane == 0) {
         for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
@@ -110,60 +106,52 @@ __global__ void __launch_bounds__(kPagesWarps * 32, 1) pages_kernel(const PagesP
     __syncwarp();
 
     // ---- producer cursor (warp-uniform) ----
-    int pi = find_unit(P.pref, P.n_units, start);
+    int pi = ci;
     int pg = start;
+    int p_uend = __ldg(P.pref + pi + 1);
     auto issue = [&](int stage) {
-        // next batch: [pg, pg + n) inside unit pi
         if (pg >= end) return;
-        const int uend = __ldg(P.pref + pi + 1);
-        const int n = min(min(kBatch, uend - pg), end - pg);
+        const int n = min(min(kBatch, p_uend - pg), end - pg);
         if (lane == 0) {
-            const UnitMeta& m = P.meta[P.unit_begin + pi];
-            const uint8_t* src = P.pool + (size_t)(m.page_base + (pg - __ldg(P.pref + pi))) * kPageBytes;
+            const int64_t base = P.meta[P.unit_begin + pi].page_base;
+            const uint8_t* src = P.pool + (size_t)(base + (pg - __ldg(P.pref + pi))) * kPageBytes;
             mbar_expect_tx(&bars[stage], n * kPageBytes);
             bulk_g2s(ring + (size_t)stage * kBatch * kPageBytes, src, n * kPageBytes, &bars[stage]);
         }
         pg += n;
-        if (pg == uend) ++pi;
+        while (pg == p_uend && pg < end) {  // next unit that has pages
+            ++pi;
+            p_uend = __ldg(P.pref + pi + 1);
+        }
     };
     for (int s = 0; s < kStages; ++s) issue(s);
 
-    // ---- consumer state ----
-    int ci = find_unit(P.pref, P.n_units, start);
     int cg = start;
     int stage = 0;
     uint32_t phase = 0;
-    const int G = P.group;
     const float sl2 = P.scale_log2;
     const float sk = kTwo24 * sl2;
 
     while (cg < end) {
-        // ---- new unit segment: load query fragments ----
         const int unit = ci;
         const int upre = __ldg(P.pref + unit);
         const int uend_g = __ldg(P.pref + unit + 1);
         const int seg_end = min(uend_g, end);
         const UnitMeta meta = P.meta[P.unit_begin + unit];
-        const int prefill_pages = (meta.n_prefill + 15) >> 4;
-        const int partial_valid = meta.n_prefill & 15;  // 0 -> last prefill page is full
+        const int partial_page = (meta.n_prefill & 15) ? ((meta.n_prefill + 15) >> 4) - 1 : -1;
+        const int partial_valid = meta.n_prefill & 15;
 
-        uint32_t qb[8][2], qs[8][2];
-        {
-            const __half* qh = P.q + ((size_t)unit * G + gid) * kHeadDim;
-#pragma unroll
-            for (int kc = 0; kc < 8; ++kc) {
-#pragma unroll
-                for (int p = 0; p < 2; ++p) {
-                    uint32_t v = 0;
-                    if (gid < G) v = *reinterpret_cast<const uint32_t*>(qh + 16 * kc + 2 * tig + 8 * p);
-                    qb[kc][p] = v;
-                    // fold 4^-(kc mod 3) (the code-extraction scale) into the query
-                    const float f = (kc % 3 == 0) ? 1.0f : ((kc % 3 == 1) ? 0.25f : 0.0625f);
-                    const uint32_t fs = pack_half2(f, f);
-                    qs[kc][p] = hmul2_u32(v, fs);
-                }
-            }
+        uint32_t qb[8][2], qsc[8][2];
+        cp_async_wait_all();
+        __syncwarp();
+        load_q_frags(qsm, G, gid, tig, qb, qsc);
+        __syncwarp();
+        if (seg_end < end) {
+            int nu = unit + 1;
+            while (__ldg(P.pref + nu + 1) == seg_end) ++nu;
+            prefetch_q(nu);
         }
+
         float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.0f, l1 = 0.0f;
         float O[8][4];
 #pragma unroll
@@ -172,109 +160,118 @@ __global__ void __launch_bounds__(kPagesWarps * 32, 1) pages_kernel(const PagesP
 
         while (cg < seg_end) {
             const int n = min(min(kBatch, uend_g - cg), end - cg);
-            const int pfirst = cg - upre;  // local page index within the unit
+            const int pfirst = cg - upre;
             mbar_wait(&bars[stage], phase);
             const uint8_t* buf = ring + (size_t)stage * kBatch * kPageBytes;
 
-            // K zero-point bias for the batch: Kb[page][h] = sum_c z[page][c] q[h][c]
-            float Kb[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+            // ---- key zero-point bias: Kb[page][h] = sum_c z[page][c] q[h][c] (rows = pages) ----
+            float Kb[4] = {0.0f, 0.0f, 0.0f, 0.0f}, Kb2[4] = {0.0f, 0.0f, 0.0f, 0.0f};
             {
                 uint4 z[4];
-                if (gid < n) {
-                    const uint8_t* zp = buf + gid * kPageBytes + kKZ + tig * 64;
+                const bool zv = gid < n;
+                const uint8_t* zp = buf + (zv ? gid : 0) * kPageBytes + kKZ + tig * 64;
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) z[j] = lds128(zp + 16 * j);
-                } else {
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) z[j] = make_uint4(0, 0, 0, 0);
+                for (int j = 0; j < 4; ++j) {
+                    z[j] = lds128(zp + 16 * j);
+                    if (!zv) z[j] = make_uint4(0, 0, 0, 0);
                 }
                 const uint32_t* zz = reinterpret_cast<const uint32_t*>(z);
 #pragma unroll
-                for (int kc = 0; kc < 8; ++kc) {
-                    const uint32_t a[4] = {zz[2 * kc], 0u, zz[2 * kc + 1], 0u};
-                    mma_16816(Kb, a, qb[kc][0], qb[kc][1]);
+                for (int kc = 0; kc < 8; kc += 2) {
+                    const uint32_t a0[4] = {zz[2 * kc], 0u, zz[2 * kc + 1], 0u};
+                    const uint32_t a1[4] = {zz[2 * kc + 2], 0u, zz[2 * kc + 3], 0u};
+                    mma_16816(Kb, a0, qb[kc][0], qb[kc][1]);
+                    mma_16816(Kb2, a1, qb[kc + 1][0], qb[kc + 1][1]);
                 }
+#pragma unroll
+                for (int r = 0; r < 4; ++r) Kb[r] += Kb2[r];
             }
 
-            for (int j = 0; j < n; ++j) {
-                const uint8_t* page = buf + j * kPageBytes;
+            // ---- scores for the 4 pages, interleaved: S[j][t][h] = sum_c code * q'' ----
+            float S[kBatch][4];
+            uint4 kw[kBatch];
+#pragma unroll
+            for (int j = 0; j < kBatch; ++j) {
+                kw[j] = lds128(buf + j * kPageBytes + kKC + lane * 16);
+                S[j][0] = S[j][1] = S[j][2] = S[j][3] = 0.0f;
+            }
+#pragma unroll
+            for (int kc = 0; kc < 8; ++kc) {
+                const int sh = (kc < 3) ? 0 : ((kc < 6) ? 6 : 12);
+                const uint32_t mask = 0x00030003u << (2 * (kc % 3));
+#pragma unroll
+                for (int j = 0; j < kBatch; ++j) {
+                    const uint2 ks = lds64(buf + j * kPageBytes + kKS + tig * 64 + kc * 8);
+                    const uint32_t a[4] = {(kw[j].x >> sh) & mask, (kw[j].y >> sh) & mask,
+                                           (kw[j].z >> sh) & mask, (kw[j].w >> sh) & mask};
+                    mma_16816(S[j], a, hmul2_u32(qsc[kc][0], ks.x), hmul2_u32(qsc[kc][1], ks.y));
+                }
+            }
+            // ---- online softmax over the batch (log2 domain) ----
+            float x[kBatch][4];
+            float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+            for (int j = 0; j < kBatch; ++j) {
+                const float kb0 = __shfl_sync(0xffffffffu, Kb[0], 4 * j + tig) * sl2;
+                const float kb1 = __shfl_sync(0xffffffffu, Kb[1], 4 * j + tig) * sl2;
+                x[j][0] = fmaf(S[j][0], sk, kb0);
+                x[j][1] = fmaf(S[j][1], sk, kb1);
+                x[j][2] = fmaf(S[j][2], sk, kb0);
+                x[j][3] = fmaf(S[j][3], sk, kb1);
                 const int lp = pfirst + j;
-                // ---- scores S[t][h] = sum_c code[t][c] * q''[h][c] ----
-                const uint4 kw = lds128(page + kKC + lane * 16);
-                uint4 ksv[4];
-#pragma unroll
-                for (int r = 0; r < 4; ++r) ksv[r] = lds128(page + kKS + tig * 64 + 16 * r);
-                const uint32_t* ks = reinterpret_cast<const uint32_t*>(ksv);  // [kc][p]
-                const uint32_t w0[4] = {kw.x, kw.y, kw.z, kw.w};
-                const uint32_t w6[4] = {kw.x >> 6, kw.y >> 6, kw.z >> 6, kw.w >> 6};
-                const uint32_t w12[4] = {kw.x >> 12, kw.y >> 12, kw.z >> 12, kw.w >> 12};
-                float S[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-#pragma unroll
-                for (int kc = 0; kc < 8; ++kc) {
-                    const uint32_t* src = (kc < 3) ? w0 : ((kc < 6) ? w6 : w12);
-                    const uint32_t mask = 0x00030003u << (2 * (kc % 3));
-                    const uint32_t a[4] = {src[0] & mask, src[1] & mask, src[2] & mask, src[3] & mask};
-                    const uint32_t b0 = hmul2_u32(qs[kc][0], ks[2 * kc]);
-                    const uint32_t b1 = hmul2_u32(qs[kc][1], ks[2 * kc + 1]);
-                    mma_16816(S, a, b0, b1);
+                if (j >= n) {
+                    x[j][0] = x[j][1] = x[j][2] = x[j][3] = -INFINITY;
+                } else if (lp == partial_page) {
+                    if (gid >= partial_valid) { x[j][0] = -INFINITY; x[j][1] = -INFINITY; }
+                    if (gid + 8 >= partial_valid) { x[j][2] = -INFINITY; x[j][3] = -INFINITY; }
                 }
-                const float kb0 = __shfl_sync(0xffffffffu, Kb[0], 4 * j + tig);
-                const float kb1 = __shfl_sync(0xffffffffu, Kb[1], 4 * j + tig);
-                float x0 = fmaf(S[0], sk, kb0 * sl2);
-                float x1 = fmaf(S[1], sk, kb1 * sl2);
-                float x2 = fmaf(S[2], sk, kb0 * sl2);
-                float x3 = fmaf(S[3], sk, kb1 * sl2);
-                if (partial_valid != 0 && lp == prefill_pages - 1) {
-                    if (gid >= partial_valid) { x0 = -INFINITY; x1 = -INFINITY; }
-                    if (gid + 8 >= partial_valid) { x2 = -INFINITY; x3 = -INFINITY; }
-                }
-                // ---- online softmax (log2 domain) ----
-                float mx0 = fmaxf(x0, x2), mx1 = fmaxf(x1, x3);
+                mx0 = fmaxf(mx0, fmaxf(x[j][0], x[j][2]));
+                mx1 = fmaxf(mx1, fmaxf(x[j][1], x[j][3]));
+            }
 #pragma unroll
-                for (int o = 4; o < 32; o <<= 1) {
-                    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
-                    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
-                }
-                const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
-                if (__any_sync(0xffffffffu, (mn0 != m0) | (mn1 != m1))) {
-                    const float a0 = fast_exp2(m0 - mn0), a1 = fast_exp2(m1 - mn1);
-                    l0 *= a0; l1 *= a1;
-#pragma unroll
-                    for (int g = 0; g < 8; ++g) {
-                        O[g][0] *= a0; O[g][1] *= a1; O[g][2] *= a0; O[g][3] *= a1;
-                    }
-                    Dvb[0] *= a0; Dvb[1] *= a1;
-                    m0 = mn0; m1 = mn1;
-                }
-                const float p0 = fast_exp2(x0 - m0), p1 = fast_exp2(x1 - m1);
-                const float p2 = fast_exp2(x2 - m0), p3 = fast_exp2(x3 - m1);
-                l0 += p0 + p2;
-                l1 += p1 + p3;
-                const uint32_t pb0 = movmatrix_trans(pack_half2(p0, p1));
-                const uint32_t pb1 = movmatrix_trans(pack_half2(p2, p3));
-                // ---- value zero-point bias: Dvb[g][h] += sum_t z[t][g] p[h][t] ----
-                {
-                    const uint2 vz = lds64(page + kVZ + lane * 8);
-                    const uint32_t a[4] = {vz.x, 0u, vz.y, 0u};
-                    mma_16816(Dvb, a, pb0, pb1);
-                }
-                // ---- O_g[c][h] += sum_t code[t][c] * p[h][t] * s[t][g] ----
-                const uint4 vw = lds128(page + kVC + lane * 16);
-                uint4 vsv[4];
-#pragma unroll
-                for (int r = 0; r < 4; ++r) vsv[r] = lds128(page + kVS + tig * 64 + 16 * r);
-                const uint32_t* vs = reinterpret_cast<const uint32_t*>(vsv);  // [g][pt]
-                const uint32_t v0[4] = {vw.x, vw.y, vw.z, vw.w};
-                const uint32_t v6[4] = {vw.x >> 6, vw.y >> 6, vw.z >> 6, vw.w >> 6};
-                const uint32_t v12[4] = {vw.x >> 12, vw.y >> 12, vw.z >> 12, vw.w >> 12};
+            for (int o = 4; o < 32; o <<= 1) {
+                mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
+                mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
+            }
+            const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+            if (__any_sync(0xffffffffu, (mn0 != m0) | (mn1 != m1))) {
+                const float a0 = fast_exp2(m0 - mn0), a1 = fast_exp2(m1 - mn1);
+                l0 *= a0; l1 *= a1;
 #pragma unroll
                 for (int g = 0; g < 8; ++g) {
-                    const uint32_t* src = (g < 3) ? v0 : ((g < 6) ? v6 : v12);
-                    const uint32_t mask = 0x00030003u << (2 * (g % 3));
-                    const uint32_t a[4] = {src[0] & mask, src[1] & mask, src[2] & mask, src[3] & mask};
-                    const uint32_t b0 = hmul2_u32(pb0, vs[2 * g]);
-                    const uint32_t b1 = hmul2_u32(pb1, vs[2 * g + 1]);
-                    mma_16816(O[g], a, b0, b1);
+                    O[g][0] *= a0; O[g][1] *= a1; O[g][2] *= a0; O[g][3] *= a1;
+                }
+                Dvb[0] *= a0; Dvb[1] *= a1;
+                m0 = mn0; m1 = mn1;
+            }
+            uint32_t pb0[kBatch], pb1[kBatch];
+#pragma unroll
+            for (int j = 0; j < kBatch; ++j) {
+                const float p0 = fast_exp2(x[j][0] - m0), p1 = fast_exp2(x[j][1] - m1);
+                const float p2 = fast_exp2(x[j][2] - m0), p3 = fast_exp2(x[j][3] - m1);
+                l0 += p0 + p2;
+                l1 += p1 + p3;
+                pb0[j] = movmatrix_trans(pack_half2(p0, p1));
+                pb1[j] = movmatrix_trans(pack_half2(p2, p3));
+            }
+            // ---- values: Dvb[g][h] += sum_t z[t][g] p[h][t];  O_g[c][h] += sum_t code * p * s ----
+#pragma unroll
+            for (int j = 0; j < kBatch; ++j) {
+                if (j < n) {
+                    const uint8_t* page = buf + j * kPageBytes;
+                    const uint2 vz = lds64(page + kVZ + lane * 8);
+                    const uint32_t az[4] = {vz.x, 0u, vz.y, 0u};
+                    mma_16816(Dvb, az, pb0[j], pb1[j]);
+                    const uint4 vw = lds128(page + kVC + lane * 16);
+#pragma unroll
+                    for (int g = 0; g < 8; ++g) {
+                        const int sh = (g < 3) ? 0 : ((g < 6) ? 6 : 12);
+                        const uint32_t mask = 0x00030003u << (2 * (g % 3));
+                        const uint2 vs = lds64(page + kVS + tig * 64 + g * 8);
+                        const uint32_t a[4] = {(vw.x >> sh) & mask, (vw.y >> sh) & mask, (vw.z >> sh) & mask,
+                                               (vw.w >> sh) & mask};
+                        mma_16816(O[g], a, hmul2_u32(pb0[j], vs.x), hmul2_u32(pb1[j], vs.y));
+                    }
                 }
             }
             __syncwarp();
@@ -282,9 +279,12 @@ __global__ void __launch_bounds__(kPagesWarps * 32, 1) pages_kernel(const PagesP
             cg += n;
             if (++stage == kStages) { stage = 0; phase ^= 1u; }
         }
-        if (cg == uend_g) ++ci;
+        if (cg == uend_g) {
+            ++ci;
+            while (cg < end && __ldg(P.pref + ci + 1) == cg) ++ci;
+        }
 
-        // ---- segment epilogue: partial (m, l, o) for (warp wg, unit) ----
+        // ---- segment epilogue: partial (m, l, o) for slot (warp wg, unit) ----
 #pragma unroll
         for (int o = 4; o < 32; o <<= 1) {
             l0 += __shfl_xor_sync(0xffffffffu, l0, o);
@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(kPagesWarps * 32, 1) pages_kernel(const PagesP
         for (int g = 0; g < 8; ++g) {
             const float dv0 = __shfl_sync(0xffffffffu, Dvb[0], 4 * g + tig);
             const float dv1 = __shfl_sync(0xffffffffu, Dvb[1], 4 * g + tig);
-            const float f = kTwo24 * ((g % 3 == 0) ? 1.0f : ((g % 3 == 1) ? 0.25f : 0.0625f));
+            const float f = extract_scale(g);
             const int c = 16 * g + gid;
             if (h0 < G) {
                 po[h0 * kHeadDim + c] = fmaf(O[g][0], f, dv0);
@@ -313,31 +313,14 @@ __global__ void __launch_bounds__(kPagesWarps * 32, 1) pages_kernel(const PagesP
                 po[h1 * kHeadDim + c + 8] = fmaf(O[g][3], f, dv1);
             }
         }
-        __threadfence();
-        __syncwarp();
-        const int w_first = upre / P.chunk;
-        const int w_last = (uend_g - 1) / P.chunk;
-        int last = 0;
-        if (lane == 0) {
-            const int old = atomicAdd(P.counters + unit, 1);
-            last = (old == w_last - w_first);
-        }
-        last = __shfl_sync(0xffffffffu, last, 0);
-        if (last) {
-            __threadfence();
-            merge_unit(P, unit, w_first, w_last);
-            if (lane == 0) P.counters[unit] = 0;
-        }
     }
 }
 
 cudaError_t launch_pages(const PagesParams& p, int grid, cudaStream_t s) {
-    const size_t smem = (size_t)kPagesWarps * kStages * kBatch * kPageBytes +
-                        (size_t)kPagesWarps * kStages * sizeof(uint64_t);
+    const size_t smem = (size_t)kPagesWarps * kWarpSmem + (size_t)kPagesWarps * kStages * sizeof(uint64_t);
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(pages_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
+        cudaError_t e = cudaFuncSetAttribute(pages_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         configured = true;
     }
@@ -346,158 +329,271 @@ cudaError_t launch_pages(const PagesParams& p, int grid, cudaStream_t s) {
 }
 
 // ---------------------------------------------------------------------------
-// residual kernel: append (+flush) and attention over the fp16 residual
+// append kernel: decode_append with flush (flush steps only)
 // ---------------------------------------------------------------------------
-constexpr int kResThreads = 256;
-constexpr int kResRowStride = kHeadDim + 2;  // halves; odd word stride -> conflict-free row reads
+constexpr int kAppendThreads = 256;
 
-struct ResSmem {
-    union {
-        PageScratch scratch[kResThreads / 32];
-        struct {
-            __half k[128][kResRowStride];
-            __half v[128][kHeadDim];
-            float q[kMaxG][kHeadDim];
-            float s[kMaxG][128];
-            float red[kMaxG][2];
-        } att;
-    };
-};
-
-__global__ void __launch_bounds__(kResThreads) residual_kernel(const ResidualParams P) {
+__global__ void __launch_bounds__(kAppendThreads) append_kernel(const ResidualParams P) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
-    ResSmem& S = *reinterpret_cast<ResSmem*>(smem_raw);
+    PageScratch* scratch = reinterpret_cast<PageScratch*>(smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = lane_id();
     const int i = blockIdx.x;
     const int u = P.unit_begin + i;
     const int d = kHeadDim;
-    UnitMeta meta = P.meta[u];
+    const UnitMeta meta = P.meta[u];
     __half* rk = P.res_k + (size_t)u * P.n_r * d;
     __half* rv = P.res_v + (size_t)u * P.n_r * d;
-    int n = meta.n_res;
-
-    if (P.k_new) {  // decode_append (cache_engine.cpp:79-90)
-        if (tid < 16) {
-            reinterpret_cast<uint4*>(rk + (size_t)n * d)[tid] =
-                reinterpret_cast<const uint4*>(P.k_new + (size_t)i * d)[tid];
-        } else if (tid < 32) {
-            reinterpret_cast<uint4*>(rv + (size_t)n * d)[tid - 16] =
-                reinterpret_cast<const uint4*>(P.v_new + (size_t)i * d)[tid - 16];
-        }
-        ++n;
-        __threadfence_block();
-        __syncthreads();
+    const int n = meta.n_res + 1;
+    if (tid < 16) {
+        reinterpret_cast<uint4*>(rk + (size_t)meta.n_res * d)[tid] = reinterpret_cast<const uint4*>(P.k_new + (size_t)i * d)[tid];
+    } else if (tid < 32) {
+        reinterpret_cast<uint4*>(rv + (size_t)meta.n_res * d)[tid - 16] =
+            reinterpret_cast<const uint4*>(P.v_new + (size_t)i * d)[tid - 16];
     }
-    const bool flush = (n == P.n_r);
-    if (flush) {
-        // quantize the full block into n_r/16 new pages (store_block, cache_engine.cpp:34-52)
-        const int npg = P.n_r / kGroup;
-        bool ok = true;
-        for (int j = warp; j < npg; j += kResThreads / 32) {
-            PageScratch& ps = S.scratch[warp];
-            for (int e = lane; e < 16 * 16; e += 32) {
-                const int r = e >> 4, c16 = e & 15;
-                reinterpret_cast<uint4*>(ps.k[r])[c16] = reinterpret_cast<const uint4*>(rk + (size_t)(16 * j + r) * d)[c16];
-                reinterpret_cast<uint4*>(ps.v[r])[c16] = reinterpret_cast<const uint4*>(rv + (size_t)(16 * j + r) * d)[c16];
-            }
-            __syncwarp();
-            const int64_t page = meta.page_base + meta.n_pages + j;
-            ok &= build_page(ps, 16, P.pool + (size_t)page * kPageBytes,
-                             P.shadow ? P.shadow + (size_t)page * (kShadowBytes / 4) : nullptr);
-        }
-        if (!ok && lane == 0) atomicOr(P.status, kStatusNonFinite);
-        __syncthreads();
-        if (tid == 0) {
-            P.meta[u].n_pages = meta.n_pages + npg;
-            P.meta[u].n_res = 0;
-        }
-        meta.n_pages += npg;
-        n = 0;
-    } else if (P.k_new && tid == 0) {
-        P.meta[u].n_res = n;
-    }
-    if (!P.attend) return;
-
-    const int G = P.group;
-    float* rml = P.res_ml + (size_t)i * 2 * kMaxG;
-    float* ro = P.res_o + (size_t)i * kMaxG * d;
-    if (n == 0) {  // empty residual: neutral partial
-        if (tid < G) { rml[tid] = -INFINITY; rml[kMaxG + tid] = 0.0f; }
-        for (int e = tid; e < G * d; e += kResThreads) ro[(e / d) * d + (e % d)] = 0.0f;
+    __threadfence_block();
+    __syncthreads();
+    if (n < P.n_r) {
+        if (tid == 0) P.meta[u].n_res = n;
         return;
     }
-    // stage residual rows and q
-    for (int e = tid; e < n * 16; e += kResThreads) {
-        const int r = e >> 4, c16 = e & 15;
-        const uint4 kv = reinterpret_cast<const uint4*>(rk + (size_t)r * d)[c16];
-        const uint32_t* kw = reinterpret_cast<const uint32_t*>(&kv);
-        uint32_t* dst = reinterpret_cast<uint32_t*>(&S.att.k[r][c16 * 8]);
-        dst[0] = kw[0]; dst[1] = kw[1]; dst[2] = kw[2]; dst[3] = kw[3];
-        reinterpret_cast<uint4*>(S.att.v[r])[c16] = reinterpret_cast<const uint4*>(rv + (size_t)r * d)[c16];
+    // store_block (cache_engine.cpp:34-52): quantize the full block into n_r/16 pages
+    const int npg = P.n_r / kGroup;
+    bool ok = true;
+    for (int j = warp; j < npg; j += kAppendThreads / 32) {
+        PageScratch& ps = scratch[warp];
+        for (int e = lane; e < 16 * 16; e += 32) {
+            const int r = e >> 4, c16 = e & 15;
+            reinterpret_cast<uint4*>(ps.k[r])[c16] = reinterpret_cast<const uint4*>(rk + (size_t)(16 * j + r) * d)[c16];
+            reinterpret_cast<uint4*>(ps.v[r])[c16] = reinterpret_cast<const uint4*>(rv + (size_t)(16 * j + r) * d)[c16];
+        }
+        __syncwarp();
+        const int64_t page = meta.page_base + meta.n_pages + j;
+        ok &= build_page(ps, 16, P.pool + (size_t)page * kPageBytes,
+                         P.shadow ? P.shadow + (size_t)page * (kShadowBytes / 4) : nullptr);
     }
-    for (int e = tid; e < G * d; e += kResThreads)
-        S.att.q[e / d][e % d] = __half2float(P.q[(size_t)i * G * d + e]);
+    if (!ok && lane == 0) atomicOr(P.status, kStatusNonFinite);
     __syncthreads();
-    // scores (log2 domain)
-    for (int e = tid; e < n * G; e += kResThreads) {
-        const int t = e / G, h = e % G;
-        float acc = 0.0f;
-        const __half2* kr = reinterpret_cast<const __half2*>(S.att.k[t]);
-#pragma unroll 8
-        for (int c2 = 0; c2 < d / 2; ++c2) {
-            const float2 kf = __half22float2(kr[c2]);
-            acc = fmaf(S.att.q[h][2 * c2], kf.x, acc);
-            acc = fmaf(S.att.q[h][2 * c2 + 1], kf.y, acc);
-        }
-        S.att.s[h][t] = acc * P.scale_log2;
+    if (tid == 0) {
+        P.meta[u].n_pages = meta.n_pages + npg;
+        P.meta[u].n_res = 0;
     }
-    __syncthreads();
-    if (warp < G) {  // per-head max / exp / sum
-        const int h = warp;
-        float mx = -INFINITY;
-        for (int t = lane; t < n; t += 32) mx = fmaxf(mx, S.att.s[h][t]);
-        for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        float sum = 0.0f;
-        for (int t = lane; t < n; t += 32) {
-            const float p = fast_exp2(S.att.s[h][t] - mx);
-            S.att.s[h][t] = p;
-            sum += p;
-        }
-        for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-        if (lane == 0) { S.att.red[h][0] = mx; S.att.red[h][1] = sum; }
-    }
-    __syncthreads();
-    const bool final_out = (meta.n_pages == 0);
-    for (int e = tid; e < G * (d / 2); e += kResThreads) {
-        const int h = e / (d / 2), c2 = e % (d / 2);
-        float a0 = 0.0f, a1 = 0.0f;
-        for (int t = 0; t < n; ++t) {
-            const float p = S.att.s[h][t];
-            const float2 vf = __half22float2(reinterpret_cast<const __half2*>(S.att.v[t])[c2]);
-            a0 = fmaf(p, vf.x, a0);
-            a1 = fmaf(p, vf.y, a1);
-        }
-        if (final_out) {
-            const float inv = 1.0f / S.att.red[h][1];
-            reinterpret_cast<__half2*>(P.out + ((size_t)i * G + h) * d)[c2] = __floats2half2_rn(a0 * inv, a1 * inv);
-        } else {
-            ro[h * d + 2 * c2] = a0;
-            ro[h * d + 2 * c2 + 1] = a1;
-        }
-    }
-    if (tid < G) { rml[tid] = S.att.red[tid][0]; rml[kMaxG + tid] = S.att.red[tid][1]; }
 }
 
-cudaError_t launch_residual(const ResidualParams& p, cudaStream_t s) {
-    const size_t smem = sizeof(ResSmem);
+cudaError_t launch_append(const ResidualParams& p, cudaStream_t s) {
+    const size_t smem = sizeof(PageScratch) * (kAppendThreads / 32);
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(residual_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
+        cudaError_t e = cudaFuncSetAttribute(append_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    residual_kernel<<<p.n_units, kResThreads, smem, s>>>(p);
+    append_kernel<<<p.n_units, kAppendThreads, smem, s>>>(p);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// finish kernel: (append) + residual attention on tensor cores + split-K merge
+// ---------------------------------------------------------------------------
+constexpr int kFinishWarps = 8;  // one warp per 16-token residual tile (n_r <= 128)
+constexpr int kResStride = kHeadDim + 8;  // halves: 272-byte rows -> conflict-free fragment loads
+constexpr int kMaxPart = 16;     // page partials staged per merge pass
+
+struct FinishSmem {
+    __half k[128][kResStride];
+    __half v[128][kResStride];
+    __half q[kMaxG * kHeadDim];
+    float wml[kFinishWarps][2][kMaxG];
+    float wo[kFinishWarps][kMaxG][kHeadDim];
+    float pml[kMaxPart][2][kMaxG];
+    float po[kMaxPart][kMaxG][kHeadDim];
+    float M[kMaxG], L[kMaxG];
+};
+
+__device__ __forceinline__ void ldmatrix_x4_trans(uint32_t (&r)[4], const void* p) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(smem_u32(p)));
+}
+
+// async-stage page partials [w0, w0 + np) of local unit i (o rows for G heads + m/l)
+__device__ __forceinline__ void stage_partials(FinishSmem& S, const ResidualParams& P, int i, int w0, int np, int G,
+                                               int tid) {
+    const int per = G * kHeadDim / 4;  // float4 chunks per partial
+    for (int e = tid; e < np * per; e += blockDim.x) {
+        const int w = e / per, r = e % per;
+        cp_async16(reinterpret_cast<float4*>(&S.po[w][0][0]) + r,
+                   reinterpret_cast<const float4*>(P.part_o + (size_t)(w0 + w + i) * kMaxG * kHeadDim) + r);
+    }
+    for (int e = tid; e < np * 4; e += blockDim.x) {  // 2 * kMaxG floats = 4 x float4
+        const int w = e >> 2, r = e & 3;
+        cp_async16(reinterpret_cast<float4*>(&S.pml[w][0][0]) + r,
+                   reinterpret_cast<const float4*>(P.part_ml + (size_t)(w0 + w + i) * 2 * kMaxG) + r);
+    }
+}
+
+__global__ void __launch_bounds__(kFinishWarps * 32) finish_kernel(const ResidualParams P, const int32_t* __restrict__ pref,
+                                                                   int chunk) {
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    FinishSmem& S = *reinterpret_cast<FinishSmem*>(smem_raw);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = lane_id();
+    const int gid = lane >> 2, tig = lane & 3;
+    const int i = blockIdx.x;
+    const int u = P.unit_begin + i;
+    const int d = kHeadDim;
+    const int G = P.group;
+    const UnitMeta meta = P.meta[u];
+    __half* rk = P.res_k + (size_t)u * P.n_r * d;
+    __half* rv = P.res_v + (size_t)u * P.n_r * d;
+    const int n_old = meta.n_res;
+    const int upre = pref[i], uend = pref[i + 1];
+    const int w_first = upre / chunk, w_last = (uend > upre) ? (uend - 1) / chunk : w_first - 1;
+    const int n_part = w_last - w_first + 1;
+
+    // ---- one burst of async copies: residual rows, q, first kMaxPart page partials ----
+    for (int e = tid; e < n_old * 16; e += blockDim.x) {
+        const int r = e >> 4, c16 = e & 15;
+        cp_async16(&S.k[r][8 * c16], reinterpret_cast<const uint4*>(rk + (size_t)r * d) + c16);
+        cp_async16(&S.v[r][8 * c16], reinterpret_cast<const uint4*>(rv + (size_t)r * d) + c16);
+    }
+    for (int e = tid; e < G * d / 8; e += blockDim.x)
+        cp_async16(reinterpret_cast<uint4*>(S.q) + e, reinterpret_cast<const uint4*>(P.q + (size_t)i * G * d) + e);
+    stage_partials(S, P, i, w_first, min(n_part, kMaxPart), G, tid);
+    cp_async_commit();
+    // decode_append (cache_engine.cpp:79-90) -- the flush case was handled by append_kernel
+    int n = n_old;
+    if (P.k_new) {
+        if (tid < 16) {
+            const uint4 x = reinterpret_cast<const uint4*>(P.k_new + (size_t)i * d)[tid];
+            reinterpret_cast<uint4*>(rk + (size_t)n * d)[tid] = x;
+            *reinterpret_cast<uint4*>(&S.k[n][8 * tid]) = x;
+        } else if (tid < 32) {
+            const uint4 x = reinterpret_cast<const uint4*>(P.v_new + (size_t)i * d)[tid - 16];
+            reinterpret_cast<uint4*>(rv + (size_t)n * d)[tid - 16] = x;
+            *reinterpret_cast<uint4*>(&S.v[n][8 * (tid - 16)]) = x;
+        }
+        if (tid == 0) P.meta[u].n_res = n + 1;
+        ++n;
+    }
+    cp_async_wait_all();
+    __syncthreads();
+
+    // ---- residual tile attention: warp w owns tokens [16w, 16w + 16) ----
+    const int ntiles = (n + 15) >> 4;
+    const float sl2 = P.scale_log2;
+    if (warp < ntiles) {
+        const int t0 = 16 * warp;
+        uint32_t qb[8][2];
+#pragma unroll
+        for (int kc = 0; kc < 8; ++kc)
+#pragma unroll
+            for (int p = 0; p < 2; ++p)
+                qb[kc][p] = (gid < G) ? *reinterpret_cast<const uint32_t*>(S.q + gid * d + 16 * kc + 2 * tig + 8 * p) : 0u;
+        float Sx[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+        for (int kc = 0; kc < 8; ++kc) {
+            uint32_t a[4];
+            a[0] = *reinterpret_cast<const uint32_t*>(&S.k[t0 + gid][16 * kc + 2 * tig]);
+            a[1] = *reinterpret_cast<const uint32_t*>(&S.k[t0 + gid + 8][16 * kc + 2 * tig]);
+            a[2] = *reinterpret_cast<const uint32_t*>(&S.k[t0 + gid][16 * kc + 2 * tig + 8]);
+            a[3] = *reinterpret_cast<const uint32_t*>(&S.k[t0 + gid + 8][16 * kc + 2 * tig + 8]);
+            mma_16816(Sx, a, qb[kc][0], qb[kc][1]);
+        }
+        float x0 = Sx[0] * sl2, x1 = Sx[1] * sl2, x2 = Sx[2] * sl2, x3 = Sx[3] * sl2;
+        if (t0 + gid >= n) { x0 = -INFINITY; x1 = -INFINITY; }
+        if (t0 + gid + 8 >= n) { x2 = -INFINITY; x3 = -INFINITY; }
+        float mx0 = fmaxf(x0, x2), mx1 = fmaxf(x1, x3);
+#pragma unroll
+        for (int o = 4; o < 32; o <<= 1) {
+            mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
+            mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
+        }
+        const float p0 = fast_exp2(x0 - mx0), p1 = fast_exp2(x1 - mx1);
+        const float p2 = fast_exp2(x2 - mx0), p3 = fast_exp2(x3 - mx1);
+        float l0 = p0 + p2, l1 = p1 + p3;
+#pragma unroll
+        for (int o = 4; o < 32; o <<= 1) {
+            l0 += __shfl_xor_sync(0xffffffffu, l0, o);
+            l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+        }
+        const uint32_t pb0 = movmatrix_trans(pack_half2(p0, p1));
+        const uint32_t pb1 = movmatrix_trans(pack_half2(p2, p3));
+        // O[c][h] = sum_t V^T[c][t] P[t][h]; A fragments via ldmatrix.trans of V[t][c]:
+        // matrices m0 (t0-7, c0-7) m1 (t0-7, c8-15) m2 (t8-15, c0-7) m3 (t8-15, c8-15)
+        // = fragment registers a0 (c0-7, t0-7) a1 (c8-15, t0-7) a2 (c0-7, t8-15) a3 (c8-15, t8-15)
+        const int mi = lane >> 3, ri = lane & 7;
+        const int h0 = 2 * tig, h1 = 2 * tig + 1;
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+            uint32_t a[4];
+            ldmatrix_x4_trans(a, &S.v[t0 + ri + 8 * (mi >> 1)][16 * g + 8 * (mi & 1)]);
+            float o[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+            mma_16816(o, a, pb0, pb1);
+            const int c = 16 * g + gid;
+            if (h0 < G) { S.wo[warp][h0][c] = o[0]; S.wo[warp][h0][c + 8] = o[2]; }
+            if (h1 < G) { S.wo[warp][h1][c] = o[1]; S.wo[warp][h1][c + 8] = o[3]; }
+        }
+        if (gid == 0) {
+            if (h0 < G) { S.wml[warp][0][h0] = mx0; S.wml[warp][1][h0] = l0; }
+            if (h1 < G) { S.wml[warp][0][h1] = mx1; S.wml[warp][1][h1] = l1; }
+        }
+    }
+    __syncthreads();
+
+    // ---- split-K merge over residual tiles and page partials (staged in passes of kMaxPart) ----
+    if (tid < G) {
+        float M = -INFINITY;
+        for (int w = 0; w < ntiles; ++w) M = fmaxf(M, S.wml[w][0][tid]);
+        for (int w = w_first; w <= w_last; ++w) M = fmaxf(M, __ldcg(P.part_ml + (size_t)(w + i) * 2 * kMaxG + tid));
+        S.M[tid] = M;
+    }
+    __syncthreads();
+    // thread -> (h, c) pairs: G * d outputs / 256 threads
+    float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f}, lsum[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    const int nout = (G * d + blockDim.x - 1) / blockDim.x;  // 1..4
+    for (int r = 0; r < nout; ++r) {
+        const int e = min(tid + r * (int)blockDim.x, G * d - 1), h = e / d, c = e % d;
+        const float M = S.M[h];
+        for (int w = 0; w < ntiles; ++w) {
+            const float sc = fast_exp2(S.wml[w][0][h] - M);
+            acc[r] += S.wo[w][h][c] * sc;
+            lsum[r] += S.wml[w][1][h] * sc;
+        }
+    }
+    for (int w0 = w_first; w0 <= w_last; w0 += kMaxPart) {
+        const int np = min(kMaxPart, w_last - w0 + 1);
+        if (w0 != w_first) {
+            __syncthreads();
+            stage_partials(S, P, i, w0, np, G, tid);
+            cp_async_commit();
+            cp_async_wait_all();
+            __syncthreads();
+        }
+        for (int r = 0; r < nout; ++r) {
+            const int e = min(tid + r * (int)blockDim.x, G * d - 1), h = e / d, c = e % d;
+            const float M = S.M[h];
+#pragma unroll 4
+            for (int w = 0; w < np; ++w) {
+                const float sc = fast_exp2(S.pml[w][0][h] - M);
+                acc[r] += S.po[w][h][c] * sc;
+                lsum[r] += S.pml[w][1][h] * sc;
+            }
+        }
+    }
+    for (int r = 0; r < nout; ++r) {
+        const int e = tid + r * blockDim.x, h = e / d, c = e % d;
+        if (e < G * d) P.out[((size_t)i * G + h) * d + c] = __float2half_rn(acc[r] / lsum[r]);
+    }
+}
+
+cudaError_t launch_finish(const ResidualParams& p, const int32_t* pref, int chunk, cudaStream_t s) {
+    const size_t smem = sizeof(FinishSmem);
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    finish_kernel<<<p.n_units, kFinishWarps * 32, smem, s>>>(p, pref, chunk);
     return cudaGetLastError();
 }
 

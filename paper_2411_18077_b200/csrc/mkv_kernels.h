@@ -51,31 +51,28 @@ struct ResidualParams {
     __half* res_v;
     uint8_t* pool;
     float* shadow;
-    float* res_ml;        // [n_units][2][kMaxG]  (local unit index)
-    float* res_o;         // [n_units][kMaxG][d]
-    __half* out;          // final output when a unit has no pages
+    const float* part_ml; // page partials (pages_kernel), merged by finish_kernel
+    const float* part_o;
+    __half* out;          // [n_units][G][d]
     float scale_log2;
-    int attend;           // 0: append only
     uint32_t* status;
 };
-cudaError_t launch_residual(const ResidualParams& p, cudaStream_t s);
+cudaError_t launch_append(const ResidualParams& p, cudaStream_t s);
+cudaError_t launch_finish(const ResidualParams& p, const int32_t* pref, int chunk, cudaStream_t s);
 
 struct PagesParams {
     const uint8_t* pool;
     const UnitMeta* meta;
     int unit_begin, n_units, group;
     const __half* q;
-    const int32_t* pref;   // [n_units + 1] local page prefix
+    const int32_t* pref;    // [n_units + 1] local page prefix
+    const int32_t* wstart;  // [n_warps] first (non-empty) unit of each warp's page range
     int chunk, total_pages, n_warps;
-    float* part_ml;        // [slots][2][kMaxG]
-    float* part_o;         // [slots][kMaxG][d]
-    const float* res_ml;
-    const float* res_o;
-    int* counters;         // [n_units] local, zero between calls
-    __half* out;
+    float* part_ml;         // [slots][2][kMaxG]   slot = warp + unit
+    float* part_o;          // [slots][kMaxG][d]
     float scale_log2;
 };
-constexpr int kPagesWarps = 8;
+constexpr int kPagesWarps = 12;
 cudaError_t launch_pages(const PagesParams& p, int grid, cudaStream_t s);
 
 // ---- utilities (synth.cu) ----
