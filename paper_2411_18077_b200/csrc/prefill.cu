@@ -1,7 +1,449 @@
-// prefill.cu -- K1: two-pass selective flash-attention prefill (placeholder
-// until the tcgen05 kernel lands in the next commit).
+// prefill.cu -- K1: two-pass selective flash-attention prefill on tcgen05.
+//
+// Restates selective_flash_attn (attention.cpp:29-117) for [B, H, L, 128]
+// fp16 tensors with GQA:
+//   pass 1  attn_fwd_kernel   one CTA per (128-query tile, q-head, batch):
+//           online softmax over 128-key tiles -> X_O (fp16) and LSE (fp32,
+//           natural log, attention.cpp:98).  S = Q K^T and O += P V are
+//           tcgen05.mma (M = N = 128, K = 16 steps) with operands staged by TMA
+//           (SWIZZLE_128B) and accumulators in TMEM; P goes registers -> smem.
+//   pass 2  acumul_kernel     one CTA per (128-key block, kv-head, batch): the
+//           paper's column-parallel pass.  S^T = K_blk Q^T
+//           is recomputed on tcgen05 into TMEM, each thread owns ONE key row and
+//           sums exp(s - lse_q) over every visible query of every q-head of its
+//           kv-head, in a fixed order -> A_cumul[b, kv-head, key] with no atomics
+//           and memory linear in L (LSE + A_cumul only).
+// Causal convention: query i sees keys 0 .. lk - lq + i (attention.cpp:42,60);
+// masked pairs contribute exactly 0.
+//
+// Warp roles (192 threads): warps 0-3 softmax / exp (thread = TMEM lane = row),
+// warp 4 TMA producer, warp 5 TMEM allocator + single-thread MMA issuer.
+#include <cudaTypedefs.h>
+
 #include "mkv_kernels.h"
+#include "mkv_sm100.cuh"
 
 namespace mkv {
-cudaError_t launch_prefill_attn(const PrefillAttnParams&, cudaStream_t) { return cudaErrorNotSupported; }
+
+using namespace sm100;
+
+namespace {
+
+constexpr int kTile = 128;
+constexpr int kHalf = kTile * 128;   // one [128 rows x 64 fp16] swizzled TMA box = 16 KB
+constexpr int kTileB = 2 * kHalf;    // [128 x 128] fp16 tile = 32 KB
+constexpr int kThreads = 192;
+constexpr uint32_t kIdescS = idesc_f16(128, 128, false);   // S = A[K-major] * B[K-major]
+constexpr uint32_t kIdescPV = idesc_f16(128, 128, true);   // O += P[K-major] * V[MN-major]
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+constexpr float kRescaleThreshold = 8.0f;  // lazy rescale (log2 units): P <= 2^8 in fp16
+
+__device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
+    return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
+}
+
+// k-th K=16 slice of a K-major [128 x 128] fp16 tile made of two 64-column swizzled halves
+__device__ __forceinline__ uint64_t kslice(const uint8_t* tile, int k) {
+    return desc_kmajor_sw128(smem_u32(tile + (k >> 2) * kHalf + (k & 3) * 32));
+}
+
+// ---------------------------------------------------------------------------
+// pass 1
+// ---------------------------------------------------------------------------
+struct FwdBars {
+    uint64_t q_full, kv_full[2], kv_empty[2], s_full[2], s_free[2], p_full, o_done;
+    uint32_t tmem;
+};
+constexpr int kFwdSmem = 6 * kTileB + 1024 + 256;  // Q, K[2], V[2], P + alignment slack + barriers
+
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_fwd_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
+                    const __grid_constant__ CUtensorMap tv, const PrefillAttnParams P) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* sm = align1024(smem_raw);
+    uint8_t* sQ = sm;
+    uint8_t* sK = sm + kTileB;       // 2 stages
+    uint8_t* sV = sm + 3 * kTileB;   // 2 stages
+    uint8_t* sP = sm + 5 * kTileB;
+    FwdBars& B = *reinterpret_cast<FwdBars*>(sm + 6 * kTileB);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int n_qt = (P.lq + kTile - 1) / kTile;
+    const int qt = n_qt - 1 - blockIdx.x;  // longest causal rows first
+    const int hq = blockIdx.y, b = blockIdx.z;
+    const int G = P.hq / P.hkv;
+    const int hk = hq / G;
+    const int q0 = qt * kTile;
+    const int offset = P.causal ? P.lk - P.lq : 0;
+    const int last_row = min(q0 + kTile, P.lq) - 1;
+    const int kmax = P.causal ? min(P.lk - 1, offset + last_row) : P.lk - 1;
+    const int n_kv = kmax / kTile + 1;
+
+    if (warp == 5) {
+        tmem_alloc(&B.tmem, 512);
+        tmem_relinquish();
+    }
+    if (tid == 128) {
+        mbar_init(&B.q_full, 1);
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&B.kv_full[s], 1);
+            mbar_init(&B.kv_empty[s], 1);
+            mbar_init(&B.s_full[s], 1);
+            mbar_init(&B.s_free[s], 128);
+        }
+        mbar_init(&B.p_full, 128);
+        mbar_init(&B.o_done, 1);
+        fence_mbar_init();
+        tma_prefetch_desc(&tq);
+        tma_prefetch_desc(&tk);
+        tma_prefetch_desc(&tv);
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = B.tmem;
+
+    if (warp == 4) {
+        // ---------------- TMA producer ----------------
+        if (lane == 0) {
+            mbar_expect_tx(&B.q_full, kTileB);
+            tma_load_4d(sQ, &tq, 0, q0, hq, b, &B.q_full);
+            tma_load_4d(sQ + kHalf, &tq, 64, q0, hq, b, &B.q_full);
+            for (int j = 0; j < n_kv; ++j) {
+                const int s = j & 1;
+                if (j >= 2) mbar_wait(&B.kv_empty[s], ((j >> 1) - 1) & 1);
+                mbar_expect_tx(&B.kv_full[s], 2 * kTileB);
+                uint8_t* k_dst = sK + s * kTileB;
+                uint8_t* v_dst = sV + s * kTileB;
+                tma_load_4d(k_dst, &tk, 0, j * kTile, hk, b, &B.kv_full[s]);
+                tma_load_4d(k_dst + kHalf, &tk, 64, j * kTile, hk, b, &B.kv_full[s]);
+                tma_load_4d(v_dst, &tv, 0, j * kTile, hk, b, &B.kv_full[s]);
+                tma_load_4d(v_dst + kHalf, &tv, 64, j * kTile, hk, b, &B.kv_full[s]);
+            }
+        }
+    } else if (warp == 5) {
+        // ---------------- MMA issuer ----------------
+        if (lane == 0) {
+            auto pv = [&](int jj) {
+                mbar_wait(&B.p_full, jj & 1);
+                tc_fence_after();
+                const uint8_t* v = sV + (jj & 1) * kTileB;
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    umma_f16(tmem + 256, kslice(sP, k), desc_mnmajor_sw128(smem_u32(v + k * 2048), kHalf), kIdescPV,
+                             (jj > 0 || k > 0) ? 1u : 0u);
+                umma_commit(&B.o_done);
+                umma_commit(&B.kv_empty[jj & 1]);
+            };
+            mbar_wait(&B.q_full, 0);
+            for (int j = 0; j < n_kv; ++j) {
+                const int s = j & 1;
+                mbar_wait(&B.kv_full[s], (j >> 1) & 1);
+                if (j >= 2) mbar_wait(&B.s_free[s], ((j >> 1) - 1) & 1);
+                tc_fence_after();
+                const uint8_t* k = sK + s * kTileB;
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+                    umma_f16(tmem + 128 * s, kslice(sQ, kk), kslice(k, kk), kIdescS, kk > 0 ? 1u : 0u);
+                umma_commit(&B.s_full[s]);
+                if (j >= 1) pv(j - 1);
+            }
+            pv(n_kv - 1);
+        }
+    } else {
+        // ---------------- softmax warps: thread = query row ----------------
+        const int r = tid;
+        const int row_g = q0 + r;
+        const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+        const float sl2 = P.scale * kLog2e;
+        const int lim = P.causal ? min(P.lk - 1, offset + row_g) : P.lk - 1;
+        float m = -INFINITY, l = 0.0f;
+        for (int j = 0; j < n_kv; ++j) {
+            const int s = j & 1;
+            mbar_wait(&B.s_full[s], (j >> 1) & 1);
+            tc_fence_after();
+            uint32_t x[128];
+            tmem_ld32(trow + 128 * s + 0, *reinterpret_cast<uint32_t(*)[32]>(x + 0));
+            tmem_ld32(trow + 128 * s + 32, *reinterpret_cast<uint32_t(*)[32]>(x + 32));
+            tmem_ld32(trow + 128 * s + 64, *reinterpret_cast<uint32_t(*)[32]>(x + 64));
+            tmem_ld32(trow + 128 * s + 96, *reinterpret_cast<uint32_t(*)[32]>(x + 96));
+            tmem_wait_ld();
+            tc_fence_before();
+            mbar_arrive(&B.s_free[s]);
+            const int cut = lim - j * kTile;  // columns c > cut are masked
+            float mt = -INFINITY;
+#pragma unroll
+            for (int c = 0; c < 128; ++c) {
+                float v = __uint_as_float(x[c]) * sl2;
+                if (c > cut) v = -INFINITY;
+                x[c] = __float_as_uint(v);
+                mt = fmaxf(mt, v);
+            }
+            const float m_new = fmaxf(m, mt);
+            float alpha = 1.0f;
+            bool rescale = false;
+            if (m == -INFINITY) {
+                m = m_new;  // nothing accumulated yet for this row (all earlier P were 0)
+            } else if (m_new > m + kRescaleThreshold) {
+                alpha = fast_exp2(m - m_new);
+                m = m_new;
+                l *= alpha;
+                rescale = true;
+            }
+            uint32_t pk[64];
+            float ls = 0.0f;
+#pragma unroll
+            for (int c = 0; c < 128; c += 2) {
+                const float p0 = fast_exp2(__uint_as_float(x[c]) - m);
+                const float p1 = fast_exp2(__uint_as_float(x[c + 1]) - m);
+                ls += p0 + p1;
+                pk[c >> 1] = pack_half2(p0, p1);
+            }
+            l += ls;
+            if (j >= 1) mbar_wait(&B.o_done, (j - 1) & 1);  // PV(j-1) done: P buffer free, O stable
+            // tcgen05.ld/st are warp-collective (.sync.aligned): rescale warp-uniformly, alpha = 1 elsewhere
+            if (__any_sync(0xffffffffu, rescale)) {
+                tc_fence_after();
+#pragma unroll
+                for (int cc = 0; cc < 4; ++cc) {
+                    uint32_t o[32];
+                    tmem_ld32(trow + 256 + 32 * cc, o);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+                    tmem_st32(trow + 256 + 32 * cc, o);
+                }
+                tmem_wait_st();
+            }
+            // P row -> smem, K-major SWIZZLE_128B: 16-byte chunk c of row r at chunk c ^ (r & 7)
+#pragma unroll
+            for (int cc = 0; cc < 16; ++cc) {
+                const int h = cc >> 3, c = cc & 7;
+                uint4 v = make_uint4(pk[4 * cc], pk[4 * cc + 1], pk[4 * cc + 2], pk[4 * cc + 3]);
+                *reinterpret_cast<uint4*>(sP + h * kHalf + r * 128 + ((c ^ (r & 7)) << 4)) = v;
+            }
+            fence_proxy_async_smem();
+            tc_fence_before();
+            mbar_arrive(&B.p_full);
+        }
+        // ---------------- epilogue ----------------
+        mbar_wait(&B.o_done, (n_kv - 1) & 1);
+        tc_fence_after();
+        const float inv = 1.0f / l;
+        const bool valid = row_g < P.lq;
+        __half* orow = P.out + (size_t)b * P.o_sb + (size_t)hq * P.o_sh + (size_t)row_g * P.o_st;
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+            uint32_t o[32];
+            tmem_ld32(trow + 256 + 32 * cc, o);
+            tmem_wait_ld();
+            if (valid) {
+#pragma unroll
+                for (int e = 0; e < 32; e += 8) {
+                    uint4 v;
+                    v.x = pack_half2(__uint_as_float(o[e]) * inv, __uint_as_float(o[e + 1]) * inv);
+                    v.y = pack_half2(__uint_as_float(o[e + 2]) * inv, __uint_as_float(o[e + 3]) * inv);
+                    v.z = pack_half2(__uint_as_float(o[e + 4]) * inv, __uint_as_float(o[e + 5]) * inv);
+                    v.w = pack_half2(__uint_as_float(o[e + 6]) * inv, __uint_as_float(o[e + 7]) * inv);
+                    *reinterpret_cast<uint4*>(orow + 32 * cc + e) = v;
+                }
+            }
+        }
+        if (valid) P.lse[((size_t)b * P.hq + hq) * P.lq + row_g] = (m + __log2f(l)) * kLn2;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 5) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// pass 2: column-parallel A_cumul
+// ---------------------------------------------------------------------------
+constexpr int kQStages = 3;
+struct AcBars {
+    uint64_t k_full, q_full[kQStages], q_empty[kQStages], s_full[2], s_free[2];
+    uint32_t tmem;
+    float lse2[2][kTile];
+};
+constexpr int kAcSmem = (1 + kQStages) * kTileB + 1024 + (int)sizeof(AcBars) + 64;
+
+__global__ void __launch_bounds__(kThreads, 1)
+    acumul_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
+                  const PrefillAttnParams P) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* sm = align1024(smem_raw);
+    uint8_t* sK = sm;
+    uint8_t* sQ = sm + kTileB;  // kQStages stages
+    AcBars& B = *reinterpret_cast<AcBars*>(sm + (1 + kQStages) * kTileB);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int kt = blockIdx.x, hk = blockIdx.y, b = blockIdx.z;
+    const int G = P.hq / P.hkv;
+    const int key0 = kt * kTile;
+    const int offset = P.causal ? P.lk - P.lq : 0;
+    const int n_qt = (P.lq + kTile - 1) / kTile;
+    const int i_min = P.causal ? max(0, key0 - offset) : 0;  // first query that sees any key of the block
+    const int t_first = i_min / kTile;
+    const int per_head = n_qt - t_first;
+    const int n_items = G * per_head;
+
+    if (warp == 5) {
+        tmem_alloc(&B.tmem, 256);
+        tmem_relinquish();
+    }
+    if (tid == 128) {
+        mbar_init(&B.k_full, 1);
+        for (int s = 0; s < kQStages; ++s) {
+            mbar_init(&B.q_full[s], 1);
+            mbar_init(&B.q_empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&B.s_full[s], 1);
+            mbar_init(&B.s_free[s], 128);
+        }
+        fence_mbar_init();
+        tma_prefetch_desc(&tq);
+        tma_prefetch_desc(&tk);
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = B.tmem;
+
+    if (warp == 4) {
+        if (lane == 0) {
+            mbar_expect_tx(&B.k_full, kTileB);
+            tma_load_4d(sK, &tk, 0, key0, hk, b, &B.k_full);
+            tma_load_4d(sK + kHalf, &tk, 64, key0, hk, b, &B.k_full);
+            for (int it = 0; it < n_items; ++it) {
+                const int s = it % kQStages;
+                if (it >= kQStages) mbar_wait(&B.q_empty[s], ((it / kQStages) - 1) & 1);
+                const int g = it / per_head, t = t_first + it % per_head;
+                const int hq = hk * G + g;
+                mbar_expect_tx(&B.q_full[s], kTileB);
+                tma_load_4d(sQ + s * kTileB, &tq, 0, t * kTile, hq, b, &B.q_full[s]);
+                tma_load_4d(sQ + s * kTileB + kHalf, &tq, 64, t * kTile, hq, b, &B.q_full[s]);
+            }
+        }
+    } else if (warp == 5) {
+        if (lane == 0) {
+            mbar_wait(&B.k_full, 0);
+            for (int it = 0; it < n_items; ++it) {
+                const int s = it % kQStages, bb = it & 1;
+                mbar_wait(&B.q_full[s], (it / kQStages) & 1);
+                if (it >= 2) mbar_wait(&B.s_free[bb], ((it >> 1) - 1) & 1);
+                tc_fence_after();
+                const uint8_t* q = sQ + s * kTileB;
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+                    umma_f16(tmem + 128 * bb, kslice(sK, kk), kslice(q, kk), kIdescS, kk > 0 ? 1u : 0u);
+                umma_commit(&B.s_full[bb]);
+                umma_commit(&B.q_empty[s]);
+            }
+        }
+    } else {
+        // thread = key row; fixed accumulation order (items in order, columns in order)
+        const int kr = tid;
+        const int kj = key0 + kr;
+        const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+        const float sl2 = P.scale * kLog2e;
+        float acc = 0.0f;
+        for (int it = 0; it < n_items; ++it) {
+            const int g = it / per_head, t = t_first + it % per_head;
+            const int hq = hk * G + g;
+            const int bb = it & 1;
+            {
+                const int i = t * kTile + tid;
+                B.lse2[bb][tid] = (i < P.lq) ? P.lse[((size_t)b * P.hq + hq) * P.lq + i] * kLog2e : INFINITY;
+            }
+            named_bar_sync(1, 128);
+            mbar_wait(&B.s_full[bb], (it >> 1) & 1);
+            tc_fence_after();
+            // query i = t*128 + c visible iff kj <= offset + i  <=>  c >= kj - offset - t*128
+            const int c_min = P.causal ? (kj - offset - t * kTile) : -1;
+            float part = 0.0f;
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+                uint32_t x[64];
+                tmem_ld32(trow + 128 * bb + 64 * half, *reinterpret_cast<uint32_t(*)[32]>(x));
+                tmem_ld32(trow + 128 * bb + 64 * half + 32, *reinterpret_cast<uint32_t(*)[32]>(x + 32));
+                tmem_wait_ld();
+#pragma unroll
+                for (int c = 0; c < 64; ++c) {
+                    const int col = 64 * half + c;
+                    const float v = fmaf(__uint_as_float(x[c]), sl2, -B.lse2[bb][col]);
+                    const float e = fast_exp2(v);
+                    part += (col >= c_min) ? e : 0.0f;
+                }
+            }
+            acc += part;
+            tc_fence_before();
+            mbar_arrive(&B.s_free[bb]);
+        }
+        if (kj < P.lk) P.a_cumul[((size_t)b * P.hkv + hk) * P.lk + kj] = acc;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 5) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 256);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host: TMA descriptors + launches
+// ---------------------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 get_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+bool make_map(CUtensorMap* m, const __half* base, int64_t sb, int64_t sh, int64_t st, int L, int H, int Bn) {
+    auto enc = get_encoder();
+    if (!enc) return false;
+    cuuint64_t dims[4] = {128, (cuuint64_t)L, (cuuint64_t)H, (cuuint64_t)Bn};
+    cuuint64_t strides[3] = {(cuuint64_t)st * 2, (cuuint64_t)sh * 2, (cuuint64_t)sb * 2};
+    cuuint32_t box[4] = {64, 128, 1, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<__half*>(base), dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+cudaError_t launch_prefill_attn(const PrefillAttnParams& p, cudaStream_t s) {
+    CUtensorMap tq, tk, tv;
+    if (!make_map(&tq, p.q, p.q_sb, p.q_sh, p.q_st, p.lq, p.hq, p.batch) ||
+        !make_map(&tk, p.k, p.k_sb, p.k_sh, p.k_st, p.lk, p.hkv, p.batch) ||
+        !make_map(&tv, p.v, p.v_sb, p.v_sh, p.v_st, p.lk, p.hkv, p.batch))
+        return cudaErrorInvalidValue;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFwdSmem);
+        if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(acumul_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kAcSmem);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    const int n_qt = (p.lq + kTile - 1) / kTile, n_kt = (p.lk + kTile - 1) / kTile;
+    attn_fwd_kernel<<<dim3(n_qt, p.hq, p.batch), kThreads, kFwdSmem, s>>>(tq, tk, tv, p);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    acumul_kernel<<<dim3(n_kt, p.hkv, p.batch), kThreads, kAcSmem, s>>>(tq, tk, p);
+    return cudaGetLastError();
+}
+
 }  // namespace mkv
