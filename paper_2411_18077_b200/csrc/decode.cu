@@ -70,6 +70,24 @@ __device__ __forceinline__ void load_q_frags(const __half* qs_smem, int G, int g
     }
 }
 
+// launch with programmatic dependent launch (PDL): the kernel may start while the
+// previous kernel on the stream drains; it must execute griddepcontrol.wait before
+// touching that kernel's outputs.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -91,20 +109,29 @@ __global__ void __launch_bounds__(kPagesWarps * 32, 1) pages_kernel(const PagesP
     const int G = P.group;
     const int qchunks = G * kHeadDim * 2 / 16;
 
-    int ci = __ldg(P.wstart + wg);  // first unit of this warp's range (host plan)
+    int ci = 0;
     auto prefetch_q = [&](int unit) {
         const uint8_t* src = reinterpret_cast<const uint8_t*>(P.q + (size_t)unit * G * kHeadDim);
         for (int e = lane; e < qchunks; e += 32) cp_async16(reinterpret_cast<uint8_t*>(qsm) + 16 * e, src + 16 * e);
         cp_async_commit();
     };
-    prefetch_q(ci);
 
+    // zero the ring once: slots past a short batch then hold finite stale data, so the
+    // batch body runs branch-free (invalid pages are masked with selects, not branches)
+    for (int e = lane; e < kStages * kBatch * kPageBytes / 16; e += 32)
+        reinterpret_cast<uint4*>(ring)[e] = make_uint4(0, 0, 0, 0);
+    fence_proxy_async_smem();
     if (lane == 0) {
         for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
         fence_mbar_init();
     }
     __syncwarp();
+    // PDL: everything above overlapped the previous kernel's tail; inputs are read below
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 
+    ci = __ldg(P.wstart + wg);  // first unit of this warp's range (host plan)
+    prefetch_q(ci);
     // ---- producer cursor (warp-uniform) ----
     int pi = ci;
     int pg = start;
@@ -168,13 +195,9 @@ __global__ void __launch_bounds__(kPagesWarps * 32, 1) pages_kernel(const PagesP
             float Kb[4] = {0.0f, 0.0f, 0.0f, 0.0f}, Kb2[4] = {0.0f, 0.0f, 0.0f, 0.0f};
             {
                 uint4 z[4];
-                const bool zv = gid < n;
-                const uint8_t* zp = buf + (zv ? gid : 0) * kPageBytes + kKZ + tig * 64;
+                const uint8_t* zp = buf + (gid & (kBatch - 1)) * kPageBytes + kKZ + tig * 64;
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    z[j] = lds128(zp + 16 * j);
-                    if (!zv) z[j] = make_uint4(0, 0, 0, 0);
-                }
+                for (int j = 0; j < 4; ++j) z[j] = lds128(zp + 16 * j);  // rows >= kBatch: unused
                 const uint32_t* zz = reinterpret_cast<const uint32_t*>(z);
 #pragma unroll
                 for (int kc = 0; kc < 8; kc += 2) {
@@ -208,6 +231,7 @@ __global__ void __launch_bounds__(kPagesWarps * 32, 1) pages_kernel(const PagesP
                 }
             }
             // ---- online softmax over the batch (log2 domain) ----
+            const bool special = (n < kBatch) || (partial_page >= pfirst && partial_page < pfirst + n);
             float x[kBatch][4];
             float mx0 = -INFINITY, mx1 = -INFINITY;
 #pragma unroll
@@ -218,12 +242,11 @@ __global__ void __launch_bounds__(kPagesWarps * 32, 1) pages_kernel(const PagesP
                 x[j][1] = fmaf(S[j][1], sk, kb1);
                 x[j][2] = fmaf(S[j][2], sk, kb0);
                 x[j][3] = fmaf(S[j][3], sk, kb1);
-                const int lp = pfirst + j;
-                if (j >= n) {
-                    x[j][0] = x[j][1] = x[j][2] = x[j][3] = -INFINITY;
-                } else if (lp == partial_page) {
-                    if (gid >= partial_valid) { x[j][0] = -INFINITY; x[j][1] = -INFINITY; }
-                    if (gid + 8 >= partial_valid) { x[j][2] = -INFINITY; x[j][3] = -INFINITY; }
+                if (special) {
+                    const int lp = pfirst + j;
+                    const int valid = (j >= n) ? 0 : ((lp == partial_page) ? partial_valid : 16);
+                    if (gid >= valid) { x[j][0] = -INFINITY; x[j][1] = -INFINITY; }
+                    if (gid + 8 >= valid) { x[j][2] = -INFINITY; x[j][3] = -INFINITY; }
                 }
                 mx0 = fmaxf(mx0, fmaxf(x[j][0], x[j][2]));
                 mx1 = fmaxf(mx1, fmaxf(x[j][1], x[j][3]));
@@ -257,21 +280,19 @@ __global__ void __launch_bounds__(kPagesWarps * 32, 1) pages_kernel(const PagesP
             // ---- values: Dvb[g][h] += sum_t z[t][g] p[h][t];  O_g[c][h] += sum_t code * p * s ----
 #pragma unroll
             for (int j = 0; j < kBatch; ++j) {
-                if (j < n) {
-                    const uint8_t* page = buf + j * kPageBytes;
-                    const uint2 vz = lds64(page + kVZ + lane * 8);
-                    const uint32_t az[4] = {vz.x, 0u, vz.y, 0u};
-                    mma_16816(Dvb, az, pb0[j], pb1[j]);
-                    const uint4 vw = lds128(page + kVC + lane * 16);
+                const uint8_t* page = buf + j * kPageBytes;
+                const uint2 vz = lds64(page + kVZ + lane * 8);
+                const uint32_t az[4] = {vz.x, 0u, vz.y, 0u};
+                mma_16816(Dvb, az, pb0[j], pb1[j]);
+                const uint4 vw = lds128(page + kVC + lane * 16);
 #pragma unroll
-                    for (int g = 0; g < 8; ++g) {
-                        const int sh = (g < 3) ? 0 : ((g < 6) ? 6 : 12);
-                        const uint32_t mask = 0x00030003u << (2 * (g % 3));
-                        const uint2 vs = lds64(page + kVS + tig * 64 + g * 8);
-                        const uint32_t a[4] = {(vw.x >> sh) & mask, (vw.y >> sh) & mask, (vw.z >> sh) & mask,
-                                               (vw.w >> sh) & mask};
-                        mma_16816(O[g], a, hmul2_u32(pb0[j], vs.x), hmul2_u32(pb1[j], vs.y));
-                    }
+                for (int g = 0; g < 8; ++g) {
+                    const int sh = (g < 3) ? 0 : ((g < 6) ? 6 : 12);
+                    const uint32_t mask = 0x00030003u << (2 * (g % 3));
+                    const uint2 vs = lds64(page + kVS + tig * 64 + g * 8);
+                    const uint32_t a[4] = {(vw.x >> sh) & mask, (vw.y >> sh) & mask, (vw.z >> sh) & mask,
+                                           (vw.w >> sh) & mask};
+                    mma_16816(O[g], a, hmul2_u32(pb0[j], vs.x), hmul2_u32(pb1[j], vs.y));
                 }
             }
             __syncwarp();
@@ -324,8 +345,7 @@ cudaError_t launch_pages(const PagesParams& p, int grid, cudaStream_t s) {
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    pages_kernel<<<grid, kPagesWarps * 32, smem, s>>>(p);
-    return cudaGetLastError();
+    return launch_pdl(pages_kernel, dim3(grid), dim3(kPagesWarps * 32), smem, s, p);
 }
 
 // ---------------------------------------------------------------------------
@@ -457,7 +477,6 @@ __global__ void __launch_bounds__(kFinishWarps * 32) finish_kernel(const Residua
     }
     for (int e = tid; e < G * d / 8; e += blockDim.x)
         cp_async16(reinterpret_cast<uint4*>(S.q) + e, reinterpret_cast<const uint4*>(P.q + (size_t)i * G * d) + e);
-    stage_partials(S, P, i, w_first, min(n_part, kMaxPart), G, tid);
     cp_async_commit();
     // decode_append (cache_engine.cpp:79-90) -- the flush case was handled by append_kernel
     int n = n_old;
@@ -537,6 +556,11 @@ __global__ void __launch_bounds__(kFinishWarps * 32) finish_kernel(const Residua
             if (h1 < G) { S.wml[warp][0][h1] = mx1; S.wml[warp][1][h1] = l1; }
         }
     }
+    // PDL: the residual part above overlapped the page kernel; its partials are read below
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    stage_partials(S, P, i, w_first, min(n_part, kMaxPart), G, tid);
+    cp_async_commit();
+    cp_async_wait_all();
     __syncthreads();
 
     // ---- split-K merge over residual tiles and page partials (staged in passes of kMaxPart) ----
@@ -593,8 +617,7 @@ cudaError_t launch_finish(const ResidualParams& p, const int32_t* pref, int chun
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    finish_kernel<<<p.n_units, kFinishWarps * 32, smem, s>>>(p, pref, chunk);
-    return cudaGetLastError();
+    return launch_pdl(finish_kernel, dim3(p.n_units), dim3(kFinishWarps * 32), smem, s, p, pref, chunk);
 }
 
 }  // namespace mkv
