@@ -264,14 +264,29 @@ __global__ void __launch_bounds__(kThreads, 1)
 // pass 2: column-parallel A_cumul
 // ---------------------------------------------------------------------------
 constexpr int kQStages = 3;
+constexpr int kAcThreads = 320;  // warps 0-7: two exp warpgroups (even / odd items), 8: TMA, 9: MMA
 struct AcBars {
     uint64_t k_full, q_full[kQStages], q_empty[kQStages], s_full[2], s_free[2];
     uint32_t tmem;
-    float lse2[2][kTile];
+    float lse2[2][2][kTile];  // [warpgroup][item parity][query]
+    float acc1[kTile];        // warpgroup 1 partial sums
 };
 constexpr int kAcSmem = (1 + kQStages) * kTileB + 1024 + (int)sizeof(AcBars) + 64;
 
-__global__ void __launch_bounds__(kThreads, 1)
+// exp2 on the FMA pipe (offloads the MUFU unit): round-to-nearest split x = j + f,
+// f in [-0.5, 0.5], 2^f by a degree-4 polynomial (rel. err < 5e-5), 2^j into the exponent.
+__device__ __forceinline__ float exp2_fma(float x) {
+    x = fmaxf(x, -127.0f);
+    const float xr = x + 12582912.0f;  // 1.5 * 2^23: rounds x to an integer in the low mantissa bits
+    const float f = x - (xr - 12582912.0f);
+    float p = fmaf(0.0096181291f, f, 0.0555041087f);
+    p = fmaf(p, f, 0.2402265070f);
+    p = fmaf(p, f, 0.6931471806f);
+    p = fmaf(p, f, 1.0f);
+    return __int_as_float(__float_as_int(p) + ((__float_as_int(xr) - 0x4B400000) << 23));
+}
+
+__global__ void __launch_bounds__(kAcThreads, 1)
     acumul_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                   const PrefillAttnParams P) {
     extern __shared__ uint8_t smem_raw[];
@@ -291,11 +306,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int per_head = n_qt - t_first;
     const int n_items = G * per_head;
 
-    if (warp == 5) {
+    if (warp == 9) {
         tmem_alloc(&B.tmem, 256);
         tmem_relinquish();
     }
-    if (tid == 128) {
+    if (tid == 256) {
         mbar_init(&B.k_full, 1);
         for (int s = 0; s < kQStages; ++s) {
             mbar_init(&B.q_full[s], 1);
@@ -314,7 +329,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     const uint32_t tmem = B.tmem;
 
-    if (warp == 4) {
+    if (warp == 8) {
         if (lane == 0) {
             mbar_expect_tx(&B.k_full, kTileB);
             tma_load_4d(sK, &tk, 0, key0, hk, b, &B.k_full);
@@ -329,7 +344,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tma_load_4d(sQ + s * kTileB + kHalf, &tq, 64, t * kTile, hq, b, &B.q_full[s]);
             }
         }
-    } else if (warp == 5) {
+    } else if (warp == 9) {
         if (lane == 0) {
             mbar_wait(&B.k_full, 0);
             for (int it = 0; it < n_items; ++it) {
@@ -346,49 +361,65 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else {
-        // thread = key row; fixed accumulation order (items in order, columns in order)
-        const int kr = tid;
+        // warpgroup wg handles items it = wg, wg + 2, ...; thread = key row; each warpgroup
+        // accumulates in a fixed order and the two partial sums are added in a fixed order.
+        const int wg = warp >> 2;
+        const int kr = tid & 127;
         const int kj = key0 + kr;
-        const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+        const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16) + 128 * wg;
         const float sl2 = P.scale * kLog2e;
         float acc = 0.0f;
-        for (int it = 0; it < n_items; ++it) {
+        for (int it = wg; it < n_items; it += 2) {
             const int g = it / per_head, t = t_first + it % per_head;
             const int hq = hk * G + g;
-            const int bb = it & 1;
+            const int k = it >> 1;  // use count of this TMEM buffer
+            float* l2 = B.lse2[wg][k & 1];
             {
-                const int i = t * kTile + tid;
-                B.lse2[bb][tid] = (i < P.lq) ? P.lse[((size_t)b * P.hq + hq) * P.lq + i] * kLog2e : INFINITY;
+                const int i = t * kTile + kr;
+                l2[kr] = (i < P.lq) ? P.lse[((size_t)b * P.hq + hq) * P.lq + i] * kLog2e : INFINITY;
             }
-            named_bar_sync(1, 128);
-            mbar_wait(&B.s_full[bb], (it >> 1) & 1);
+            named_bar_sync(1 + wg, 128);
+            mbar_wait(&B.s_full[wg], k & 1);
             tc_fence_after();
             // query i = t*128 + c visible iff kj <= offset + i  <=>  c >= kj - offset - t*128
             const int c_min = P.causal ? (kj - offset - t * kTile) : -1;
+            const bool full = __all_sync(0xffffffffu, c_min <= 0);
             float part = 0.0f;
 #pragma unroll
             for (int half = 0; half < 2; ++half) {
                 uint32_t x[64];
-                tmem_ld32(trow + 128 * bb + 64 * half, *reinterpret_cast<uint32_t(*)[32]>(x));
-                tmem_ld32(trow + 128 * bb + 64 * half + 32, *reinterpret_cast<uint32_t(*)[32]>(x + 32));
+                tmem_ld32(trow + 64 * half, *reinterpret_cast<uint32_t(*)[32]>(x));
+                tmem_ld32(trow + 64 * half + 32, *reinterpret_cast<uint32_t(*)[32]>(x + 32));
                 tmem_wait_ld();
+                if (half == 1) {
+                    tc_fence_before();
+                    mbar_arrive(&B.s_free[wg]);  // TMEM buffer free for the next MMA
+                }
+                if (full) {
 #pragma unroll
-                for (int c = 0; c < 64; ++c) {
-                    const int col = 64 * half + c;
-                    const float v = fmaf(__uint_as_float(x[c]), sl2, -B.lse2[bb][col]);
-                    const float e = fast_exp2(v);
-                    part += (col >= c_min) ? e : 0.0f;
+                    for (int c = 0; c < 64; ++c) {
+                        const float v = fmaf(__uint_as_float(x[c]), sl2, -l2[64 * half + c]);
+                        part += (c & 3) == 3 ? exp2_fma(v) : fast_exp2(v);
+                    }
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 64; ++c) {
+                        const int col = 64 * half + c;
+                        const float v = fmaf(__uint_as_float(x[c]), sl2, -l2[col]);
+                        const float e = (c & 3) == 3 ? exp2_fma(v) : fast_exp2(v);
+                        part += (col >= c_min) ? e : 0.0f;
+                    }
                 }
             }
             acc += part;
-            tc_fence_before();
-            mbar_arrive(&B.s_free[bb]);
         }
-        if (kj < P.lk) P.a_cumul[((size_t)b * P.hkv + hk) * P.lk + kj] = acc;
+        if (wg == 1) B.acc1[kr] = acc;
+        named_bar_sync(3, 256);
+        if (wg == 0 && kj < P.lk) P.a_cumul[((size_t)b * P.hkv + hk) * P.lk + kj] = acc + B.acc1[kr];
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 5) {
+    if (warp == 9) {
         tc_fence_after();
         tmem_dealloc(tmem, 256);
     }
@@ -442,7 +473,7 @@ cudaError_t launch_prefill_attn(const PrefillAttnParams& p, cudaStream_t s) {
     attn_fwd_kernel<<<dim3(n_qt, p.hq, p.batch), kThreads, kFwdSmem, s>>>(tq, tk, tv, p);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    acumul_kernel<<<dim3(n_kt, p.hkv, p.batch), kThreads, kAcSmem, s>>>(tq, tk, p);
+    acumul_kernel<<<dim3(n_kt, p.hkv, p.batch), kAcThreads, kAcSmem, s>>>(tq, tk, p);
     return cudaGetLastError();
 }
 
