@@ -48,52 +48,82 @@ __device__ __forceinline__ uint64_t kslice(const uint8_t* tile, int k) {
     return desc_kmajor_sw128(smem_u32(tile + (k >> 2) * kHalf + (k & 3) * 32));
 }
 
+// exp2 on the FMA pipe (offloads the MUFU unit): round-to-nearest split x = j + f,
+// f in [-0.5, 0.5], 2^f by a degree-4 polynomial (rel. err < 5e-5), 2^j into the exponent.
+__device__ __forceinline__ float exp2_fma(float x) {
+    x = fmaxf(x, -127.0f);
+    const float xr = x + 12582912.0f;  // 1.5 * 2^23: rounds x to an integer in the low mantissa bits
+    const float f = x - (xr - 12582912.0f);
+    float p = fmaf(0.0096181291f, f, 0.0555041087f);
+    p = fmaf(p, f, 0.2402265070f);
+    p = fmaf(p, f, 0.6931471806f);
+    p = fmaf(p, f, 1.0f);
+    return __int_as_float(__float_as_int(p) + ((__float_as_int(xr) - 0x4B400000) << 23));
+}
+
 // ---------------------------------------------------------------------------
 // pass 1
 // ---------------------------------------------------------------------------
+// Two query tiles (A, B) per CTA ping-pong on the tensor core (FA4-style): while
+// warpgroup A runs softmax on S_A(j), the MMA warp computes P_B(j-1)V / S_B(j)
+// and vice versa.  K/V tiles are loaded once for both query tiles.  P never
+// touches shared memory: softmax writes fp16 P over the first 64 TMEM columns
+// of its own S buffer and the PV product reads A from TMEM.
+// TMEM (512 cols): tile h: S_h / P_h at 256h, O_h at 256h + 128.
 struct FwdBars {
-    uint64_t q_full, kv_full[2], kv_empty[2], s_full[2], s_free[2], p_full, o_done;
+    uint64_t q_full, kv_full[2], kv_empty[2], s_full[2], p_full[2], o_full[2];
     uint32_t tmem;
 };
-constexpr int kFwdSmem = 6 * kTileB + 1024 + 256;  // Q, K[2], V[2], P + alignment slack + barriers
+constexpr int kFwdThreads = 320;  // warps 0-3 softmax A, 4-7 softmax B, 8 TMA, 9 MMA
+constexpr int kFwdSmem = 6 * kTileB + 1024 + 256;  // Q[2], K[2], V[2] + alignment slack + barriers
 
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kFwdThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                     const __grid_constant__ CUtensorMap tv, const PrefillAttnParams P) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* sm = align1024(smem_raw);
-    uint8_t* sQ = sm;
-    uint8_t* sK = sm + kTileB;       // 2 stages
-    uint8_t* sV = sm + 3 * kTileB;   // 2 stages
-    uint8_t* sP = sm + 5 * kTileB;
+    uint8_t* sQ = sm;                // 2 query tiles
+    uint8_t* sK = sm + 2 * kTileB;   // 2 stages
+    uint8_t* sV = sm + 4 * kTileB;   // 2 stages
     FwdBars& B = *reinterpret_cast<FwdBars*>(sm + 6 * kTileB);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int n_qt = (P.lq + kTile - 1) / kTile;
-    const int qt = n_qt - 1 - blockIdx.x;  // longest causal rows first
+    const int n_pairs = (n_qt + 1) / 2;
+    const int pair = n_pairs - 1 - blockIdx.x;  // longest causal rows first
     const int hq = blockIdx.y, b = blockIdx.z;
     const int G = P.hq / P.hkv;
     const int hk = hq / G;
-    const int q0 = qt * kTile;
     const int offset = P.causal ? P.lk - P.lq : 0;
-    const int last_row = min(q0 + kTile, P.lq) - 1;
-    const int kmax = P.causal ? min(P.lk - 1, offset + last_row) : P.lk - 1;
-    const int n_kv = kmax / kTile + 1;
+    // per query tile h: first row, number of KV tiles it needs
+    int q0[2], nkv[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int qt = 2 * pair + h;
+        q0[h] = qt * kTile;
+        if (qt < n_qt) {
+            const int last_row = min(q0[h] + kTile, P.lq) - 1;
+            const int kmax = P.causal ? min(P.lk - 1, offset + last_row) : P.lk - 1;
+            nkv[h] = kmax / kTile + 1;
+        } else {
+            nkv[h] = 0;
+        }
+    }
+    const int nmax = max(nkv[0], nkv[1]);
 
-    if (warp == 5) {
+    if (warp == 9) {
         tmem_alloc(&B.tmem, 512);
         tmem_relinquish();
     }
-    if (tid == 128) {
+    if (tid == 256) {
         mbar_init(&B.q_full, 1);
         for (int s = 0; s < 2; ++s) {
             mbar_init(&B.kv_full[s], 1);
             mbar_init(&B.kv_empty[s], 1);
             mbar_init(&B.s_full[s], 1);
-            mbar_init(&B.s_free[s], 128);
+            mbar_init(&B.p_full[s], 128);
+            mbar_init(&B.o_full[s], 1);
         }
-        mbar_init(&B.p_full, 128);
-        mbar_init(&B.o_done, 1);
         fence_mbar_init();
         tma_prefetch_desc(&tq);
         tma_prefetch_desc(&tk);
@@ -104,13 +134,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     const uint32_t tmem = B.tmem;
 
-    if (warp == 4) {
+    if (warp == 8) {
         // ---------------- TMA producer ----------------
         if (lane == 0) {
-            mbar_expect_tx(&B.q_full, kTileB);
-            tma_load_4d(sQ, &tq, 0, q0, hq, b, &B.q_full);
-            tma_load_4d(sQ + kHalf, &tq, 64, q0, hq, b, &B.q_full);
-            for (int j = 0; j < n_kv; ++j) {
+            const int ntiles = nkv[1] > 0 ? 2 : 1;
+            mbar_expect_tx(&B.q_full, ntiles * kTileB);
+            tma_load_4d(sQ, &tq, 0, q0[0], hq, b, &B.q_full);
+            tma_load_4d(sQ + kHalf, &tq, 64, q0[0], hq, b, &B.q_full);
+            if (ntiles == 2) {
+                tma_load_4d(sQ + kTileB, &tq, 0, q0[1], hq, b, &B.q_full);
+                tma_load_4d(sQ + kTileB + kHalf, &tq, 64, q0[1], hq, b, &B.q_full);
+            }
+            for (int j = 0; j < nmax; ++j) {
                 const int s = j & 1;
                 if (j >= 2) mbar_wait(&B.kv_empty[s], ((j >> 1) - 1) & 1);
                 mbar_expect_tx(&B.kv_full[s], 2 * kTileB);
@@ -122,64 +157,82 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tma_load_4d(v_dst + kHalf, &tv, 64, j * kTile, hk, b, &B.kv_full[s]);
             }
         }
-    } else if (warp == 5) {
-        // ---------------- MMA issuer ----------------
+    } else if (warp == 9) {
+        // ---------------- MMA issuer (one thread) ----------------
         if (lane == 0) {
-            auto pv = [&](int jj) {
-                mbar_wait(&B.p_full, jj & 1);
-                tc_fence_after();
-                const uint8_t* v = sV + (jj & 1) * kTileB;
-#pragma unroll
-                for (int k = 0; k < 8; ++k)
-                    umma_f16(tmem + 256, kslice(sP, k), desc_mnmajor_sw128(smem_u32(v + k * 2048), kHalf), kIdescPV,
-                             (jj > 0 || k > 0) ? 1u : 0u);
-                umma_commit(&B.o_done);
-                umma_commit(&B.kv_empty[jj & 1]);
-            };
-            mbar_wait(&B.q_full, 0);
-            for (int j = 0; j < n_kv; ++j) {
-                const int s = j & 1;
-                mbar_wait(&B.kv_full[s], (j >> 1) & 1);
-                if (j >= 2) mbar_wait(&B.s_free[s], ((j >> 1) - 1) & 1);
-                tc_fence_after();
-                const uint8_t* k = sK + s * kTileB;
+            auto issue_s = [&](int h, int j) {  // S_h = Q_h K_j^T  (M = N = 128, 8 K-steps)
+                const uint8_t* k = sK + (j & 1) * kTileB;
+                const uint8_t* q = sQ + h * kTileB;
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk)
-                    umma_f16(tmem + 128 * s, kslice(sQ, kk), kslice(k, kk), kIdescS, kk > 0 ? 1u : 0u);
-                umma_commit(&B.s_full[s]);
-                if (j >= 1) pv(j - 1);
+                    umma_f16(tmem + 256 * h, kslice(q, kk), kslice(k, kk), kIdescS, kk > 0 ? 1u : 0u);
+                umma_commit(&B.s_full[h]);
+            };
+            auto issue_pv = [&](int h, int j) {  // O_h += P_h V_j, P from TMEM (16 keys = 8 columns)
+                const uint8_t* v = sV + (j & 1) * kTileB;
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+                    umma_f16_ts(tmem + 256 * h + 128, tmem + 256 * h + 8 * kk,
+                                desc_mnmajor_sw128(smem_u32(v + kk * 2048), kHalf), kIdescPV,
+                                (j > 0 || kk > 0) ? 1u : 0u);
+            };
+            mbar_wait(&B.q_full, 0);
+            mbar_wait(&B.kv_full[0], 0);
+            tc_fence_after();
+            issue_s(0, 0);
+            if (nkv[1] > 0) issue_s(1, 0);
+            for (int j = 0; j < nmax; ++j) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    if (j >= nkv[h]) continue;
+                    mbar_wait(&B.p_full[h], j & 1);
+                    tc_fence_after();
+                    issue_pv(h, j);
+                    if (j + 1 < nkv[h]) {
+                        mbar_wait(&B.kv_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
+                        tc_fence_after();
+                        issue_s(h, j + 1);  // in-order tensor pipe: overwrites S_h/P_h after PV_h(j) read it
+                    } else {
+                        umma_commit(&B.o_full[h]);
+                    }
+                }
+                umma_commit(&B.kv_empty[j & 1]);
             }
-            pv(n_kv - 1);
         }
     } else {
-        // ---------------- softmax warps: thread = query row ----------------
-        const int r = tid;
-        const int row_g = q0 + r;
-        const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+        // ---------------- softmax warpgroups: thread = query row of tile h ----------------
+        const int h = warp >> 2;
+        const int r = tid & 127;
+        const int row_g = (h ? q0[1] : q0[0]) + r;
+        const int n = h ? nkv[1] : nkv[0];
+        const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16) + 256 * h;
         const float sl2 = P.scale * kLog2e;
         const int lim = P.causal ? min(P.lk - 1, offset + row_g) : P.lk - 1;
         float m = -INFINITY, l = 0.0f;
-        for (int j = 0; j < n_kv; ++j) {
-            const int s = j & 1;
-            mbar_wait(&B.s_full[s], (j >> 1) & 1);
+        for (int j = 0; j < n; ++j) {
+            mbar_wait(&B.s_full[h], j & 1);  // also implies PV_h(j-1) completed (commit order)
             tc_fence_after();
+            // one TMEM read of the 128 scores; P is packed in place over x (x[c/2] <- c, c+1)
             uint32_t x[128];
-            tmem_ld32(trow + 128 * s + 0, *reinterpret_cast<uint32_t(*)[32]>(x + 0));
-            tmem_ld32(trow + 128 * s + 32, *reinterpret_cast<uint32_t(*)[32]>(x + 32));
-            tmem_ld32(trow + 128 * s + 64, *reinterpret_cast<uint32_t(*)[32]>(x + 64));
-            tmem_ld32(trow + 128 * s + 96, *reinterpret_cast<uint32_t(*)[32]>(x + 96));
+            tmem_ld32(trow + 0, *reinterpret_cast<uint32_t(*)[32]>(x + 0));
+            tmem_ld32(trow + 32, *reinterpret_cast<uint32_t(*)[32]>(x + 32));
+            tmem_ld32(trow + 64, *reinterpret_cast<uint32_t(*)[32]>(x + 64));
+            tmem_ld32(trow + 96, *reinterpret_cast<uint32_t(*)[32]>(x + 96));
             tmem_wait_ld();
-            tc_fence_before();
-            mbar_arrive(&B.s_free[s]);
             const int cut = lim - j * kTile;  // columns c > cut are masked
+            const bool nomask = __all_sync(0xffffffffu, cut >= kTile - 1);
             float mt = -INFINITY;
+            if (nomask) {
 #pragma unroll
-            for (int c = 0; c < 128; ++c) {
-                float v = __uint_as_float(x[c]) * sl2;
-                if (c > cut) v = -INFINITY;
-                x[c] = __float_as_uint(v);
-                mt = fmaxf(mt, v);
+                for (int c = 0; c < 128; ++c) mt = fmaxf(mt, __uint_as_float(x[c]));
+            } else {
+#pragma unroll
+                for (int c = 0; c < 128; ++c) {
+                    if (c > cut) x[c] = __float_as_uint(-INFINITY);
+                    mt = fmaxf(mt, __uint_as_float(x[c]));
+                }
             }
+            mt *= sl2;
             const float m_new = fmaxf(m, mt);
             float alpha = 1.0f;
             bool rescale = false;
@@ -191,70 +244,65 @@ __global__ void __launch_bounds__(kThreads, 1)
                 l *= alpha;
                 rescale = true;
             }
-            uint32_t pk[64];
+            // P = 2^(s*scale*log2e - m) -> fp16 pairs packed in place, then written over S in TMEM
             float ls = 0.0f;
 #pragma unroll
-            for (int c = 0; c < 128; c += 2) {
-                const float p0 = fast_exp2(__uint_as_float(x[c]) - m);
-                const float p1 = fast_exp2(__uint_as_float(x[c + 1]) - m);
+            for (int cc = 0; cc < 128; cc += 2) {
+                const float a0 = fmaf(__uint_as_float(x[cc]), sl2, -m), a1 = fmaf(__uint_as_float(x[cc + 1]), sl2, -m);
+                const float p0 = ((cc & 7) == 6) ? exp2_fma(a0) : fast_exp2(a0);
+                const float p1 = fast_exp2(a1);
                 ls += p0 + p1;
-                pk[c >> 1] = pack_half2(p0, p1);
+                x[cc >> 1] = pack_half2(p0, p1);
             }
-            l += ls;
-            if (j >= 1) mbar_wait(&B.o_done, (j - 1) & 1);  // PV(j-1) done: P buffer free, O stable
-            // tcgen05.ld/st are warp-collective (.sync.aligned): rescale warp-uniformly, alpha = 1 elsewhere
+            tmem_st32(trow + 0, *reinterpret_cast<uint32_t(*)[32]>(x + 0));
+            tmem_st32(trow + 32, *reinterpret_cast<uint32_t(*)[32]>(x + 32));
+            // O_h is stable (PV_h(j-1) done, PV_h(j) not issued yet); rescale after P is out of registers; tcgen05.ld/st are warp-collective
             if (__any_sync(0xffffffffu, rescale)) {
-                tc_fence_after();
 #pragma unroll
                 for (int cc = 0; cc < 4; ++cc) {
                     uint32_t o[32];
-                    tmem_ld32(trow + 256 + 32 * cc, o);
+                    tmem_ld32(trow + 128 + 32 * cc, o);
                     tmem_wait_ld();
 #pragma unroll
                     for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-                    tmem_st32(trow + 256 + 32 * cc, o);
+                    tmem_st32(trow + 128 + 32 * cc, o);
                 }
-                tmem_wait_st();
             }
-            // P row -> smem, K-major SWIZZLE_128B: 16-byte chunk c of row r at chunk c ^ (r & 7)
-#pragma unroll
-            for (int cc = 0; cc < 16; ++cc) {
-                const int h = cc >> 3, c = cc & 7;
-                uint4 v = make_uint4(pk[4 * cc], pk[4 * cc + 1], pk[4 * cc + 2], pk[4 * cc + 3]);
-                *reinterpret_cast<uint4*>(sP + h * kHalf + r * 128 + ((c ^ (r & 7)) << 4)) = v;
-            }
-            fence_proxy_async_smem();
+            l += ls;
+            tmem_wait_st();
             tc_fence_before();
-            mbar_arrive(&B.p_full);
+            mbar_arrive(&B.p_full[h]);
         }
         // ---------------- epilogue ----------------
-        mbar_wait(&B.o_done, (n_kv - 1) & 1);
-        tc_fence_after();
-        const float inv = 1.0f / l;
-        const bool valid = row_g < P.lq;
-        __half* orow = P.out + (size_t)b * P.o_sb + (size_t)hq * P.o_sh + (size_t)row_g * P.o_st;
+        if (n > 0) {
+            mbar_wait(&B.o_full[h], 0);
+            tc_fence_after();
+            const float inv = 1.0f / l;
+            const bool valid = row_g < P.lq;
+            __half* orow = P.out + (size_t)b * P.o_sb + (size_t)hq * P.o_sh + (size_t)row_g * P.o_st;
 #pragma unroll
-        for (int cc = 0; cc < 4; ++cc) {
-            uint32_t o[32];
-            tmem_ld32(trow + 256 + 32 * cc, o);
-            tmem_wait_ld();
-            if (valid) {
+            for (int cc = 0; cc < 4; ++cc) {
+                uint32_t o[32];
+                tmem_ld32(trow + 128 + 32 * cc, o);
+                tmem_wait_ld();
+                if (valid) {
 #pragma unroll
-                for (int e = 0; e < 32; e += 8) {
-                    uint4 v;
-                    v.x = pack_half2(__uint_as_float(o[e]) * inv, __uint_as_float(o[e + 1]) * inv);
-                    v.y = pack_half2(__uint_as_float(o[e + 2]) * inv, __uint_as_float(o[e + 3]) * inv);
-                    v.z = pack_half2(__uint_as_float(o[e + 4]) * inv, __uint_as_float(o[e + 5]) * inv);
-                    v.w = pack_half2(__uint_as_float(o[e + 6]) * inv, __uint_as_float(o[e + 7]) * inv);
-                    *reinterpret_cast<uint4*>(orow + 32 * cc + e) = v;
+                    for (int e = 0; e < 32; e += 8) {
+                        uint4 v;
+                        v.x = pack_half2(__uint_as_float(o[e]) * inv, __uint_as_float(o[e + 1]) * inv);
+                        v.y = pack_half2(__uint_as_float(o[e + 2]) * inv, __uint_as_float(o[e + 3]) * inv);
+                        v.z = pack_half2(__uint_as_float(o[e + 4]) * inv, __uint_as_float(o[e + 5]) * inv);
+                        v.w = pack_half2(__uint_as_float(o[e + 6]) * inv, __uint_as_float(o[e + 7]) * inv);
+                        *reinterpret_cast<uint4*>(orow + 32 * cc + e) = v;
+                    }
                 }
             }
+            if (valid) P.lse[((size_t)b * P.hq + hq) * P.lq + row_g] = (m + __log2f(l)) * kLn2;
         }
-        if (valid) P.lse[((size_t)b * P.hq + hq) * P.lq + row_g] = (m + __log2f(l)) * kLn2;
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 5) {
+    if (warp == 9) {
         tc_fence_after();
         tmem_dealloc(tmem, 512);
     }
@@ -272,19 +320,6 @@ struct AcBars {
     float acc1[kTile];        // warpgroup 1 partial sums
 };
 constexpr int kAcSmem = (1 + kQStages) * kTileB + 1024 + (int)sizeof(AcBars) + 64;
-
-// exp2 on the FMA pipe (offloads the MUFU unit): round-to-nearest split x = j + f,
-// f in [-0.5, 0.5], 2^f by a degree-4 polynomial (rel. err < 5e-5), 2^j into the exponent.
-__device__ __forceinline__ float exp2_fma(float x) {
-    x = fmaxf(x, -127.0f);
-    const float xr = x + 12582912.0f;  // 1.5 * 2^23: rounds x to an integer in the low mantissa bits
-    const float f = x - (xr - 12582912.0f);
-    float p = fmaf(0.0096181291f, f, 0.0555041087f);
-    p = fmaf(p, f, 0.2402265070f);
-    p = fmaf(p, f, 0.6931471806f);
-    p = fmaf(p, f, 1.0f);
-    return __int_as_float(__float_as_int(p) + ((__float_as_int(xr) - 0x4B400000) << 23));
-}
 
 __global__ void __launch_bounds__(kAcThreads, 1)
     acumul_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
@@ -470,7 +505,7 @@ cudaError_t launch_prefill_attn(const PrefillAttnParams& p, cudaStream_t s) {
         configured = true;
     }
     const int n_qt = (p.lq + kTile - 1) / kTile, n_kt = (p.lk + kTile - 1) / kTile;
-    attn_fwd_kernel<<<dim3(n_qt, p.hq, p.batch), kThreads, kFwdSmem, s>>>(tq, tk, tv, p);
+    attn_fwd_kernel<<<dim3((n_qt + 1) / 2, p.hq, p.batch), kFwdThreads, kFwdSmem, s>>>(tq, tk, tv, p);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     acumul_kernel<<<dim3(n_kt, p.hkv, p.batch), kAcThreads, kAcSmem, s>>>(tq, tk, p);
