@@ -268,7 +268,7 @@ int mkv_cache_create(const mkv_cache_config* cfg, mkv_cache** out) {
         acc += c->cap_pages[u];
     }
     c->total_pages = acc;
-    c->part_slots = num_sms() * kPagesWarps + n;
+    c->part_slots = num_sms() * kMaxPagesWarps + n;
     auto al = [&](void** p, size_t bytes) -> cudaError_t { return cudaMalloc(p, std::max<size_t>(bytes, 16)); };
     cudaError_t e = cudaSuccess;
     if (e == cudaSuccess) e = al((void**)&c->d_meta, sizeof(UnitMeta) * n);
@@ -420,7 +420,8 @@ static int get_plan(mkv_cache* c, int ub, int n, cudaStream_t s, Plan** out) {
         *out = &pl;
         return MKV_OK;
     }
-    const int max_warps = num_sms() * kPagesWarps;
+    const int wpc = pages_config().warps;
+    const int max_warps = num_sms() * wpc;
     std::vector<int32_t> buf(n + 1 + max_warps, 0);
     int32_t* pref = buf.data();
     for (int i = 0; i < n; ++i) pref[i + 1] = pref[i] + c->n_pages[ub + i];
@@ -434,13 +435,13 @@ static int get_plan(mkv_cache* c, int ub, int n, cudaStream_t s, Plan** out) {
         while (i < n - 1 && pref[i + 1] <= p) ++i;
         wstart[w] = i;
     }
-    if (!pl.d_pref) CK(cudaMalloc(&pl.d_pref, sizeof(int32_t) * (c->n_units + 1 + max_warps)));
+    if (!pl.d_pref) CK(cudaMalloc(&pl.d_pref, sizeof(int32_t) * (c->n_units + 1 + num_sms() * kMaxPagesWarps)));
     CK(cudaMemcpyAsync(pl.d_pref, buf.data(), sizeof(int32_t) * buf.size(), cudaMemcpyHostToDevice, s));
     pl.d_wstart = pl.d_pref + n + 1;
     pl.hash = h;
     pl.total = total;
     pl.chunk = chunk;
-    pl.grid = (warps + kPagesWarps - 1) / kPagesWarps;
+    pl.grid = (warps + wpc - 1) / wpc;
     *out = &pl;
     return MKV_OK;
 }
@@ -449,7 +450,7 @@ static void fill_pages_params(mkv_cache* c, const Plan* pl, const mkv_decode_arg
     pp.pool = c->d_pool; pp.meta = c->d_meta; pp.unit_begin = a->unit_begin; pp.n_units = a->n_units;
     pp.group = a->group; pp.q = static_cast<const __half*>(a->q);
     pp.pref = pl->d_pref; pp.wstart = pl->d_wstart; pp.chunk = pl->chunk; pp.total_pages = pl->total;
-    pp.n_warps = pl->grid * kPagesWarps;
+    pp.n_warps = pl->grid * pages_config().warps;
     pp.part_ml = c->d_part_ml; pp.part_o = c->d_part_o;
     pp.scale_log2 = a->scale * 1.4426950408889634f;
 }

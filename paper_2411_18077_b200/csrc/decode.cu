@@ -27,6 +27,8 @@
 // zero points enter through one extra mma per page (keys: sum_c q_c z_c over a
 // 4-page batch; values: sum_t p_t z_t).  See DESIGN.md.
 #include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
 
 #include "mkv_kernels.h"
 #include "mkv_page.cuh"
@@ -35,11 +37,12 @@ namespace mkv {
 
 namespace {
 
-constexpr int kStages = 2;
 constexpr int kBatch = 4;  // pages per bulk copy / per K-bias mma / per softmax update
 constexpr float kTwo24 = 16777216.0f;
+constexpr float kLazy = 3.0f;  // log2 units: P <= 8 keeps fp16 P and P*s far from overflow
 constexpr int kQBytes = kMaxG * kHeadDim * 2;  // per-warp q staging
-constexpr int kWarpSmem = kStages * kBatch * kPageBytes + kQBytes;
+template <int kStages>
+__host__ __device__ constexpr int warp_smem() { return kStages * kBatch * kPageBytes + kQBytes; }
 
 __device__ __forceinline__ uint4 lds128(const uint8_t* p) { return *reinterpret_cast<const uint4*>(p); }
 __device__ __forceinline__ uint2 lds64(const uint8_t* p) { return *reinterpret_cast<const uint2*>(p); }
@@ -93,16 +96,18 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
 // ---------------------------------------------------------------------------
 // pages kernel
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kPagesWarps * 32, 1) pages_kernel(const PagesParams P) {
+template <int kWarps, int kStages>
+__global__ void __launch_bounds__(kWarps * 32, 1) pages_kernel(const PagesParams P) {
+    constexpr int kWarpSmem = warp_smem<kStages>();
     extern __shared__ __align__(128) uint8_t smem[];
     const int warp = threadIdx.x >> 5, lane = lane_id();
     const int gid = lane >> 2, tig = lane & 3;
     uint8_t* wsm = smem + (size_t)warp * kWarpSmem;
     uint8_t* ring = wsm;
     __half* qsm = reinterpret_cast<__half*>(wsm + kStages * kBatch * kPageBytes);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)kPagesWarps * kWarpSmem) + warp * kStages;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)kWarps * kWarpSmem) + warp * kStages;
 
-    const int wg = blockIdx.x * kPagesWarps + warp;
+    const int wg = blockIdx.x * kWarps + warp;
     const int start = wg * P.chunk;
     const int end = min(start + P.chunk, P.total_pages);
     if (start >= end) return;
@@ -136,19 +141,23 @@ __global__ void __launch_bounds__(kPagesWarps * 32, 1) pages_kernel(const PagesP
     int pi = ci;
     int pg = start;
     int p_uend = __ldg(P.pref + pi + 1);
+    // pool address of "global page 0" of unit pi (its first page minus its prefix)
+    const uint8_t* p_base = P.pool + (P.meta[P.unit_begin + pi].page_base - __ldg(P.pref + pi)) * kPageBytes;
     auto issue = [&](int stage) {
         if (pg >= end) return;
         const int n = min(min(kBatch, p_uend - pg), end - pg);
         if (lane == 0) {
-            const int64_t base = P.meta[P.unit_begin + pi].page_base;
-            const uint8_t* src = P.pool + (size_t)(base + (pg - __ldg(P.pref + pi))) * kPageBytes;
             mbar_expect_tx(&bars[stage], n * kPageBytes);
-            bulk_g2s(ring + (size_t)stage * kBatch * kPageBytes, src, n * kPageBytes, &bars[stage]);
+            bulk_g2s(ring + (size_t)stage * kBatch * kPageBytes, p_base + (size_t)pg * kPageBytes, n * kPageBytes,
+                     &bars[stage]);
         }
         pg += n;
-        while (pg == p_uend && pg < end) {  // next unit that has pages
-            ++pi;
-            p_uend = __ldg(P.pref + pi + 1);
+        if (pg == p_uend && pg < end) {
+            while (pg == p_uend) {  // next unit that has pages
+                ++pi;
+                p_uend = __ldg(P.pref + pi + 1);
+            }
+            p_base = P.pool + (P.meta[P.unit_begin + pi].page_base - __ldg(P.pref + pi)) * kPageBytes;
         }
     };
     for (int s = 0; s < kStages; ++s) issue(s);
@@ -173,6 +182,14 @@ __global__ void __launch_bounds__(kPagesWarps * 32, 1) pages_kernel(const PagesP
         __syncwarp();
         load_q_frags(qsm, G, gid, tig, qb, qsc);
         __syncwarp();
+        {  // K-bias query copy carries the softmax scale: Kb comes out in log2 units
+            const uint32_t s2 = pack_half2(P.scale_log2, P.scale_log2);
+#pragma unroll
+            for (int kc = 0; kc < 8; ++kc) {
+                qb[kc][0] = hmul2_u32(qb[kc][0], s2);
+                qb[kc][1] = hmul2_u32(qb[kc][1], s2);
+            }
+        }
         if (seg_end < end) {
             int nu = unit + 1;
             while (__ldg(P.pref + nu + 1) == seg_end) ++nu;
@@ -195,9 +212,9 @@ __global__ void __launch_bounds__(kPagesWarps * 32, 1) pages_kernel(const PagesP
             float Kb[4] = {0.0f, 0.0f, 0.0f, 0.0f}, Kb2[4] = {0.0f, 0.0f, 0.0f, 0.0f};
             {
                 uint4 z[4];
-                const uint8_t* zp = buf + (gid & (kBatch - 1)) * kPageBytes + kKZ + tig * 64;
+                const uint8_t* zp = buf + (gid & (kBatch - 1)) * kPageBytes + kKZ + tig * 16;
 #pragma unroll
-                for (int j = 0; j < 4; ++j) z[j] = lds128(zp + 16 * j);  // rows >= kBatch: unused
+                for (int j = 0; j < 4; ++j) z[j] = lds128(zp + 64 * j);  // rows >= kBatch: unused
                 const uint32_t* zz = reinterpret_cast<const uint32_t*>(z);
 #pragma unroll
                 for (int kc = 0; kc < 8; kc += 2) {
@@ -224,7 +241,7 @@ __global__ void __launch_bounds__(kPagesWarps * 32, 1) pages_kernel(const PagesP
                 const uint32_t mask = 0x00030003u << (2 * (kc % 3));
 #pragma unroll
                 for (int j = 0; j < kBatch; ++j) {
-                    const uint2 ks = lds64(buf + j * kPageBytes + kKS + tig * 64 + kc * 8);
+                    const uint2 ks = lds64(buf + j * kPageBytes + kKS + ((kc >> 1) * 4 + tig) * 16 + (kc & 1) * 8);
                     const uint32_t a[4] = {(kw[j].x >> sh) & mask, (kw[j].y >> sh) & mask,
                                            (kw[j].z >> sh) & mask, (kw[j].w >> sh) & mask};
                     mma_16816(S[j], a, hmul2_u32(qsc[kc][0], ks.x), hmul2_u32(qsc[kc][1], ks.y));
@@ -236,8 +253,8 @@ __global__ void __launch_bounds__(kPagesWarps * 32, 1) pages_kernel(const PagesP
             float mx0 = -INFINITY, mx1 = -INFINITY;
 #pragma unroll
             for (int j = 0; j < kBatch; ++j) {
-                const float kb0 = __shfl_sync(0xffffffffu, Kb[0], 4 * j + tig) * sl2;
-                const float kb1 = __shfl_sync(0xffffffffu, Kb[1], 4 * j + tig) * sl2;
+                const float kb0 = __shfl_sync(0xffffffffu, Kb[0], 4 * j + tig);
+                const float kb1 = __shfl_sync(0xffffffffu, Kb[1], 4 * j + tig);
                 x[j][0] = fmaf(S[j][0], sk, kb0);
                 x[j][1] = fmaf(S[j][1], sk, kb1);
                 x[j][2] = fmaf(S[j][2], sk, kb0);
@@ -256,8 +273,9 @@ __global__ void __launch_bounds__(kPagesWarps * 32, 1) pages_kernel(const PagesP
                 mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
                 mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
             }
+            // lazy rescale: keep the running max unless it grows by > kLazy (then P <= 2^kLazy)
             const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
-            if (__any_sync(0xffffffffu, (mn0 != m0) | (mn1 != m1))) {
+            if (__any_sync(0xffffffffu, (mn0 > m0 + kLazy) | (mn1 > m1 + kLazy))) {
                 const float a0 = fast_exp2(m0 - mn0), a1 = fast_exp2(m1 - mn1);
                 l0 *= a0; l1 *= a1;
 #pragma unroll
@@ -289,7 +307,7 @@ __global__ void __launch_bounds__(kPagesWarps * 32, 1) pages_kernel(const PagesP
                 for (int g = 0; g < 8; ++g) {
                     const int sh = (g < 3) ? 0 : ((g < 6) ? 6 : 12);
                     const uint32_t mask = 0x00030003u << (2 * (g % 3));
-                    const uint2 vs = lds64(page + kVS + tig * 64 + g * 8);
+                    const uint2 vs = lds64(page + kVS + ((g >> 1) * 4 + tig) * 16 + (g & 1) * 8);
                     const uint32_t a[4] = {(vw.x >> sh) & mask, (vw.y >> sh) & mask, (vw.z >> sh) & mask,
                                            (vw.w >> sh) & mask};
                     mma_16816(O[g], a, hmul2_u32(pb0[j], vs.x), hmul2_u32(pb1[j], vs.y));
@@ -337,15 +355,41 @@ __global__ void __launch_bounds__(kPagesWarps * 32, 1) pages_kernel(const PagesP
     }
 }
 
-cudaError_t launch_pages(const PagesParams& p, int grid, cudaStream_t s) {
-    const size_t smem = (size_t)kPagesWarps * kWarpSmem + (size_t)kPagesWarps * kStages * sizeof(uint64_t);
+template <int W, int S>
+static cudaError_t launch_pages_t(const PagesParams& p, int grid, cudaStream_t s) {
+    const size_t smem = (size_t)W * warp_smem<S>() + (size_t)W * S * sizeof(uint64_t);
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(pages_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e = cudaFuncSetAttribute(pages_kernel<W, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    return launch_pdl(pages_kernel, dim3(grid), dim3(kPagesWarps * 32), smem, s, p);
+    return launch_pdl(pages_kernel<W, S>, dim3(grid), dim3(W * 32), smem, s, p);
+}
+
+// (warps per CTA, ring stages) of the page kernel; MKV_PAGES_CFG=WxS selects a variant
+PagesConfig pages_config() {
+    static PagesConfig cfg = [] {
+        PagesConfig c{12, 2};
+        if (const char* e = getenv("MKV_PAGES_CFG")) {
+            int w = 0, s = 0;
+            if (sscanf(e, "%dx%d", &w, &s) == 2 &&
+                ((w == 12 && s == 2) || (w == 8 && s == 3) || (w == 10 && s == 2) || (w == 6 && s == 4) ||
+                 (w == 8 && s == 2)))
+                c = PagesConfig{w, s};
+        }
+        return c;
+    }();
+    return cfg;
+}
+
+cudaError_t launch_pages(const PagesParams& p, int grid, cudaStream_t s) {
+    const PagesConfig c = pages_config();
+    if (c.warps == 8 && c.stages == 3) return launch_pages_t<8, 3>(p, grid, s);
+    if (c.warps == 10 && c.stages == 2) return launch_pages_t<10, 2>(p, grid, s);
+    if (c.warps == 6 && c.stages == 4) return launch_pages_t<6, 4>(p, grid, s);
+    if (c.warps == 8 && c.stages == 2) return launch_pages_t<8, 2>(p, grid, s);
+    return launch_pages_t<12, 2>(p, grid, s);
 }
 
 // ---------------------------------------------------------------------------

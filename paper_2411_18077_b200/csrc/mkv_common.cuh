@@ -18,11 +18,11 @@ constexpr int kGroup = 16;  // quantization group = tokens per page (quantizer.h
 //
 //  KC  u32[32][4]    lane L word r = tt + 2p: token t = gid + 8tt; bits 2kc (lo)
 //                    = code(t, 16kc + 2tig + 8p), bits 16 + 2kc (hi) = code(t, ch + 1)
-//  KS  half2[4][8][2] (tig, kc, p) = (scale[16kc+2tig+8p], scale[..+1])   K per-channel
-//  KZ  half2[4][8][2] same order, zero points
+//  KS  half2[4][4][2][2] (kc/2, tig, kc%2, p) = (scale[16kc+2tig+8p], scale[..+1])   K per-channel
+//  KZ  same order, zero points      (a lane's (kc, kc+1) pair is one conflict-free 16-byte load)
 //  VC  u32[32][4]    lane L word r = cc + 2pt: channel c = 16g + gid + 8cc, token
 //                    t = 2tig + 8pt; bits 2g (lo) = code(t, c), bits 16 + 2g (hi) = code(t + 1, c)
-//  VS  half2[4][8][2] (tig, g, pt) = (scale[t=2tig+8pt][g], scale[t+1][g])  V per-token
+//  VS  half2[4][4][2][2] (g/2, tig, g%2, pt) = (scale[t=2tig+8pt][g], scale[t+1][g])  V per-token
 //  VZ  half2[8][4][2] (g, tig, pt) = (zero[2tig+8pt][g], zero[2tig+8pt+1][g])
 //
 // The reference stream (quantizer.cpp:102-136) is recovered by
@@ -53,12 +53,12 @@ __host__ __device__ inline CodePos v_code_pos(int t, int c) {
 // half index (not byte) inside KS / KZ for channel c
 __host__ __device__ inline int k_param_idx(int c) {
     const int kc = c >> 4, w = c & 15, p = w >> 3, tig = (w & 7) >> 1, e = w & 1;
-    return ((tig * 8 + kc) * 2 + p) * 2 + e;
+    return (((((kc >> 1) * 4 + tig) * 2 + (kc & 1)) * 2 + p) * 2) + e;
 }
 // half index inside VS for (token t, group g)
 __host__ __device__ inline int vs_param_idx(int t, int g) {
     const int pt = t >> 3, w = t & 7, tig = w >> 1, e = w & 1;
-    return ((tig * 8 + g) * 2 + pt) * 2 + e;
+    return (((((g >> 1) * 4 + tig) * 2 + (g & 1)) * 2 + pt) * 2) + e;
 }
 // half index inside VZ for (token t, group g)
 __host__ __device__ inline int vz_param_idx(int t, int g) {

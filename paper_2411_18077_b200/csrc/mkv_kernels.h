@@ -72,7 +72,11 @@ struct PagesParams {
     float* part_o;          // [slots][kMaxG][d]
     float scale_log2;
 };
-constexpr int kPagesWarps = 12;
+constexpr int kMaxPagesWarps = 12;  // partial-slot sizing
+struct PagesConfig {
+    int warps, stages;
+};
+PagesConfig pages_config();
 cudaError_t launch_pages(const PagesParams& p, int grid, cudaStream_t s);
 
 // ---- utilities (synth.cu) ----
