@@ -521,6 +521,9 @@ __global__ void __launch_bounds__(kFinishWarps * 32) finish_kernel(const Residua
     }
     for (int e = tid; e < G * d / 8; e += blockDim.x)
         cp_async16(reinterpret_cast<uint4*>(S.q) + e, reinterpret_cast<const uint4*>(P.q + (size_t)i * G * d) + e);
+    // PDL: the page kernel's partials are complete past this point; fetch them in the same burst
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    stage_partials(S, P, i, w_first, min(n_part, kMaxPart), G, tid);
     cp_async_commit();
     // decode_append (cache_engine.cpp:79-90) -- the flush case was handled by append_kernel
     int n = n_old;
@@ -600,18 +603,15 @@ __global__ void __launch_bounds__(kFinishWarps * 32) finish_kernel(const Residua
             if (h1 < G) { S.wml[warp][0][h1] = mx1; S.wml[warp][1][h1] = l1; }
         }
     }
-    // PDL: the residual part above overlapped the page kernel; its partials are read below
-    asm volatile("griddepcontrol.wait;\n" ::: "memory");
-    stage_partials(S, P, i, w_first, min(n_part, kMaxPart), G, tid);
-    cp_async_commit();
-    cp_async_wait_all();
     __syncthreads();
 
     // ---- split-K merge over residual tiles and page partials (staged in passes of kMaxPart) ----
     if (tid < G) {
         float M = -INFINITY;
         for (int w = 0; w < ntiles; ++w) M = fmaxf(M, S.wml[w][0][tid]);
-        for (int w = w_first; w <= w_last; ++w) M = fmaxf(M, __ldcg(P.part_ml + (size_t)(w + i) * 2 * kMaxG + tid));
+        const int np0 = min(n_part, kMaxPart);
+        for (int w = 0; w < np0; ++w) M = fmaxf(M, S.pml[w][0][tid]);  // staged copy
+        for (int w = w_first + np0; w <= w_last; ++w) M = fmaxf(M, __ldcg(P.part_ml + (size_t)(w + i) * 2 * kMaxG + tid));
         S.M[tid] = M;
     }
     __syncthreads();
