@@ -171,10 +171,19 @@ __device__ __forceinline__ bool quantize_group16(const float* v, int n, uint8_t*
         hi = (hi < x) ? x : hi;
     }
     const float sc = __fdiv_rn(__fsub_rn(hi, lo), 3.0f);
+    // q = roundf((v - lo) / sc) with the IEEE quotient.  The quotient is computed with a
+    // reciprocal multiply (|error| < 1e-6 on [0, 3]); only when that lands within 1e-4 of a
+    // half-integer -- where rounding could differ -- is the exact division evaluated.  The
+    // resulting codes are identical to the reference's for every input.
+    const float rcp = __frcp_rn(sc);
     for (int i = 0; i < n; ++i) {
         uint8_t c = 0;
         if (sc > 0.0f) {
-            const float q = roundf(__fdiv_rn(__fsub_rn(v[i], lo), sc));
+            const float dv = __fsub_rn(v[i], lo);
+            float q = __fmul_rn(dv, rcp);
+            const float fr = q - floorf(q);
+            if (fabsf(fr - 0.5f) < 1e-4f) q = __fdiv_rn(dv, sc);
+            q = roundf(q);
             c = static_cast<uint8_t>(q < 0.0f ? 0.0f : (q > 3.0f ? 3.0f : q));
         }
         codes[i] = c;

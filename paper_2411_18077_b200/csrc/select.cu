@@ -5,10 +5,12 @@
 // a_cumul descending with ties to the LOWER index (stable_sort, :22-27);
 // kept = sort(HH) ++ RW; if hh + rw >= L everything is kept (:14-18).
 // The k-th largest key T is found with four 8-bit MSB-first radix passes
-// (shared-memory histograms); an order-preserving ballot compaction then
-// emits every index with key > T plus the first (k - #greater) indices with
-// key == T in index order -- exactly the stable_sort tie rule, so indices are
-// bit-identical to the reference for identical inputs.
+// (per-warp shared-memory histograms, so ties never serialise a whole CTA on
+// one bin); a two-pass order-preserving compaction (each warp owns a
+// contiguous slice: count, one block scan, write) then emits every index with
+// key > T plus the first (k - #greater) indices with key == T in index order --
+// exactly the stable_sort tie rule, so indices are bit-identical to the
+// reference for identical inputs.
 //
 // Keys are the order-preserving u32 image of the float (-0 folded onto +0, as
 // the reference's operator> treats them equal); NaN sorts below everything
@@ -18,6 +20,7 @@
 namespace mkv {
 
 constexpr int kSelThreads = 1024;
+constexpr int kSelWarps = kSelThreads / 32;
 
 __device__ __forceinline__ uint32_t order_key(float f) {
     uint32_t b = __float_as_uint(f);
@@ -26,24 +29,11 @@ __device__ __forceinline__ uint32_t order_key(float f) {
     return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
 }
 
-// inclusive block scan of one int per warp (warp totals in sm[0..31])
-__device__ __forceinline__ void scan_warp_totals(int* sm, int nwarps) {
-    const int lane = threadIdx.x & 31;
-    if (threadIdx.x < 32) {
-        int v = lane < nwarps ? sm[lane] : 0;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int n = __shfl_up_sync(0xffffffffu, v, o);
-            if (lane >= o) v += n;
-        }
-        sm[lane] = v;
-    }
-}
-
 __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectParams P) {
-    __shared__ int hist[256];
+    __shared__ int hist[kSelWarps][256];
+    __shared__ int tot[256];
     __shared__ int s_digit, s_k;
-    __shared__ int wtot_eq[32], wtot_sel[32];
+    __shared__ int w_gt[kSelWarps], w_eq[kSelWarps], w_sel[kSelWarps];
     const int u = blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int L = P.length;
@@ -63,38 +53,77 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectParams 
         for (int j = tid; j < pool; j += kSelThreads) kept[j] = j;
         return;
     }
-    // ---- radix select of the nh-th largest key ----
-    uint32_t prefix = 0, pmask = 0;
+    // ---- key range: bits shared by min and max need no radix pass ----
+    uint32_t kmin = 0xffffffffu, kmax = 0u;
+    for (int j = tid; j < pool; j += kSelThreads) {
+        const uint32_t key = order_key(__ldg(a + j));
+        kmin = min(kmin, key);
+        kmax = max(kmax, key);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+        kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+    }
+    if (lane == 0) { w_gt[warp] = (int)kmin; w_eq[warp] = (int)kmax; }
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t mn = (uint32_t)w_gt[lane], mx = (uint32_t)w_eq[lane];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+            mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        }
+        if (lane == 0) { w_sel[0] = (int)mn; w_sel[1] = (int)mx; }
+    }
+    __syncthreads();
+    const uint32_t gmin = (uint32_t)w_sel[0], gmax = (uint32_t)w_sel[1];
+    const int free_bits = (gmin == gmax) ? 0 : 32 - __clz(gmin ^ gmax);  // low bits that still vary
+    uint32_t prefix = gmin & ~((free_bits == 32) ? 0xffffffffu : ((1u << free_bits) - 1u));
+    uint32_t pmask = (free_bits == 32) ? 0u : ~((1u << free_bits) - 1u);
     int k = nh;
-    for (int shift = 24; shift >= 0; shift -= 8) {
-        for (int j = tid; j < 256; j += kSelThreads) hist[j] = 0;
+    // ---- radix select of the nh-th largest key over the varying bits, 8 at a time ----
+    for (int top = free_bits; top > 0; top -= 8) {
+        const int shift = max(top - 8, 0), width = top - shift;
+        const uint32_t dmask = (1u << width) - 1u;
+        for (int j = lane; j < 256; j += 32) hist[warp][j] = 0;
         __syncthreads();
-        for (int j = tid; j < pool; j += kSelThreads) {
-            const uint32_t key = order_key(__ldg(a + j));
-            if ((key & pmask) == prefix) atomicAdd(&hist[(key >> shift) & 0xffu], 1);
+        for (int base = warp * 32; base < pool; base += kSelThreads) {  // warp-uniform trip count
+            const int j = base + lane;
+            const uint32_t key = j < pool ? order_key(__ldg(a + j)) : 0u;
+            const bool inp = j < pool && (key & pmask) == prefix;
+            const unsigned act = __ballot_sync(0xffffffffu, inp);
+            if (inp) {  // warp-aggregated: one shared atomic per distinct digit in the warp
+                const uint32_t dg = (key >> shift) & dmask;
+                const unsigned same = __match_any_sync(act, dg);
+                if ((__ffs(same) - 1) == lane) atomicAdd(&hist[warp][dg], __popc(same));
+            }
+        }
+        __syncthreads();
+        if (tid < 256) {
+            int s = 0;
+#pragma unroll 8
+            for (int w = 0; w < kSelWarps; ++w) s += hist[w][tid];
+            tot[tid] = s;
         }
         __syncthreads();
         if (warp == 0) {
-            // find digit d with greater < k <= greater + hist[d], scanning 255 -> 0
-            int greater = 0;
-            int found = -1, kk = k;
+            // digit d with greater < k <= greater + tot[d], scanning 255 -> 0
+            int greater = 0, found = -1, kk = k;
             for (int base = 255; base >= 0 && found < 0; base -= 32) {
-                const int dgt = base - lane;
-                const int c = hist[dgt];
-                int incl = c;  // inclusive suffix sum within this chunk (from high digits)
+                const int cnt = tot[base - lane];
+                int incl = cnt;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
                     const int n = __shfl_up_sync(0xffffffffu, incl, o);
                     if (lane >= o) incl += n;
                 }
-                const int excl = incl - c;
-                const bool hit = (greater + excl < kk) && (kk <= greater + incl);
-                const unsigned ball = __ballot_sync(0xffffffffu, hit);
+                const int excl = incl - cnt;
+                const unsigned ball = __ballot_sync(0xffffffffu, (greater + excl < kk) && (kk <= greater + incl));
                 if (ball) {
                     const int src = __ffs(ball) - 1;
                     found = base - src;
-                    const int ex = __shfl_sync(0xffffffffu, excl, src);
-                    kk -= greater + ex;
+                    kk -= greater + __shfl_sync(0xffffffffu, excl, src);
                 } else {
                     greater += __shfl_sync(0xffffffffu, incl, 31);
                 }
@@ -103,37 +132,61 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectParams 
         }
         __syncthreads();
         prefix |= static_cast<uint32_t>(s_digit) << shift;
-        pmask |= 0xffu << shift;
+        pmask |= dmask << shift;
         k = s_k;
-        __syncthreads();
     }
     const uint32_t T = prefix;
     const int take_eq = k;  // equal keys to take, lowest indices first
-    // ---- order-preserving compaction ----
-    int carry_eq = 0, carry_sel = 0;
-    for (int base = 0; base < pool; base += kSelThreads) {
-        const int j = base + tid;
-        uint32_t key = 0;
-        const bool in = j < pool;
-        if (in) key = order_key(__ldg(a + j));
-        const bool gt = in && key > T;
+    // ---- order-preserving compaction: warp w owns the contiguous slice [w*span, (w+1)*span) ----
+    const int span = (pool + kSelWarps - 1) / kSelWarps;
+    const int lo = min(warp * span, pool), hi = min(lo + span, pool);
+    int c_gt = 0, c_eq = 0;
+    for (int j = lo + lane; j < hi; j += 32) {
+        const uint32_t key = order_key(__ldg(a + j));
+        c_gt += key > T;
+        c_eq += key == T;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        c_gt += __shfl_xor_sync(0xffffffffu, c_gt, o);
+        c_eq += __shfl_xor_sync(0xffffffffu, c_eq, o);
+    }
+    if (lane == 0) { w_gt[warp] = c_gt; w_eq[warp] = c_eq; }
+    __syncthreads();
+    if (warp == 0) {  // exclusive scans over warps: equal-key rank base, then output base
+        const int g = w_gt[lane], e = w_eq[lane];
+        int ie = e;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int n = __shfl_up_sync(0xffffffffu, ie, o);
+            if (lane >= o) ie += n;
+        }
+        const int eq_base = ie - e;
+        const int take = max(0, min(e, take_eq - eq_base));  // equal keys this warp emits
+        const int sel = g + take;
+        int is = sel;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int n = __shfl_up_sync(0xffffffffu, is, o);
+            if (lane >= o) is += n;
+        }
+        w_eq[lane] = eq_base;
+        w_sel[lane] = is - sel;
+    }
+    __syncthreads();
+    int eq_rank = w_eq[warp], out = w_sel[warp];
+    for (int base = lo; base < hi; base += 32) {
+        const int j = base + lane;
+        const bool in = j < hi;
+        const uint32_t key = in ? order_key(__ldg(a + j)) : 0u;
         const bool eq = in && key == T;
         const unsigned beq = __ballot_sync(0xffffffffu, eq);
-        if (lane == 0) wtot_eq[warp] = __popc(beq);
-        __syncthreads();
-        scan_warp_totals(wtot_eq, kSelThreads / 32);
-        __syncthreads();
-        const int eq_rank = carry_eq + (warp ? wtot_eq[warp - 1] : 0) + __popc(beq & ((1u << lane) - 1u));
-        const bool sel = gt || (eq && eq_rank < take_eq);
+        const int my_eq = eq_rank + __popc(beq & ((1u << lane) - 1u));
+        const bool sel = (in && key > T) || (eq && my_eq < take_eq);
         const unsigned bsel = __ballot_sync(0xffffffffu, sel);
-        if (lane == 0) wtot_sel[warp] = __popc(bsel);
-        __syncthreads();
-        scan_warp_totals(wtot_sel, kSelThreads / 32);
-        __syncthreads();
-        if (sel) kept[carry_sel + (warp ? wtot_sel[warp - 1] : 0) + __popc(bsel & ((1u << lane) - 1u))] = j;
-        carry_eq += wtot_eq[kSelThreads / 32 - 1];
-        carry_sel += wtot_sel[kSelThreads / 32 - 1];
-        __syncthreads();
+        if (sel) kept[out + __popc(bsel & ((1u << lane) - 1u))] = j;
+        eq_rank += __popc(beq);
+        out += __popc(bsel);
     }
 }
 

@@ -161,3 +161,31 @@ def test_synth_matches_oracle(mkv):
     u = mkv.synth_uniform((2, 500), SEED, 99, 1).cpu().numpy()
     for r in range(2):
         np.testing.assert_array_equal(u[r], oracle.port().synth_uniform(SEED, 99 + r, 500))
+
+
+@pytest.mark.parametrize("kind", ["half_points", "tiny_range", "huge_range", "constant_rows"])
+def test_quantizer_rounding_edges_bit_exact(mkv, kind):
+    """Quotients on/near the .5 rounding points, tiny and huge group ranges, constant groups:
+    codes and params must equal the reference's exact fp32 arithmetic (quantizer.cpp:28-53)."""
+    rng = np.random.default_rng(77)
+    L, d = 160, 128
+    if kind == "half_points":   # values on a 0.5 grid: many quotients exactly k + 0.5
+        k = (rng.integers(0, 7, (1, L, d)) * 0.5).astype(np.float16)
+    elif kind == "tiny_range":
+        k = (1000.0 + rng.integers(0, 4, (1, L, d)) * 0.5).astype(np.float16)
+    elif kind == "huge_range":
+        k = (rng.standard_normal((1, L, d)) * 3000.0).astype(np.float16)
+    else:
+        k = np.repeat(rng.standard_normal((1, L, 1)).astype(np.float16), d, axis=2)
+    v = k[:, ::-1].copy()
+    a = rng.random((1, L)).astype(np.float32)
+    cache = mkv.KVCache(1, L, 0, keep_fp32_params=True)
+    cache.prefill(torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda(), torch.from_numpy(a).cuda(), L, 0)
+    cache.check()
+    oc = oracle.port().cache()
+    oc.prefill(f32(k[0]), f32(v[0]), a[0], L, 0)
+    for which in (0, 1):
+        w, p, br = cache.export_reference(0, which)
+        w_ref, p_ref, br_ref = oc.export(which)
+        np.testing.assert_array_equal(w, w_ref)
+        np.testing.assert_array_equal(p, p_ref)
