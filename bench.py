@@ -71,48 +71,50 @@ def budgets_host(cfg):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
+    """SM clock and throttle reasons sampled DURING the timed region (NVML, 5 ms period;
+    nvidia-smi as a fallback)."""
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4}
 
     def __init__(self, index=0):
-        self.index, self.rows, self.proc = index, [], None
+        self.index, self.rows, self.stop = index, [], threading.Event()
+        self.max_mhz = None
+
+    def _poll(self):
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+            while not self.stop.is_set():
+                sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+                try:
+                    rs = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                except Exception:
+                    rs = N.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                self.rows.append((sm, rs))
+                time.sleep(0.005)
+        except Exception:
+            self.rows = []
 
     def __enter__(self):
-        try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-        except Exception:
-            self.proc = None
+        self.t = threading.Thread(target=self._poll, daemon=True)
+        self.t.start()
+        time.sleep(0.02)
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) == 6:
-                self.rows.append(parts)
-
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=2)
-            except Exception:
-                self.proc.kill()
+        self.stop.set()
+        self.t.join(timeout=2)
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower().startswith("active")})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"], "samples": 0}
+        sm = [r[0] for r in self.rows]
+        reasons = sorted({n for _, rs in self.rows for n, bit in self.REASONS.items() if rs & bit})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(self.rows)}
 
 
 def load_peaks():
@@ -227,7 +229,9 @@ def run_mkv(args, rank, world):
     tokens_per_s = world * B * args.steps / (ms / 1e3)
     res = dict(ms_per_step=ms_per_step, tokens_per_s=tokens_per_s,
                hbm_gbs=bytes_timed / (ms / 1e3) / 1e9 * world, clocks=clk.summary(), setup_s=setup_s,
-               gpu_launches=args.steps * NL * 2, preroll=preroll,
+               gpu_launches=args.steps * NL * 2 + NL * sum(1 for s in range(args.warmup, steps_total)
+                                                            if (preroll + s + 1) % n_r == 0),
+               preroll=preroll,
                flushes_in_timed=sum(1 for s in range(args.warmup, steps_total) if (preroll + s + 1) % n_r == 0))
     # ---- dominant kernel alone (K4 page kernel), CUDA events on its stream ----
     reps = 20
@@ -305,9 +309,35 @@ def run_prefill_bench(args):
     P = L * (L + 1) / 2
     flops = Hq * 6 * d * P
     acs = float(r.a_cumul.double().sum().item())
-    return {"workload": "Mistral-7B layer, 128K causal prefill (32q/8kv, d=128)", "ms": ms,
-            "tflops": flops / (ms / 1e3) / 1e12, "flop_count": "3 GEMM-eq = 6*d*L(L+1)/2 per q-head",
-            "a_cumul_sum_over_G_lq": acs / (Hq * L)}
+    _, bf16_peak, _, _ = load_peaks()
+    out = {"workload": "Mistral-7B layer, 128K causal prefill (32q/8kv, d=128)", "ms": ms,
+           "tflops": flops / (ms / 1e3) / 1e12, "frac_of_bf16_peak": flops / (ms / 1e3) / 1e12 / bf16_peak,
+           "flop_count": "3 GEMM-eq = 6*d*L(L+1)/2 per q-head", "a_cumul_sum_over_G_lq": acs / (Hq * L)}
+    # K2 + K3 on the same layer at the 20% budget (10% HH + 10% RW): selection + gather/pack
+    hh = rw = int(math.floor(0.10 * L))
+    ac = r.a_cumul.view(Hkv, L)
+    cache = mkv.KVCache(Hkv, hh + rw, 0)
+    kk, vv = k.view(Hkv, L, d), v.view(Hkv, L, d)
+    kept, nk = mkv.select_token_counts(ac, hh, rw)
+    cache.prefill_kept(kk, vv, kept, nk)
+    torch.cuda.synchronize()
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    e[0].record()
+    for _ in range(5):
+        kept, nk = mkv.select_token_counts(ac, hh, rw)
+    e[1].record()
+    for _ in range(5):
+        cache.prefill_kept(kk, vv, kept, nk)
+    e[2].record()
+    torch.cuda.synchronize()
+    t2, t3 = e[0].elapsed_time(e[1]) / 5, e[1].elapsed_time(e[2]) / 5
+    n_kept = hh + rw
+    out["select_ms"] = t2
+    out["select_gbs"] = Hkv * (4 * L + 4 * n_kept) / (t2 / 1e3) / 1e9
+    out["pack_ms"] = t3
+    out["pack_gbs"] = Hkv * n_kept * (4 * d + 4 + d) / (t3 / 1e3) / 1e9
+    cache.close()
+    return out
 
 
 # ---------------------------------------------------------------------------
