@@ -458,19 +458,17 @@ cudaError_t launch_append(const ResidualParams& p, cudaStream_t s) {
 // ---------------------------------------------------------------------------
 // finish kernel: (append) + residual attention on tensor cores + split-K merge
 // ---------------------------------------------------------------------------
-constexpr int kFinishWarps = 8;  // one warp per 16-token residual tile (n_r <= 128)
-constexpr int kResStride = kHeadDim + 8;  // halves: 272-byte rows -> conflict-free fragment loads
-constexpr int kMaxPart = 16;     // page partials staged per merge pass
+// Finish kernel (one CTA per unit, launched with PDL): decode_append and the exact fp16
+// residual attention first, then -- after griddepcontrol.wait -- a single-round split-K
+// merge of the residual and page partials (online max, no extra barriers).
+constexpr int kFinishWarps = 8;
+constexpr int kFinishThreads = kFinishWarps * 32;
 
 struct FinishSmem {
-    __half k[128][kResStride];
-    __half v[128][kResStride];
-    __half q[kMaxG * kHeadDim];
+    // per warp: 16 K rows + 16 V rows (swizzled 16-byte chunks); afterwards the warp's
+    // residual partial o[G][128] (fp32, <= 4 KB) reuses the same bytes
+    uint8_t tile[kFinishWarps][8192];
     float wml[kFinishWarps][2][kMaxG];
-    float wo[kFinishWarps][kMaxG][kHeadDim];
-    float pml[kMaxPart][2][kMaxG];
-    float po[kMaxPart][kMaxG][kHeadDim];
-    float M[kMaxG], L[kMaxG];
 };
 
 __device__ __forceinline__ void ldmatrix_x4_trans(uint32_t (&r)[4], const void* p) {
@@ -479,23 +477,7 @@ __device__ __forceinline__ void ldmatrix_x4_trans(uint32_t (&r)[4], const void* 
                  : "r"(smem_u32(p)));
 }
 
-// async-stage page partials [w0, w0 + np) of local unit i (o rows for G heads + m/l)
-__device__ __forceinline__ void stage_partials(FinishSmem& S, const ResidualParams& P, int i, int w0, int np, int G,
-                                               int tid) {
-    const int per = G * kHeadDim / 4;  // float4 chunks per partial
-    for (int e = tid; e < np * per; e += blockDim.x) {
-        const int w = e / per, r = e % per;
-        cp_async16(reinterpret_cast<float4*>(&S.po[w][0][0]) + r,
-                   reinterpret_cast<const float4*>(P.part_o + (size_t)(w0 + w + i) * kMaxG * kHeadDim) + r);
-    }
-    for (int e = tid; e < np * 4; e += blockDim.x) {  // 2 * kMaxG floats = 4 x float4
-        const int w = e >> 2, r = e & 3;
-        cp_async16(reinterpret_cast<float4*>(&S.pml[w][0][0]) + r,
-                   reinterpret_cast<const float4*>(P.part_ml + (size_t)(w0 + w + i) * 2 * kMaxG) + r);
-    }
-}
-
-__global__ void __launch_bounds__(kFinishWarps * 32) finish_kernel(const ResidualParams P, const int32_t* __restrict__ pref,
+__global__ void __launch_bounds__(kFinishThreads, 2) finish_kernel(const ResidualParams P, const int32_t* __restrict__ pref,
                                                                    int chunk) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
     FinishSmem& S = *reinterpret_cast<FinishSmem*>(smem_raw);
@@ -505,151 +487,170 @@ __global__ void __launch_bounds__(kFinishWarps * 32) finish_kernel(const Residua
     const int u = P.unit_begin + i;
     const int d = kHeadDim;
     const int G = P.group;
-    const UnitMeta meta = P.meta[u];
-    __half* rk = P.res_k + (size_t)u * P.n_r * d;
-    __half* rv = P.res_v + (size_t)u * P.n_r * d;
-    const int n_old = meta.n_res;
+    // pre-wait prologue: meta / plan were produced before the page kernel started
+    const int n_old = P.meta[u].n_res;
+    const bool app = P.k_new != nullptr;
+    const int n = n_old + (app ? 1 : 0);
+    const int ntiles = (n + 15) >> 4;
     const int upre = pref[i], uend = pref[i + 1];
     const int w_first = upre / chunk, w_last = (uend > upre) ? (uend - 1) / chunk : w_first - 1;
     const int n_part = w_last - w_first + 1;
-
-    // ---- one burst of async copies: residual rows, q, first kMaxPart page partials ----
-    for (int e = tid; e < n_old * 16; e += blockDim.x) {
-        const int r = e >> 4, c16 = e & 15;
-        cp_async16(&S.k[r][8 * c16], reinterpret_cast<const uint4*>(rk + (size_t)r * d) + c16);
-        cp_async16(&S.v[r][8 * c16], reinterpret_cast<const uint4*>(rv + (size_t)r * d) + c16);
-    }
-    for (int e = tid; e < G * d / 8; e += blockDim.x)
-        cp_async16(reinterpret_cast<uint4*>(S.q) + e, reinterpret_cast<const uint4*>(P.q + (size_t)i * G * d) + e);
-    // PDL: the page kernel's partials are complete past this point; fetch them in the same burst
-    asm volatile("griddepcontrol.wait;\n" ::: "memory");
-    stage_partials(S, P, i, w_first, min(n_part, kMaxPart), G, tid);
-    cp_async_commit();
-    // decode_append (cache_engine.cpp:79-90) -- the flush case was handled by append_kernel
-    int n = n_old;
-    if (P.k_new) {
-        if (tid < 16) {
-            const uint4 x = reinterpret_cast<const uint4*>(P.k_new + (size_t)i * d)[tid];
-            reinterpret_cast<uint4*>(rk + (size_t)n * d)[tid] = x;
-            *reinterpret_cast<uint4*>(&S.k[n][8 * tid]) = x;
-        } else if (tid < 32) {
-            const uint4 x = reinterpret_cast<const uint4*>(P.v_new + (size_t)i * d)[tid - 16];
-            reinterpret_cast<uint4*>(rv + (size_t)n * d)[tid - 16] = x;
-            *reinterpret_cast<uint4*>(&S.v[n][8 * (tid - 16)]) = x;
-        }
-        if (tid == 0) P.meta[u].n_res = n + 1;
-        ++n;
-    }
-    cp_async_wait_all();
-    __syncthreads();
-
-    // ---- residual tile attention: warp w owns tokens [16w, 16w + 16) ----
-    const int ntiles = (n + 15) >> 4;
+    __half* rk = P.res_k + (size_t)u * P.n_r * d;
+    __half* rv = P.res_v + (size_t)u * P.n_r * d;
     const float sl2 = P.scale_log2;
-    if (warp < ntiles) {
-        const int t0 = 16 * warp;
-        uint32_t qb[8][2];
+    const int h0 = 2 * tig, h1 = 2 * tig + 1;
+
+    // ---- residual attention (overlaps the page kernel): warp w owns tiles w, w + 4 ----
+    uint32_t qb[8][2];
 #pragma unroll
-        for (int kc = 0; kc < 8; ++kc)
+    for (int kc = 0; kc < 8; ++kc)
 #pragma unroll
-            for (int p = 0; p < 2; ++p)
-                qb[kc][p] = (gid < G) ? *reinterpret_cast<const uint32_t*>(S.q + gid * d + 16 * kc + 2 * tig + 8 * p) : 0u;
+        for (int p = 0; p < 2; ++p)
+            qb[kc][p] = (gid < G) ? __ldg(reinterpret_cast<const uint32_t*>(P.q + ((size_t)i * G + gid) * d + 16 * kc +
+                                                                              2 * tig + 8 * p))
+                                  : 0u;
+    float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.0f, l1 = 0.0f;
+    float O[8][4];
+#pragma unroll
+    for (int g = 0; g < 8; ++g) O[g][0] = O[g][1] = O[g][2] = O[g][3] = 0.0f;
+    uint8_t* tile = S.tile[warp];
+    // rows past the residual count are multiplied by p = 0: they must hold finite values
+    for (int e = lane; e < 8192 / 16; e += 32) reinterpret_cast<uint4*>(tile)[e] = make_uint4(0, 0, 0, 0);
+    __syncwarp();
+    for (int t = warp; t < ntiles; t += kFinishWarps) {
+        const int row0 = 16 * t;
+        const int nrows = min(16, n_old - row0);  // rows already in the residual buffer
+        for (int e = lane; e < 256; e += 32) {
+            const int r = e >> 4, cc = e & 15;
+            if (r < nrows) {
+                const int off = r * 256 + ((cc ^ (r & 7)) << 4);
+                cp_async16(tile + off, rk + (size_t)(row0 + r) * d + cc * 8);
+                cp_async16(tile + 4096 + off, rv + (size_t)(row0 + r) * d + cc * 8);
+            }
+        }
+        cp_async_commit();
+        if (app && n_old >= row0 && n_old < row0 + 16) {  // decode_append (cache_engine.cpp:79-90)
+            const int r = n_old - row0, cc = lane & 15;
+            const bool is_v = lane >= 16;
+            const uint4 x = reinterpret_cast<const uint4*>((is_v ? P.v_new : P.k_new) + (size_t)i * d)[cc];
+            reinterpret_cast<uint4*>((is_v ? rv : rk) + (size_t)n_old * d)[cc] = x;
+            *reinterpret_cast<uint4*>(tile + (is_v ? 4096 : 0) + r * 256 + ((cc ^ (r & 7)) << 4)) = x;
+        }
+        cp_async_wait_all();
+        __syncwarp();
         float Sx[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
         for (int kc = 0; kc < 8; ++kc) {
             uint32_t a[4];
-            a[0] = *reinterpret_cast<const uint32_t*>(&S.k[t0 + gid][16 * kc + 2 * tig]);
-            a[1] = *reinterpret_cast<const uint32_t*>(&S.k[t0 + gid + 8][16 * kc + 2 * tig]);
-            a[2] = *reinterpret_cast<const uint32_t*>(&S.k[t0 + gid][16 * kc + 2 * tig + 8]);
-            a[3] = *reinterpret_cast<const uint32_t*>(&S.k[t0 + gid + 8][16 * kc + 2 * tig + 8]);
+            a[0] = *reinterpret_cast<const uint32_t*>(tile + gid * 256 + (((2 * kc) ^ gid) << 4) + 4 * tig);
+            a[1] = *reinterpret_cast<const uint32_t*>(tile + (gid + 8) * 256 + (((2 * kc) ^ gid) << 4) + 4 * tig);
+            a[2] = *reinterpret_cast<const uint32_t*>(tile + gid * 256 + (((2 * kc + 1) ^ gid) << 4) + 4 * tig);
+            a[3] = *reinterpret_cast<const uint32_t*>(tile + (gid + 8) * 256 + (((2 * kc + 1) ^ gid) << 4) + 4 * tig);
             mma_16816(Sx, a, qb[kc][0], qb[kc][1]);
         }
+        const int valid = n - row0;
         float x0 = Sx[0] * sl2, x1 = Sx[1] * sl2, x2 = Sx[2] * sl2, x3 = Sx[3] * sl2;
-        if (t0 + gid >= n) { x0 = -INFINITY; x1 = -INFINITY; }
-        if (t0 + gid + 8 >= n) { x2 = -INFINITY; x3 = -INFINITY; }
+        if (gid >= valid) { x0 = -INFINITY; x1 = -INFINITY; }
+        if (gid + 8 >= valid) { x2 = -INFINITY; x3 = -INFINITY; }
         float mx0 = fmaxf(x0, x2), mx1 = fmaxf(x1, x3);
 #pragma unroll
         for (int o = 4; o < 32; o <<= 1) {
             mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
             mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
         }
-        const float p0 = fast_exp2(x0 - mx0), p1 = fast_exp2(x1 - mx1);
-        const float p2 = fast_exp2(x2 - mx0), p3 = fast_exp2(x3 - mx1);
-        float l0 = p0 + p2, l1 = p1 + p3;
+        const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+        const float a0 = fast_exp2(m0 - mn0), a1 = fast_exp2(m1 - mn1);
+        m0 = mn0; m1 = mn1;
+        l0 *= a0; l1 *= a1;
 #pragma unroll
-        for (int o = 4; o < 32; o <<= 1) {
-            l0 += __shfl_xor_sync(0xffffffffu, l0, o);
-            l1 += __shfl_xor_sync(0xffffffffu, l1, o);
-        }
+        for (int g = 0; g < 8; ++g) { O[g][0] *= a0; O[g][1] *= a1; O[g][2] *= a0; O[g][3] *= a1; }
+        const float p0 = fast_exp2(x0 - m0), p1 = fast_exp2(x1 - m1);
+        const float p2 = fast_exp2(x2 - m0), p3 = fast_exp2(x3 - m1);
+        l0 += p0 + p2;
+        l1 += p1 + p3;
         const uint32_t pb0 = movmatrix_trans(pack_half2(p0, p1));
         const uint32_t pb1 = movmatrix_trans(pack_half2(p2, p3));
-        // O[c][h] = sum_t V^T[c][t] P[t][h]; A fragments via ldmatrix.trans of V[t][c]:
-        // matrices m0 (t0-7, c0-7) m1 (t0-7, c8-15) m2 (t8-15, c0-7) m3 (t8-15, c8-15)
-        // = fragment registers a0 (c0-7, t0-7) a1 (c8-15, t0-7) a2 (c0-7, t8-15) a3 (c8-15, t8-15)
+        // O[c][h] += sum_t V^T[c][t] P[t][h]; ldmatrix.trans of the swizzled V rows:
+        // m0 (t0-7, c0-7) m1 (t0-7, c8-15) m2 (t8-15, c0-7) m3 (t8-15, c8-15) = a0 a1 a2 a3
         const int mi = lane >> 3, ri = lane & 7;
-        const int h0 = 2 * tig, h1 = 2 * tig + 1;
+        const int vr = ri + 8 * (mi >> 1);
 #pragma unroll
         for (int g = 0; g < 8; ++g) {
             uint32_t a[4];
-            ldmatrix_x4_trans(a, &S.v[t0 + ri + 8 * (mi >> 1)][16 * g + 8 * (mi & 1)]);
-            float o[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-            mma_16816(o, a, pb0, pb1);
-            const int c = 16 * g + gid;
-            if (h0 < G) { S.wo[warp][h0][c] = o[0]; S.wo[warp][h0][c + 8] = o[2]; }
-            if (h1 < G) { S.wo[warp][h1][c] = o[1]; S.wo[warp][h1][c + 8] = o[3]; }
+            ldmatrix_x4_trans(a, tile + 4096 + vr * 256 + ((((2 * g) + (mi & 1)) ^ (vr & 7)) << 4));
+            mma_16816(O[g], a, pb0, pb1);
         }
-        if (gid == 0) {
-            if (h0 < G) { S.wml[warp][0][h0] = mx0; S.wml[warp][1][h0] = l0; }
-            if (h1 < G) { S.wml[warp][0][h1] = mx1; S.wml[warp][1][h1] = l1; }
-        }
+        __syncwarp();
     }
-    __syncthreads();
-
-    // ---- split-K merge over residual tiles and page partials (staged in passes of kMaxPart) ----
-    if (tid < G) {
-        float M = -INFINITY;
-        for (int w = 0; w < ntiles; ++w) M = fmaxf(M, S.wml[w][0][tid]);
-        const int np0 = min(n_part, kMaxPart);
-        for (int w = 0; w < np0; ++w) M = fmaxf(M, S.pml[w][0][tid]);  // staged copy
-        for (int w = w_first + np0; w <= w_last; ++w) M = fmaxf(M, __ldcg(P.part_ml + (size_t)(w + i) * 2 * kMaxG + tid));
-        S.M[tid] = M;
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+        l0 += __shfl_xor_sync(0xffffffffu, l0, o);
+        l1 += __shfl_xor_sync(0xffffffffu, l1, o);
     }
-    __syncthreads();
-    // thread -> (h, c) pairs: G * d outputs / 256 threads
-    float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f}, lsum[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-    const int nout = (G * d + blockDim.x - 1) / blockDim.x;  // 1..4
-    for (int r = 0; r < nout; ++r) {
-        const int e = min(tid + r * (int)blockDim.x, G * d - 1), h = e / d, c = e % d;
-        const float M = S.M[h];
-        for (int w = 0; w < ntiles; ++w) {
-            const float sc = fast_exp2(S.wml[w][0][h] - M);
-            acc[r] += S.wo[w][h][c] * sc;
-            lsum[r] += S.wml[w][1][h] * sc;
-        }
+    // warp partial -> smem over the warp's (now idle) tile buffer (l = 0 for warps without tiles)
+    float* wo = reinterpret_cast<float*>(tile);  // [kMaxG][128]
+    __syncwarp();
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+        const int c = 16 * g + gid;
+        if (h0 < G) { wo[h0 * kHeadDim + c] = O[g][0]; wo[h0 * kHeadDim + c + 8] = O[g][2]; }
+        if (h1 < G) { wo[h1 * kHeadDim + c] = O[g][1]; wo[h1 * kHeadDim + c + 8] = O[g][3]; }
     }
-    for (int w0 = w_first; w0 <= w_last; w0 += kMaxPart) {
-        const int np = min(kMaxPart, w_last - w0 + 1);
-        if (w0 != w_first) {
-            __syncthreads();
-            stage_partials(S, P, i, w0, np, G, tid);
-            cp_async_commit();
-            cp_async_wait_all();
-            __syncthreads();
-        }
-        for (int r = 0; r < nout; ++r) {
-            const int e = min(tid + r * (int)blockDim.x, G * d - 1), h = e / d, c = e % d;
-            const float M = S.M[h];
-#pragma unroll 4
-            for (int w = 0; w < np; ++w) {
-                const float sc = fast_exp2(S.pml[w][0][h] - M);
-                acc[r] += S.po[w][h][c] * sc;
-                lsum[r] += S.pml[w][1][h] * sc;
+    if (gid == 0) {
+        if (h0 < G) { S.wml[warp][0][h0] = m0; S.wml[warp][1][h0] = l0; }
+        if (h1 < G) { S.wml[warp][0][h1] = m1; S.wml[warp][1][h1] = l1; }
+    }
+    if (app && tid == 0) P.meta[u].n_res = n;  // only this CTA reads this unit's n_res after the append
+    // ---- the page partials are complete past this point ----
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    __syncthreads();  // residual warp partials visible
+    // Single-round merge: every thread loads (m, l, o) of up to 16 page partials at once and
+    // folds them with an online max (no global-max pass, no further barriers).
+    for (int e = tid; e < G * (d / 2); e += kFinishThreads) {
+        const int h = e / (d / 2), c2 = e % (d / 2);
+        float M = -INFINITY, L = 0.0f, ax = 0.0f, ay = 0.0f;
+        for (int w = 0; w < kFinishWarps; ++w) {
+            const float lw = S.wml[w][1][h];
+            if (lw > 0.0f) {
+                const float mw = S.wml[w][0][h];
+                const float nm = fmaxf(M, mw);
+                const float f = fast_exp2(M - nm), s = fast_exp2(mw - nm);
+                const float2 wv = reinterpret_cast<const float2*>(S.tile[w])[h * (kHeadDim / 2) + c2];
+                ax = fmaf(wv.x, s, ax * f);
+                ay = fmaf(wv.y, s, ay * f);
+                L = fmaf(lw, s, L * f);
+                M = nm;
             }
         }
-    }
-    for (int r = 0; r < nout; ++r) {
-        const int e = tid + r * blockDim.x, h = e / d, c = e % d;
-        if (e < G * d) P.out[((size_t)i * G + h) * d + c] = __float2half_rn(acc[r] / lsum[r]);
+        for (int p0 = 0; p0 < n_part; p0 += 16) {
+            float pm[16], pl[16];
+            float2 po[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                const int slot = w_first + p0 + k + i;
+                const bool ok = p0 + k < n_part;
+                pm[k] = ok ? __ldcg(P.part_ml + (size_t)slot * 2 * kMaxG + h) : -INFINITY;
+                pl[k] = ok ? __ldcg(P.part_ml + (size_t)slot * 2 * kMaxG + kMaxG + h) : 0.0f;
+                po[k] = ok ? __ldcg(reinterpret_cast<const float2*>(P.part_o + ((size_t)slot * kMaxG + h) * d) + c2)
+                           : make_float2(0.0f, 0.0f);
+            }
+            float cm = pm[0];
+#pragma unroll
+            for (int k = 1; k < 16; ++k) cm = fmaxf(cm, pm[k]);
+            const float nm = fmaxf(M, cm);
+            const float f = fast_exp2(M - nm);
+            ax *= f; ay *= f; L *= f;
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                const float s = fast_exp2(pm[k] - nm);  // 0 for absent partials (m = -inf)
+                ax = fmaf(po[k].x, s, ax);
+                ay = fmaf(po[k].y, s, ay);
+                L = fmaf(pl[k], s, L);
+            }
+            M = nm;
+        }
+        const float li = 1.0f / L;
+        reinterpret_cast<__half2*>(P.out + ((size_t)i * G + h) * d)[c2] = __floats2half2_rn(ax * li, ay * li);
     }
 }
 
@@ -661,7 +662,7 @@ cudaError_t launch_finish(const ResidualParams& p, const int32_t* pref, int chun
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    return launch_pdl(finish_kernel, dim3(p.n_units), dim3(kFinishWarps * 32), smem, s, p, pref, chunk);
+    return launch_pdl(finish_kernel, dim3(p.n_units), dim3(kFinishThreads), smem, s, p, pref, chunk);
 }
 
 }  // namespace mkv
