@@ -21,8 +21,8 @@
 //                  tile), and the split-K merge of every partial into out.
 //
 // Dequantization never materialises fp16 K/V: each 2-bit code becomes an fp16
-// *subnormal* code * 4^s * 2^-24 with one LOP3 (s = kc mod 3 after a 0/6/12-bit
-// shift), the 4^-s and the per-channel key scale are folded into the query
+// *subnormal* code * 4^s * 2^-24 with one LOP3 (s = position for the first five codes of a
+// word, after one 10-bit shift for the last three), the 4^-s and the per-channel key scale are folded into the query
 // fragment, the per-token value scale into the probability fragment, and the
 // zero points enter through one extra mma per page (keys: sum_c q_c z_c over a
 // 4-page batch; values: sum_t p_t z_t).  See DESIGN.md.
@@ -53,9 +53,14 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
-__device__ __forceinline__ float extract_scale(int k) {  // 2^24 * 4^-(k mod 3)
-    return kTwo24 * ((k % 3 == 0) ? 1.0f : ((k % 3 == 1) ? 0.25f : 0.0625f));
+// Code position k (0..7) of a word: k < 5 is read in place (bits 2k, 16+2k lie in the fp16
+// mantissa: value code * 4^k * 2^-24); k >= 5 after one shift by 10 (value code * 4^(k-5) * 2^-24).
+__host__ __device__ constexpr int code_class(int k) { return k < 5 ? k : k - 5; }
+__host__ __device__ constexpr int code_shift(int k) { return k < 5 ? 0 : 10; }
+__host__ __device__ constexpr float pow4_neg(int s) {  // 4^-s, exact
+    return s == 0 ? 1.0f : (s == 1 ? 0.25f : (s == 2 ? 0.0625f : (s == 3 ? 0.015625f : 0.00390625f)));
 }
+__device__ __forceinline__ float extract_scale(int k) { return kTwo24 * pow4_neg(code_class(k)); }
 
 // q of local unit i, head gid (zero for gid >= G), staged in smem, -> B fragments
 __device__ __forceinline__ void load_q_frags(const __half* qs_smem, int G, int gid, int tig, uint32_t (&qb)[8][2],
@@ -67,7 +72,7 @@ __device__ __forceinline__ void load_q_frags(const __half* qs_smem, int G, int g
             uint32_t v = 0;
             if (gid < G) v = *reinterpret_cast<const uint32_t*>(qs_smem + gid * kHeadDim + 16 * kc + 2 * tig + 8 * p);
             qb[kc][p] = v;
-            const float f = (kc % 3 == 0) ? 1.0f : ((kc % 3 == 1) ? 0.25f : 0.0625f);
+            const float f = pow4_neg(code_class(kc));
             qsc[kc][p] = hmul2_u32(v, pack_half2(f, f));
         }
     }
@@ -237,8 +242,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pages_kernel(const PagesParams
             }
 #pragma unroll
             for (int kc = 0; kc < 8; ++kc) {
-                const int sh = (kc < 3) ? 0 : ((kc < 6) ? 6 : 12);
-                const uint32_t mask = 0x00030003u << (2 * (kc % 3));
+                const int sh = code_shift(kc);
+                const uint32_t mask = 0x00030003u << (2 * code_class(kc));
 #pragma unroll
                 for (int j = 0; j < kBatch; ++j) {
                     const uint2 ks = lds64(buf + j * kPageBytes + kKS + ((kc >> 1) * 4 + tig) * 16 + (kc & 1) * 8);
@@ -305,8 +310,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pages_kernel(const PagesParams
                 const uint4 vw = lds128(page + kVC + lane * 16);
 #pragma unroll
                 for (int g = 0; g < 8; ++g) {
-                    const int sh = (g < 3) ? 0 : ((g < 6) ? 6 : 12);
-                    const uint32_t mask = 0x00030003u << (2 * (g % 3));
+                    const int sh = code_shift(g);
+                    const uint32_t mask = 0x00030003u << (2 * code_class(g));
                     const uint2 vs = lds64(page + kVS + ((g >> 1) * 4 + tig) * 16 + (g & 1) * 8);
                     const uint32_t a[4] = {(vw.x >> sh) & mask, (vw.y >> sh) & mask, (vw.z >> sh) & mask,
                                            (vw.w >> sh) & mask};
