@@ -512,7 +512,7 @@ static int decode_impl(mkv_cache* c, const mkv_decode_args* a, bool attend, cuda
         fill_pages_params(c, pl, a, pp);
         CK(launch_pages(pp, pl->grid, s));
     }
-    CK(launch_finish(rp, pl->d_pref, std::max(pl->chunk, 1), s));
+    CK(launch_finish(rp, pl->d_pref, std::max(pl->chunk, 1), pl->total > 0, s));
     return MKV_OK;
 }
 

@@ -136,12 +136,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pages_kernel(const PagesParams
         fence_mbar_init();
     }
     __syncwarp();
-    // PDL: everything above overlapped the previous kernel's tail; inputs are read below
-    asm volatile("griddepcontrol.wait;\n" ::: "memory");
-    if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
-
     ci = __ldg(P.wstart + wg);  // first unit of this warp's range (host plan)
-    prefetch_q(ci);
     // ---- producer cursor (warp-uniform) ----
     int pi = ci;
     int pg = start;
@@ -165,7 +160,14 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pages_kernel(const PagesParams
             p_base = P.pool + (P.meta[P.unit_begin + pi].page_base - __ldg(P.pref + pi)) * kPageBytes;
         }
     };
+    // The first kStages batches are requested before griddepcontrol.wait: under PDL they
+    // overlap the previous kernel's tail.  Safe because no kernel that may still be running
+    // writes these pages (the append kernel of a flush step is a full-dependency launch)
+    // or the plan/meta fields read here; q is read and partials are written after the wait.
     for (int s = 0; s < kStages; ++s) issue(s);
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    prefetch_q(ci);
 
     int cg = start;
     int stage = 0;
@@ -504,6 +506,9 @@ __global__ void __launch_bounds__(kFinishThreads, 2) finish_kernel(const Residua
     __half* rv = P.res_v + (size_t)u * P.n_r * d;
     const float sl2 = P.scale_log2;
     const int h0 = 2 * tig, h1 = 2 * tig + 1;
+    // the next layer's page kernel may start its prologue and first page loads on SMs this
+    // grid leaves free (it reads nothing this kernel writes before its own griddepcontrol.wait)
+    if (tid == 0) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 
     // ---- residual attention (overlaps the page kernel): warp w owns tiles w, w + 4 ----
     uint32_t qb[8][2];
@@ -659,13 +664,19 @@ __global__ void __launch_bounds__(kFinishThreads, 2) finish_kernel(const Residua
     }
 }
 
-cudaError_t launch_finish(const ResidualParams& p, const int32_t* pref, int chunk, cudaStream_t s) {
+cudaError_t launch_finish(const ResidualParams& p, const int32_t* pref, int chunk, bool after_pages, cudaStream_t s) {
     const size_t smem = sizeof(FinishSmem);
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         configured = true;
+    }
+    // PDL only behind a page kernel: a finish that follows another finish (no pages) reads
+    // the n_res / residual rows that kernel writes, so it needs the full dependency
+    if (!after_pages) {
+        finish_kernel<<<p.n_units, kFinishThreads, smem, s>>>(p, pref, chunk);
+        return cudaGetLastError();
     }
     return launch_pdl(finish_kernel, dim3(p.n_units), dim3(kFinishThreads), smem, s, p, pref, chunk);
 }

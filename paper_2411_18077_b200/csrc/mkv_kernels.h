@@ -58,7 +58,7 @@ struct ResidualParams {
     uint32_t* status;
 };
 cudaError_t launch_append(const ResidualParams& p, cudaStream_t s);
-cudaError_t launch_finish(const ResidualParams& p, const int32_t* pref, int chunk, cudaStream_t s);
+cudaError_t launch_finish(const ResidualParams& p, const int32_t* pref, int chunk, bool after_pages, cudaStream_t s);
 
 struct PagesParams {
     const uint8_t* pool;
