@@ -177,6 +177,10 @@ int mkv_cache_append(mkv_cache* cache, int unit_begin, int n_units, const void* 
  * reusing the residual partials of the previous mkv_decode_step on the same
  * units.  Used by bench.py to time the dominant kernel for its roofline. */
 int mkv_decode_pages_only(mkv_cache* cache, const mkv_decode_args* args, void* stream);
+/* Diagnostics: per-warp timeline of the latest K4 page kernel (only when the process
+ * runs with MKV_DECODE_TRACE set): 4 globaltimer stamps per warp {start, after
+ * griddepcontrol.wait, pages done, 0}.  Returns words written. */
+int mkv_debug_decode_trace(const mkv_cache* cache, uint64_t* out, int max_words);
 /* Multi-layer decode step: n_layers consecutive calls in one FFI crossing. */
 int mkv_decode_step_layers(mkv_cache* cache, int n_layers, const mkv_decode_args* args,
                            void* stream);

@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libminikv_b200.so")
+LIB_PATH = os.environ.get("MKV_LIB_PATH") or os.path.join(HERE, "libminikv_b200.so")  # override: A/B builds
 HEADER = os.path.join(os.path.dirname(HERE), "include", "minikv_b200.h")
 
 MKV_OK = 0
@@ -108,7 +108,7 @@ EXPORTS = [
     "mkv_prefill_attn", "mkv_select", "mkv_allocate_pyramid", "mkv_allocate_uniform",
     "mkv_cache_create", "mkv_cache_destroy", "mkv_cache_bytes", "mkv_cache_unit_info",
     "mkv_cache_prefill", "mkv_cache_prefill_select", "mkv_decode_step", "mkv_cache_append",
-    "mkv_decode_step_layers", "mkv_decode_pages_only", "mkv_cache_export_sizes", "mkv_cache_export_reference",
+    "mkv_decode_step_layers", "mkv_debug_decode_trace", "mkv_decode_pages_only", "mkv_cache_export_sizes", "mkv_cache_export_reference",
     "mkv_cache_export_residual", "mkv_cache_check",
     "mkv_synth_fp16", "mkv_synth_fp16_rows", "mkv_synth_uniform_f32",
 ]
@@ -144,6 +144,8 @@ def lib():
     L.mkv_cache_export_reference.argtypes = [vp, i32, i32, vp, vp, vp]
     L.mkv_cache_export_residual.argtypes = [vp, i32, vp, vp]
     L.mkv_cache_check.argtypes = [vp]
+    if hasattr(L, "mkv_debug_decode_trace"):  # diagnostics entry (absent in older A/B builds)
+        L.mkv_debug_decode_trace.argtypes = [vp, vp, i32]
     L.mkv_synth_fp16.argtypes = [vp, i64, C.c_uint64, C.c_uint64, vp]
     L.mkv_synth_fp16_rows.argtypes = [vp, i64, i64, i64, C.c_uint64, C.c_uint64, C.c_uint64, vp]
     L.mkv_synth_uniform_f32.argtypes = [vp, i64, i64, i64, C.c_uint64, C.c_uint64, C.c_uint64, vp]

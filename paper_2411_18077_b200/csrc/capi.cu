@@ -9,6 +9,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -98,6 +99,7 @@ struct mkv_cache {
     uint32_t* d_status = nullptr;
     float* d_part_ml = nullptr;
     float* d_part_o = nullptr;
+    uint64_t* d_trace = nullptr;  // diagnostics only (MKV_DECODE_TRACE)
     int part_slots = 0;
     std::unordered_map<uint64_t, Plan> plans;  // key: (unit_begin, n_units)
 
@@ -105,7 +107,7 @@ struct mkv_cache {
         for (auto& kv : plans) cudaFree(kv.second.d_pref);
         cudaFree(d_meta); cudaFree(d_pool); cudaFree(d_shadow); cudaFree(d_res_k); cudaFree(d_res_v);
         cudaFree(d_status);
-        cudaFree(d_part_ml); cudaFree(d_part_o);
+        cudaFree(d_part_ml); cudaFree(d_part_o); cudaFree(d_trace);
     }
 
     UnitMeta meta_of(int u) const {
@@ -453,6 +455,12 @@ static void fill_pages_params(mkv_cache* c, const Plan* pl, const mkv_decode_arg
     pp.n_warps = pl->grid * pages_config().warps;
     pp.part_ml = c->d_part_ml; pp.part_o = c->d_part_o;
     pp.scale_log2 = a->scale * 1.4426950408889634f;
+    pp.trace = nullptr;
+    static const bool tracing = getenv("MKV_DECODE_TRACE") != nullptr;
+    if (tracing) {  // per-warp timeline of the most recent page kernel (mkv_debug_decode_trace)
+        if (!c->d_trace) cudaMalloc(&c->d_trace, sizeof(uint64_t) * 4 * num_sms() * kMaxPagesWarps);
+        pp.trace = c->d_trace;
+    }
 }
 
 static int decode_impl(mkv_cache* c, const mkv_decode_args* a, bool attend, cudaStream_t s) {
@@ -514,6 +522,15 @@ static int decode_impl(mkv_cache* c, const mkv_decode_args* a, bool attend, cuda
     }
     CK(launch_finish(rp, pl->d_pref, std::max(pl->chunk, 1), pl->total > 0, s));
     return MKV_OK;
+}
+
+int mkv_debug_decode_trace(const mkv_cache* c, uint64_t* out, int max_words) {
+    if (!c || !out) return fail(MKV_ERR_INVALID_ARGUMENT, "trace: null");
+    if (!c->d_trace) return fail(MKV_ERR_RUNTIME, "trace: run with MKV_DECODE_TRACE set");
+    CK(cudaDeviceSynchronize());
+    const int n = std::min(max_words, 4 * num_sms() * kMaxPagesWarps);
+    CK(cudaMemcpy(out, c->d_trace, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost));
+    return n;
 }
 
 int mkv_decode_step(mkv_cache* c, const mkv_decode_args* a, void* stream) {

@@ -113,6 +113,14 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pages_kernel(const PagesParams
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)kWarps * kWarpSmem) + warp * kStages;
 
     const int wg = blockIdx.x * kWarps + warp;
+    auto stamp = [&](int k) {
+        if (P.trace != nullptr && lane == 0) {
+            uint64_t t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            P.trace[(size_t)wg * 4 + k] = t;
+        }
+    };
+    stamp(0);
     const int start = wg * P.chunk;
     const int end = min(start + P.chunk, P.total_pages);
     if (start >= end) return;
@@ -167,6 +175,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pages_kernel(const PagesParams
     for (int s = 0; s < kStages; ++s) issue(s);
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
     if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    stamp(1);
     prefetch_q(ci);
 
     int cg = start;
@@ -360,6 +369,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pages_kernel(const PagesParams
             }
         }
     }
+    stamp(2);
 }
 
 template <int W, int S>

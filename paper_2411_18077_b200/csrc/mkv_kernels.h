@@ -71,6 +71,7 @@ struct PagesParams {
     float* part_ml;         // [slots][2][kMaxG]   slot = warp + unit
     float* part_o;          // [slots][kMaxG][d]
     float scale_log2;
+    uint64_t* trace;        // diagnostics: per warp {start, after wait, done} (globaltimer), or null
 };
 constexpr int kMaxPagesWarps = 12;  // partial-slot sizing
 struct PagesConfig {

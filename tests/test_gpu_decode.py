@@ -106,3 +106,32 @@ def test_decode_residual_only_unit(mkv):
                                 torch.from_numpy(tv).cuda(), 0.1).float().cpu().numpy()
         exp = oc.decode_step(f32(q[0, 0]), f32(tk[0]), f32(tv[0]), 0.1, param_fp16=True)
         assert max_abs(out[0, 0], exp) <= TOL
+
+
+def test_decode_residual_tiles_split_across_warps(mkv):
+    # tiny prefill blocks and long residuals: one unit's fp16 residual tiles are spread over
+    # several warps (residual partials + the arrival-counter merge), appends land in every tile
+    worst = run_decode(mkv, n_units=40, G=4, L=64, hh=8, rw=8, steps=100, check_every=9)
+    assert worst <= TOL
+
+
+def test_decode_attend_only_is_idempotent(mkv):
+    """k_new = None attends without appending: repeated calls give identical outputs."""
+    d, n, G = 128, 6, 4
+    rng = np.random.default_rng(5)
+    L = 500
+    k = torch.from_numpy(rng.standard_normal((n, L, d)).astype(np.float16)).cuda()
+    v = torch.from_numpy(rng.standard_normal((n, L, d)).astype(np.float16)).cuda()
+    a = torch.from_numpy(rng.random((n, L)).astype(np.float32)).cuda()
+    cache = mkv.KVCache(n, 200, max_decode_tokens=64)
+    cache.prefill(k, v, a, 100, 100)
+    for s in range(20):
+        tk = torch.from_numpy(rng.standard_normal((n, d)).astype(np.float16)).cuda()
+        cache.append(tk, tk)
+    q = torch.from_numpy(rng.standard_normal((n, G, d)).astype(np.float16)).cuda()
+    o1 = cache.decode_step(q, None, None, 0.09).clone()
+    o2 = cache.decode_step(q, None, None, 0.09)
+    assert torch.equal(o1, o2)
+    assert [cache.unit_info(u)["tokens_residual"] for u in range(n)] == [20] * n
+    rk, rv = cache.export_residual(0)
+    assert rk.shape == (20, d)
