@@ -426,10 +426,12 @@ static int get_plan(mkv_cache* c, int ub, int n, cudaStream_t s, Plan** out) {
     const int max_warps = num_sms() * wpc;
     std::vector<int32_t> buf(n + 1 + max_warps, 0);
     int32_t* pref = buf.data();
-    for (int i = 0; i < n; ++i) pref[i + 1] = pref[i] + c->n_pages[ub + i];
+    // each unit's pages padded to whole 4-page batches, warp ranges whole batches: every
+    // warp gets the same number of batches (a batch costs the same however full it is)
+    for (int i = 0; i < n; ++i) pref[i + 1] = pref[i] + ((c->n_pages[ub + i] + 3) & ~3);
     const int total = pref[n];
     const int min_chunk = 8;
-    const int chunk = std::max(min_chunk, (total + max_warps - 1) / std::max(max_warps, 1));
+    const int chunk = (std::max(min_chunk, (total + max_warps - 1) / std::max(max_warps, 1)) + 3) & ~3;
     const int warps = total > 0 ? (total + chunk - 1) / chunk : 0;
     int32_t* wstart = pref + n + 1;
     for (int w = 0, i = 0; w < warps; ++w) {  // first unit with pages that contains page w*chunk

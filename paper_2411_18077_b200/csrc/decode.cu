@@ -148,24 +148,26 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pages_kernel(const PagesParams
     // ---- producer cursor (warp-uniform) ----
     int pi = ci;
     int pg = start;
-    int p_uend = __ldg(P.pref + pi + 1);
+    int p_uend = __ldg(P.pref + pi + 1);  // units start at multiples of kBatch (padded prefix)
+    int p_rend = __ldg(P.pref + pi) + P.meta[P.unit_begin + pi].n_pages;  // end of its real pages
     // pool address of "global page 0" of unit pi (its first page minus its prefix)
     const uint8_t* p_base = P.pool + (P.meta[P.unit_begin + pi].page_base - __ldg(P.pref + pi)) * kPageBytes;
     auto issue = [&](int stage) {
         if (pg >= end) return;
-        const int n = min(min(kBatch, p_uend - pg), end - pg);
+        const int n = min(kBatch, p_rend - pg);  // batches never straddle units or warp ranges
         if (lane == 0) {
             mbar_expect_tx(&bars[stage], n * kPageBytes);
             bulk_g2s(ring + (size_t)stage * kBatch * kPageBytes, p_base + (size_t)pg * kPageBytes, n * kPageBytes,
                      &bars[stage]);
         }
-        pg += n;
+        pg += kBatch;
         if (pg == p_uend && pg < end) {
             while (pg == p_uend) {  // next unit that has pages
                 ++pi;
                 p_uend = __ldg(P.pref + pi + 1);
             }
             p_base = P.pool + (P.meta[P.unit_begin + pi].page_base - __ldg(P.pref + pi)) * kPageBytes;
+            p_rend = __ldg(P.pref + pi) + P.meta[P.unit_begin + pi].n_pages;
         }
     };
     // The first kStages batches are requested before griddepcontrol.wait: under PDL they
@@ -218,8 +220,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pages_kernel(const PagesParams
         for (int g = 0; g < 8; ++g) O[g][0] = O[g][1] = O[g][2] = O[g][3] = 0.0f;
         float Dvb[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 
+        const int uend_real = upre + meta.n_pages;
         while (cg < seg_end) {
-            const int n = min(min(kBatch, uend_g - cg), end - cg);
+            const int n = min(kBatch, uend_real - cg);
             const int pfirst = cg - upre;
             mbar_wait(&bars[stage], phase);
             const uint8_t* buf = ring + (size_t)stage * kBatch * kPageBytes;
@@ -331,7 +334,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pages_kernel(const PagesParams
             }
             __syncwarp();
             issue(stage);  // refill this stage with the batch kStages ahead
-            cg += n;
+            cg += kBatch;
             if (++stage == kStages) { stage = 0; phase ^= 1u; }
         }
         if (cg == uend_g) {
