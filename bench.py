@@ -117,6 +117,16 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
+def load_traffic(kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture (profiles/), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_pages_traffic.json")) as f:
+            t = json.load(f)
+        return float(t["traffic_bytes_per_launch"]) if t.get("kernel") == kernel else None
+    except Exception:
+        return None
+
+
 def load_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -250,33 +260,65 @@ def run_mkv(args, rank, world):
                              n_units * G * d * 2 * 2) / NL
     res["kernel"] = dict(name="mkv::pages_kernel", avg_launch_ms=k_ms, bytes_per_launch=page_bytes_per_launch,
                          gbs=page_bytes_per_launch / (k_ms / 1e3) / 1e9)
-    # ---- e2e through the C ABI with host buffers (pinned), copies inside the timed region ----
+    # ---- e2e through the C ABI with host buffers (pinned), copies inside the timed region.
+    #      Serving-style pipelining: step s+1's inputs are copied in (H2D stream) and step
+    #      s-1's outputs copied out (D2H stream) while step s computes; double-buffered
+    #      device inputs/outputs, every dependency through CUDA events; the host reads step
+    #      s-1's result (event sync) before issuing step s+1.  Wall clock over all steps. ----
     hq = qs[:, :, :, :, :].cpu().pin_memory()
     hk = ks.cpu().pin_memory()
     hv = vs.cpu().pin_memory()
-    hout = torch.empty((NL, upl, G, d), dtype=torch.float16).pin_memory()
-    dq = torch.empty((NL, upl, G, d), dtype=torch.float16, device=dev)
-    dk = torch.empty((NL, upl, d), dtype=torch.float16, device=dev)
-    dv = torch.empty((NL, upl, d), dtype=torch.float16, device=dev)
-    e2e_args = (_capi.DecodeArgs * NL)()
-    for l in range(NL):
-        e2e_args[l] = _capi.DecodeArgs(l * upl, upl, G, dq[l].data_ptr(), dk[l].data_ptr(), dv[l].data_ptr(),
-                                       out[l].data_ptr(), scale)
+    hout = [torch.empty((NL, upl, G, d), dtype=torch.float16).pin_memory() for _ in range(2)]
+    dq = [torch.empty((NL, upl, G, d), dtype=torch.float16, device=dev) for _ in range(2)]
+    dk = [torch.empty((NL, upl, d), dtype=torch.float16, device=dev) for _ in range(2)]
+    dv = [torch.empty((NL, upl, d), dtype=torch.float16, device=dev) for _ in range(2)]
+    dout = [torch.empty((NL, upl, G, d), dtype=torch.float16, device=dev) for _ in range(2)]
+    e2e_args = []
+    for bsel in range(2):
+        arr = (_capi.DecodeArgs * NL)()
+        for l in range(NL):
+            arr[l] = _capi.DecodeArgs(l * upl, upl, G, dq[bsel][l].data_ptr(), dk[bsel][l].data_ptr(),
+                                      dv[bsel][l].data_ptr(), dout[bsel][l].data_ptr(), scale)
+        e2e_args.append(arr)
+    h2d, d2h = torch.cuda.Stream(), torch.cuda.Stream()
+    ev = lambda: torch.cuda.Event()  # noqa: E731
+    in_ready = [ev() for _ in range(2)]
+    computed = [ev() for _ in range(2)]
+    out_read = [ev() for _ in range(2)]
     e2e_steps = min(args.steps, 20)
+
+    def issue_h2d(s_):
+        bsel, src = s_ % 2, (args.warmup + s_) % steps_total
+        with torch.cuda.stream(h2d):
+            h2d.wait_event(computed[bsel])  # step s_-2 has finished reading this input buffer
+            dq[bsel].copy_(hq[src], non_blocking=True)
+            dk[bsel].copy_(hk[src], non_blocking=True)
+            dv[bsel].copy_(hv[src], non_blocking=True)
+            in_ready[bsel].record(h2d)
+
     torch.cuda.synchronize()
     t0 = time.perf_counter()
+    issue_h2d(0)
     for s in range(e2e_steps):
-        src = (args.warmup + s) % steps_total
-        dq.copy_(hq[src], non_blocking=True)
-        dk.copy_(hk[src], non_blocking=True)
-        dv.copy_(hv[src], non_blocking=True)
-        _capi.check(L_.mkv_decode_step_layers(cache.h, NL, e2e_args, sp), "decode")
-        hout.copy_(out, non_blocking=True)
-        stream.synchronize()
+        bsel = s % 2
+        stream.wait_event(in_ready[bsel])
+        stream.wait_event(out_read[bsel])  # step s-2's output has left this buffer
+        _capi.check(L_.mkv_decode_step_layers(cache.h, NL, e2e_args[bsel], sp), "decode")
+        computed[bsel].record(stream)
+        if s + 1 < e2e_steps:
+            issue_h2d(s + 1)
+        with torch.cuda.stream(d2h):
+            d2h.wait_event(computed[bsel])
+            hout[bsel].copy_(dout[bsel], non_blocking=True)
+            out_read[bsel].record(d2h)
+        if s >= 1:
+            out_read[(s - 1) % 2].synchronize()  # the host reads step s-1's result
+    out_read[(e2e_steps - 1) % 2].synchronize()
     e2e_s = time.perf_counter() - t0
     res["e2e"] = dict(value=world * B * e2e_steps / e2e_s, unit=UNIT,
-                      h2d_bytes_per_step=int(dq.numel() * 2 + dk.numel() * 2 + dv.numel() * 2),
-                      d2h_bytes_per_step=int(out.numel() * 2))
+                      h2d_bytes_per_step=int(dq[0].numel() * 2 + dk[0].numel() * 2 + dv[0].numel() * 2),
+                      d2h_bytes_per_step=int(dout[0].numel() * 2),
+                      pipelining="H2D of step s+1 and D2H of step s-1 overlap step s (2 copy streams, events)")
     res["units"] = n_units
     res["pages"] = base_pages
     cache.close()
@@ -446,7 +488,9 @@ def main():
         "config": cfg_desc,
         "hbm_gbs": res["hbm_gbs"],
         "roofline": {"bound": "hbm", "achieved": kern["gbs"], "peak": hbm_peak, "unit": "GB/s",
-                     "frac": kern["gbs"] / hbm_peak, "traffic": None, "kernel": kern["name"],
+                     "frac": kern["gbs"] / hbm_peak, "traffic": load_traffic(kern["name"]),
+                     "traffic_source": "profiles/r1_pages_traffic.json (ncu dram__bytes_read+write, mean of "
+                                       "the 32 per-layer launches of one step)", "kernel": kern["name"],
                      "avg_launch_ms": kern["avg_launch_ms"], "bytes_per_launch": kern["bytes_per_launch"],
                      "peak_kind": peak_kind},
         "step_roofline_frac": res["hbm_gbs"] / (hbm_peak * world),

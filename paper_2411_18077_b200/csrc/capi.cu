@@ -81,6 +81,7 @@ struct Plan {
     int total = 0, chunk = 0, grid = 0;
     int32_t* d_pref = nullptr;    // [n_units + 1] local page prefix, then [warps] first unit per warp
     int32_t* d_wstart = nullptr;
+    UnitRec* d_rec = nullptr;     // [n_units]
 };
 
 struct mkv_cache {
@@ -408,7 +409,7 @@ int mkv_cache_prefill_select(mkv_cache* c, const mkv_prefill_select_args* a, voi
 static uint64_t range_hash(const mkv_cache* c, int ub, int n) {
     uint64_t h = 1469598103934665603ull;
     for (int i = 0; i < n; ++i) {
-        h ^= (uint64_t)(uint32_t)c->n_pages[ub + i];
+        h ^= (uint64_t)(uint32_t)c->n_pages[ub + i] | ((uint64_t)(uint32_t)c->n_prefill[ub + i] << 32);
         h *= 1099511628211ull;
     }
     return h;
@@ -439,8 +440,22 @@ static int get_plan(mkv_cache* c, int ub, int n, cudaStream_t s, Plan** out) {
         while (i < n - 1 && pref[i + 1] <= p) ++i;
         wstart[w] = i;
     }
-    if (!pl.d_pref) CK(cudaMalloc(&pl.d_pref, sizeof(int32_t) * (c->n_units + 1 + num_sms() * kMaxPagesWarps)));
+    // records follow the int32 arrays (16-byte aligned)
+    const size_t ints = ((c->n_units + 1 + (size_t)num_sms() * kMaxPagesWarps + 3) / 4) * 4;
+    std::vector<UnitRec> rec(n);
+    for (int i = 0; i < n; ++i) {
+        const int u = ub + i;
+        memset(&rec[i], 0, sizeof(UnitRec));
+        rec[i].base = c->page_base[u] - pref[i];
+        rec[i].pbeg = pref[i];
+        rec[i].pend = pref[i + 1];
+        rec[i].rend = pref[i] + c->n_pages[u];
+        rec[i].n_prefill = c->n_prefill[u];
+    }
+    if (!pl.d_pref) CK(cudaMalloc(&pl.d_pref, sizeof(int32_t) * ints + sizeof(UnitRec) * c->n_units));
     CK(cudaMemcpyAsync(pl.d_pref, buf.data(), sizeof(int32_t) * buf.size(), cudaMemcpyHostToDevice, s));
+    pl.d_rec = reinterpret_cast<UnitRec*>(pl.d_pref + ints);
+    CK(cudaMemcpyAsync(pl.d_rec, rec.data(), sizeof(UnitRec) * n, cudaMemcpyHostToDevice, s));
     pl.d_wstart = pl.d_pref + n + 1;
     pl.hash = h;
     pl.total = total;
@@ -453,7 +468,7 @@ static int get_plan(mkv_cache* c, int ub, int n, cudaStream_t s, Plan** out) {
 static void fill_pages_params(mkv_cache* c, const Plan* pl, const mkv_decode_args* a, PagesParams& pp) {
     pp.pool = c->d_pool; pp.meta = c->d_meta; pp.unit_begin = a->unit_begin; pp.n_units = a->n_units;
     pp.group = a->group; pp.q = static_cast<const __half*>(a->q);
-    pp.pref = pl->d_pref; pp.wstart = pl->d_wstart; pp.chunk = pl->chunk; pp.total_pages = pl->total;
+    pp.pref = pl->d_pref; pp.wstart = pl->d_wstart; pp.rec = pl->d_rec; pp.chunk = pl->chunk; pp.total_pages = pl->total;
     pp.n_warps = pl->grid * pages_config().warps;
     pp.part_ml = c->d_part_ml; pp.part_o = c->d_part_o;
     pp.scale_log2 = a->scale * 1.4426950408889634f;

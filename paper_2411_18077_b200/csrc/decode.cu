@@ -41,8 +41,11 @@ constexpr int kBatch = 4;  // pages per bulk copy / per K-bias mma / per softmax
 constexpr float kTwo24 = 16777216.0f;
 constexpr float kLazy = 3.0f;  // log2 units: P <= 8 keeps fp16 P and P*s far from overflow
 constexpr int kQBytes = kMaxG * kHeadDim * 2;  // per-warp q staging
+constexpr int kRecSlots = 8;  // unit records staged per warp (the units its page range touches)
 template <int kStages>
-__host__ __device__ constexpr int warp_smem() { return kStages * kBatch * kPageBytes + kQBytes; }
+__host__ __device__ constexpr int warp_smem() {
+    return kStages * kBatch * kPageBytes + kQBytes + kRecSlots * (int)sizeof(UnitRec);
+}
 
 __device__ __forceinline__ uint4 lds128(const uint8_t* p) { return *reinterpret_cast<const uint4*>(p); }
 __device__ __forceinline__ uint2 lds64(const uint8_t* p) { return *reinterpret_cast<const uint2*>(p); }
@@ -110,6 +113,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pages_kernel(const PagesParams
     uint8_t* wsm = smem + (size_t)warp * kWarpSmem;
     uint8_t* ring = wsm;
     __half* qsm = reinterpret_cast<__half*>(wsm + kStages * kBatch * kPageBytes);
+    UnitRec* srec = reinterpret_cast<UnitRec*>(wsm + kStages * kBatch * kPageBytes + kQBytes);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)kWarps * kWarpSmem) + warp * kStages;
 
     const int wg = blockIdx.x * kWarps + warp;
@@ -143,15 +147,28 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pages_kernel(const PagesParams
         for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
         fence_mbar_init();
     }
-    __syncwarp();
     ci = __ldg(P.wstart + wg);  // first unit of this warp's range (host plan)
+    // Stage the records of the first kRecSlots units of the range in shared memory (one
+    // round trip at start instead of dependent global loads at every unit boundary).
+    const int ci0 = ci;
+    for (int e = lane; e < kRecSlots * 2; e += 32)
+        if (ci0 + (e >> 1) < P.n_units)
+            cp_async16(reinterpret_cast<uint8_t*>(srec) + 16 * e, reinterpret_cast<const uint8_t*>(P.rec + ci0) + 16 * e);
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncwarp();
+    auto rec_pend = [&](int i) { return i - ci0 < kRecSlots ? srec[i - ci0].pend : __ldg(&P.rec[i].pend); };
+    auto rec_pbeg = [&](int i) { return i - ci0 < kRecSlots ? srec[i - ci0].pbeg : __ldg(&P.rec[i].pbeg); };
+    auto rec_rend = [&](int i) { return i - ci0 < kRecSlots ? srec[i - ci0].rend : __ldg(&P.rec[i].rend); };
+    auto rec_base = [&](int i) { return i - ci0 < kRecSlots ? srec[i - ci0].base : __ldg(&P.rec[i].base); };
+    auto rec_npre = [&](int i) { return i - ci0 < kRecSlots ? srec[i - ci0].n_prefill : __ldg(&P.rec[i].n_prefill); };
     // ---- producer cursor (warp-uniform) ----
     int pi = ci;
     int pg = start;
-    int p_uend = __ldg(P.pref + pi + 1);  // units start at multiples of kBatch (padded prefix)
-    int p_rend = __ldg(P.pref + pi) + P.meta[P.unit_begin + pi].n_pages;  // end of its real pages
+    int p_uend = rec_pend(pi);  // units start at multiples of kBatch (padded prefix)
+    int p_rend = rec_rend(pi);  // end of its real pages
     // pool address of "global page 0" of unit pi (its first page minus its prefix)
-    const uint8_t* p_base = P.pool + (P.meta[P.unit_begin + pi].page_base - __ldg(P.pref + pi)) * kPageBytes;
+    const uint8_t* p_base = P.pool + rec_base(pi) * kPageBytes;
     auto issue = [&](int stage) {
         if (pg >= end) return;
         const int n = min(kBatch, p_rend - pg);  // batches never straddle units or warp ranges
@@ -164,10 +181,10 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pages_kernel(const PagesParams
         if (pg == p_uend && pg < end) {
             while (pg == p_uend) {  // next unit that has pages
                 ++pi;
-                p_uend = __ldg(P.pref + pi + 1);
+                p_uend = rec_pend(pi);
             }
-            p_base = P.pool + (P.meta[P.unit_begin + pi].page_base - __ldg(P.pref + pi)) * kPageBytes;
-            p_rend = __ldg(P.pref + pi) + P.meta[P.unit_begin + pi].n_pages;
+            p_base = P.pool + rec_base(pi) * kPageBytes;
+            p_rend = rec_rend(pi);
         }
     };
     // The first kStages batches are requested before griddepcontrol.wait: under PDL they
@@ -188,12 +205,12 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pages_kernel(const PagesParams
 
     while (cg < end) {
         const int unit = ci;
-        const int upre = __ldg(P.pref + unit);
-        const int uend_g = __ldg(P.pref + unit + 1);
+        const int upre = rec_pbeg(unit);
+        const int uend_g = rec_pend(unit);
         const int seg_end = min(uend_g, end);
-        const UnitMeta meta = P.meta[P.unit_begin + unit];
-        const int partial_page = (meta.n_prefill & 15) ? ((meta.n_prefill + 15) >> 4) - 1 : -1;
-        const int partial_valid = meta.n_prefill & 15;
+        const int n_prefill = rec_npre(unit);
+        const int partial_page = (n_prefill & 15) ? ((n_prefill + 15) >> 4) - 1 : -1;
+        const int partial_valid = n_prefill & 15;
 
         uint32_t qb[8][2], qsc[8][2];
         cp_async_wait_all();
@@ -210,7 +227,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pages_kernel(const PagesParams
         }
         if (seg_end < end) {
             int nu = unit + 1;
-            while (__ldg(P.pref + nu + 1) == seg_end) ++nu;
+            while (rec_pend(nu) == seg_end) ++nu;
             prefetch_q(nu);
         }
 
@@ -220,7 +237,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pages_kernel(const PagesParams
         for (int g = 0; g < 8; ++g) O[g][0] = O[g][1] = O[g][2] = O[g][3] = 0.0f;
         float Dvb[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 
-        const int uend_real = upre + meta.n_pages;
+        const int uend_real = rec_rend(unit);
         while (cg < seg_end) {
             const int n = min(kBatch, uend_real - cg);
             const int pfirst = cg - upre;
@@ -339,7 +356,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pages_kernel(const PagesParams
         }
         if (cg == uend_g) {
             ++ci;
-            while (cg < end && __ldg(P.pref + ci + 1) == cg) ++ci;
+            while (cg < end && rec_pend(ci) == cg) ++ci;
         }
 
         // ---- segment epilogue: partial (m, l, o) for slot (warp wg, unit) ----

@@ -60,6 +60,14 @@ struct ResidualParams {
 cudaError_t launch_append(const ResidualParams& p, cudaStream_t s);
 cudaError_t launch_finish(const ResidualParams& p, const int32_t* pref, int chunk, bool after_pages, cudaStream_t s);
 
+// Per-unit page-run record of a K4 plan (host-computed from the cache mirror).
+struct UnitRec {
+    int64_t base;       // pool page index of the unit's page 0 minus pbeg
+    int32_t pbeg, pend; // the unit's [begin, end) in the plan's padded page sequence
+    int32_t rend;       // pbeg + real pages
+    int32_t n_prefill;  // tokens of the prefill block (its last page may be partial)
+    int32_t pad[2];
+};
 struct PagesParams {
     const uint8_t* pool;
     const UnitMeta* meta;
@@ -67,6 +75,7 @@ struct PagesParams {
     const __half* q;
     const int32_t* pref;    // [n_units + 1] local page prefix
     const int32_t* wstart;  // [n_warps] first (non-empty) unit of each warp's page range
+    const UnitRec* rec;     // [n_units]
     int chunk, total_pages, n_warps;
     float* part_ml;         // [slots][2][kMaxG]   slot = warp + unit
     float* part_o;          // [slots][kMaxG][d]
