@@ -206,12 +206,18 @@ int mkv_prefill_attn(const mkv_prefill_args* a, void* stream) {
 // ---------------------------------------------------------------------------
 static int do_select(const float* a_cumul, int64_t a_stride, int n_units, int length, const int32_t* hh_host,
                      int rw, int32_t* kept, int64_t kept_stride, int32_t* n_kept, cudaStream_t s) {
+    // one budget for every unit (the common case) travels as a kernel argument: no
+    // host->device copy (a pageable copy would serialise the host with the stream)
+    bool uniform = true;
+    for (int i = 1; i < n_units; ++i) uniform &= hh_host[i] == hh_host[0];
     int32_t* d_hh = nullptr;
-    CK(cudaMallocAsync(&d_hh, sizeof(int32_t) * n_units, s));
-    CK(cudaMemcpyAsync(d_hh, hh_host, sizeof(int32_t) * n_units, cudaMemcpyHostToDevice, s));
-    SelectParams p{a_cumul, a_stride, n_units, length, d_hh, rw, kept, kept_stride, n_kept};
+    if (!uniform) {
+        CK(cudaMallocAsync(&d_hh, sizeof(int32_t) * n_units, s));
+        CK(cudaMemcpyAsync(d_hh, hh_host, sizeof(int32_t) * n_units, cudaMemcpyHostToDevice, s));
+    }
+    SelectParams p{a_cumul, a_stride, n_units, length, d_hh, uniform ? hh_host[0] : 0, rw, kept, kept_stride, n_kept};
     cudaError_t e = launch_select(p, s);
-    cudaFreeAsync(d_hh, s);
+    if (d_hh) cudaFreeAsync(d_hh, s);
     if (e != cudaSuccess) return cuda_fail(e, "select kernel");
     return MKV_OK;
 }

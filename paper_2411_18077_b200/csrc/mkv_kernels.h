@@ -32,7 +32,8 @@ struct SelectParams {
     const float* a;
     int64_t a_stride;
     int n_units, length;
-    const int32_t* hh;  // device [n_units]
+    const int32_t* hh;  // device [n_units], or null: every unit keeps hh_uniform
+    int hh_uniform;
     int rw;
     int32_t* kept;
     int64_t kept_stride;

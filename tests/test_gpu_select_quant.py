@@ -189,3 +189,27 @@ def test_quantizer_rounding_edges_bit_exact(mkv, kind):
         w_ref, p_ref, br_ref = oc.export(which)
         np.testing.assert_array_equal(w, w_ref)
         np.testing.assert_array_equal(p, p_ref)
+
+
+@pytest.mark.parametrize("cluster", ["0", "2", "8", "16"])
+@pytest.mark.parametrize("L,hh,rw,kind", [
+    (131072, 13107, 13107, "ties"), (131072, 65536, 0, "uniform"), (65536, 100, 3000, "allequal"),
+    (40000, 19999, 1, "ties"),
+])
+def test_select_cluster_path_matches_oracle(mkv, monkeypatch, cluster, L, hh, rw, kind):
+    """Few long units (configs[3]: 8 x 128K) take the thread-block-cluster radix select;
+    every cluster size gives the single-CTA kernel's (= the reference's) indices."""
+    monkeypatch.setenv("MKV_SELECT_CLUSTER", cluster)
+    rng = np.random.default_rng(L + hh + int(cluster))
+    n = 3
+    if kind == "uniform":
+        a = rng.random((n, L)).astype(np.float32)
+    elif kind == "ties":
+        a = _ties(rng, n * L, 5).reshape(n, L)
+    else:
+        a = np.ones((n, L), np.float32)
+    a[:, rng.integers(0, L, L // 50)] = -0.0
+    kept, nks = mkv.select_token_counts(torch.from_numpy(a).cuda(), hh, rw)
+    kept = kept.cpu().numpy()
+    for u in range(n):
+        np.testing.assert_array_equal(kept[u, :nks[u]], oracle_select(a[u], hh, rw))
