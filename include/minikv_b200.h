@@ -94,6 +94,18 @@ int mkv_select(const mkv_select_args* args, void* stream);
 int mkv_allocate_pyramid(size_t mean_budget_x, size_t layers, size_t depth, int bottom_heavy,
                          int64_t* per_layer_hh);
 int mkv_allocate_uniform(size_t total_hh, size_t layers, int64_t* per_layer_hh);
+/* replaces: LayerAllocation allocate_variance(per_layer_variance, total_hh, mode)      */
+/*           selection.hpp:52-56, selection.cpp:85-128 (host arithmetic, bit-exact);    */
+/* inverse = 0: VarianceMode::Prop, 1: VarianceMode::Inv; *uniform_fallback as the     */
+/* reference's LayerAllocation::uniform_fallback.                                       */
+int mkv_allocate_variance(const float* per_layer_variance, size_t layers, size_t total_hh,
+                          int inverse, int64_t* per_layer_hh, int* uniform_fallback);
+/* replaces: float layer_score_variance(a_cumul)  selection.hpp:58-59,                */
+/*           selection.cpp:130-146 -- on the device, for n_units rows of A_cumul at    */
+/* once (fp32 [n_units, length], row stride a_stride): population variance with two   */
+/* fp64 passes per row -> out fp32 [n_units] (device), stream-ordered.                 */
+int mkv_score_variance(const float* a_cumul, int64_t a_stride, int n_units, int length, float* out,
+                       void* stream);
 
 /* ------------------------------------------------------------------------ */
 /* Device KV cache: one handle owns n_units (seq, layer, kv-head) caches.    */

@@ -97,6 +97,10 @@ class _Lib:
         ap.argtypes = [_sz, _sz, _sz, C.c_int, _i64p]
         au = getattr(L, p + "allocate_uniform")
         au.argtypes = [_sz, _sz, _i64p]
+        av = getattr(L, p + "allocate_variance")
+        av.argtypes = [_f32p, _sz, _sz, C.c_int, _i64p, C.POINTER(C.c_int)]
+        lv = getattr(L, p + "layer_score_variance")
+        lv.argtypes = [_f32p, _sz, C.POINTER(C.c_float)]
 
     def fn(self, name):
         return getattr(self.lib, self.prefix + name)
@@ -164,6 +168,21 @@ class _Lib:
         _check(self.fn("allocate_pyramid")(x, layers, depth, int(bottom_heavy), out),
                "allocate_pyramid")
         return out[:layers]
+
+    # selection.cpp:85-128 (inverse: VarianceMode::Inv)
+    def allocate_variance(self, variances, total, inverse=False):
+        v = _f32(np.asarray(variances, np.float32))
+        out = np.zeros(max(len(v), 1), np.int64)
+        fb = C.c_int(0)
+        _check(self.fn("allocate_variance")(v, len(v), total, int(inverse), out, C.byref(fb)), "allocate_variance")
+        return out[:len(v)], bool(fb.value)
+
+    # selection.cpp:130-146
+    def layer_score_variance(self, a):
+        a = _f32(np.asarray(a, np.float32))
+        r = C.c_float(0)
+        _check(self.fn("layer_score_variance")(a, len(a), C.byref(r)), "layer_score_variance")
+        return r.value
 
     # selection.cpp:48-59
     def allocate_uniform(self, total, layers):

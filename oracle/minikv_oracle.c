@@ -424,6 +424,69 @@ int mko_allocate_pyramid(size_t mean_x, size_t layers, size_t depth, int bottom_
     return MKO_OK;
 }
 
+/* selection.cpp:85-128 */
+typedef struct {
+    double frac;
+    size_t idx;
+} mko_frac;
+
+int mko_allocate_variance(const float* variance, size_t layers, size_t total_hh, int inverse,
+                          int64_t* out, int* uniform_fallback) {
+    if (layers < 1) return MKO_INVALID;
+    const double eps = 1e-6;
+    double* shares = (double*)malloc(layers * sizeof(double));
+    mko_frac* fr = (mko_frac*)malloc(layers * sizeof(mko_frac));
+    if (!shares || !fr) { free(shares); free(fr); return MKO_RUNTIME; }
+    double sum = 0.0;
+    int all_zero = 1;
+    for (size_t i = 0; i < layers; ++i) {
+        if (variance[i] < 0) { free(shares); free(fr); return MKO_INVALID; }
+        if (variance[i] > 0) all_zero = 0;
+        shares[i] = inverse ? 1.0 / ((double)variance[i] + eps) : (double)variance[i];
+        sum += shares[i];
+    }
+    *uniform_fallback = 0;
+    if (all_zero && !inverse) {
+        free(shares); free(fr);
+        *uniform_fallback = 1;
+        return mko_allocate_uniform(total_hh, layers, out);
+    }
+    size_t assigned = 0;
+    for (size_t i = 0; i < layers; ++i) {
+        const double target = (double)total_hh * shares[i] / sum;
+        out[i] = (int64_t)floor(target);
+        assigned += (size_t)out[i];
+        fr[i].frac = target - floor(target);
+        fr[i].idx = i;
+    }
+    /* stable sort by fraction, descending (insertion sort keeps equal fractions in index order) */
+    for (size_t i = 1; i < layers; ++i) {
+        mko_frac x = fr[i];
+        size_t j = i;
+        while (j > 0 && fr[j - 1].frac < x.frac) { fr[j] = fr[j - 1]; --j; }
+        fr[j] = x;
+    }
+    for (size_t r = 0; assigned < total_hh; ++r, ++assigned) ++out[fr[r % layers].idx];
+    free(shares);
+    free(fr);
+    return MKO_OK;
+}
+
+/* selection.cpp:130-146 */
+int mko_layer_score_variance(const float* a, size_t n, float* out) {
+    if (n == 0) return MKO_INVALID;
+    double mean = 0.0;
+    for (size_t i = 0; i < n; ++i) mean += a[i];
+    mean /= (double)n;
+    double var = 0.0;
+    for (size_t i = 0; i < n; ++i) {
+        const double d = a[i] - mean;
+        var += d * d;
+    }
+    *out = (float)(var / (double)n);
+    return MKO_OK;
+}
+
 /* ------------------------------------------------------------------ */
 /* cache engine (cache_engine.cpp)                                    */
 /* ------------------------------------------------------------------ */

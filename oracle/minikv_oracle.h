@@ -73,6 +73,12 @@ int mko_select_token_counts(const float* a_cumul, size_t l, size_t hh_count, siz
 int mko_select_tokens(const float* a_cumul, size_t l, double alpha_hh, double alpha_rw,
                       int64_t* kept, size_t* n_kept, int* clamped);               /* :35-46 */
 int mko_allocate_uniform(size_t total_hh, size_t layers, int64_t* out);            /* :48-59 */
+/* selection.cpp:85-128: shares var (Prop) or 1/(var + 1e-6) (Inv) in double, all-zero Prop
+ * falls back to uniform (flag), largest-remainder rounding, remainder ties to the lower layer. */
+int mko_allocate_variance(const float* variance, size_t layers, size_t total_hh, int inverse,
+                          int64_t* out, int* uniform_fallback);
+/* selection.cpp:130-146: population variance, two double passes in index order. */
+int mko_layer_score_variance(const float* a_cumul, size_t n, float* out);
 int mko_allocate_pyramid(size_t mean_x, size_t layers, size_t depth, int bottom_heavy,
                          int64_t* out);                                            /* :61-83 */
 

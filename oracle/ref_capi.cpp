@@ -165,6 +165,22 @@ int mkr_allocate_uniform(size_t total, size_t layers, int64_t* out) {
     })
 }
 
+// selection.cpp:85-128
+int mkr_allocate_variance(const float* variance, size_t layers, size_t total, int inverse, int64_t* out,
+                          int* uniform_fallback) {
+    GUARD({
+        LayerAllocation a = allocate_variance(Vector(variance, variance + layers), total,
+                                              inverse ? VarianceMode::Inv : VarianceMode::Prop);
+        for (std::size_t i = 0; i < layers; ++i) out[i] = static_cast<int64_t>(a.per_layer_hh[i]);
+        *uniform_fallback = a.uniform_fallback ? 1 : 0;
+    })
+}
+
+// selection.cpp:130-146
+int mkr_layer_score_variance(const float* a, size_t n, float* out) {
+    GUARD({ *out = layer_score_variance(Vector(a, a + n)); })
+}
+
 // ---- cache engine: an opaque KVCacheLayer handle ----
 
 struct mkr_cache {

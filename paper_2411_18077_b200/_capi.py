@@ -106,6 +106,7 @@ class DecodeArgs(C.Structure):
 EXPORTS = [
     "mkv_last_error", "mkv_abi_version", "mkv_device_check",
     "mkv_prefill_attn", "mkv_select", "mkv_allocate_pyramid", "mkv_allocate_uniform",
+    "mkv_allocate_variance", "mkv_score_variance",
     "mkv_cache_create", "mkv_cache_destroy", "mkv_cache_bytes", "mkv_cache_unit_info",
     "mkv_cache_prefill", "mkv_cache_prefill_select", "mkv_decode_step", "mkv_cache_append",
     "mkv_decode_step_layers", "mkv_debug_decode_trace", "mkv_decode_pages_only", "mkv_cache_export_sizes", "mkv_cache_export_reference",
@@ -130,6 +131,8 @@ def lib():
     L.mkv_select.argtypes = [C.POINTER(SelectArgs), vp]
     L.mkv_allocate_pyramid.argtypes = [C.c_size_t, C.c_size_t, C.c_size_t, i32, C.POINTER(C.c_int64)]
     L.mkv_allocate_uniform.argtypes = [C.c_size_t, C.c_size_t, C.POINTER(C.c_int64)]
+    L.mkv_allocate_variance.argtypes = [vp, C.c_size_t, C.c_size_t, i32, C.POINTER(C.c_int64), C.POINTER(C.c_int)]
+    L.mkv_score_variance.argtypes = [vp, i64, i32, i32, vp, vp]
     L.mkv_cache_create.argtypes = [C.POINTER(CacheConfig), C.POINTER(vp)]
     L.mkv_cache_destroy.argtypes = [vp]
     L.mkv_cache_bytes.argtypes = [vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]

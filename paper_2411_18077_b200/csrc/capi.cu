@@ -6,6 +6,7 @@
 // ABI; no CPU fallback exists -- on a non-sm_100 device every compute call
 // fails with MKV_ERR_UNSUPPORTED.
 #include <algorithm>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -170,6 +171,49 @@ int mkv_allocate_pyramid(size_t mean_x, size_t layers, size_t depth, int bottom_
     return MKV_OK;
 }
 
+int mkv_allocate_variance(const float* var, size_t layers, size_t total_hh, int inverse, int64_t* out,
+                          int* uniform_fallback) {
+    if (layers < 1) return fail(MKV_ERR_INVALID_ARGUMENT, "allocate_variance: no layers");
+    if (!var || !out || !uniform_fallback) return fail(MKV_ERR_INVALID_ARGUMENT, "allocate_variance: null argument");
+    constexpr double kEps = 1e-6;
+    std::vector<double> shares(layers);
+    double sum = 0.0;
+    bool all_zero = true;
+    for (size_t i = 0; i < layers; ++i) {
+        if (var[i] < 0) return fail(MKV_ERR_INVALID_ARGUMENT, "allocate_variance: negative variance");
+        if (var[i] > 0) all_zero = false;
+        shares[i] = inverse ? 1.0 / (static_cast<double>(var[i]) + kEps) : static_cast<double>(var[i]);
+        sum += shares[i];
+    }
+    *uniform_fallback = 0;
+    if (all_zero && !inverse) {  // degenerate Prop: uniform allocation, flagged
+        *uniform_fallback = 1;
+        return mkv_allocate_uniform(total_hh, layers, out);
+    }
+    // largest-remainder rounding; remainder ties go to the lower layer
+    std::vector<std::pair<double, size_t>> fracs(layers);
+    size_t assigned = 0;
+    for (size_t i = 0; i < layers; ++i) {
+        const double target = static_cast<double>(total_hh) * shares[i] / sum;
+        out[i] = static_cast<int64_t>(std::floor(target));
+        assigned += static_cast<size_t>(out[i]);
+        fracs[i] = {target - std::floor(target), i};
+    }
+    std::stable_sort(fracs.begin(), fracs.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
+    for (size_t r = 0; assigned < total_hh; ++r, ++assigned) ++out[fracs[r % layers].second];
+    return MKV_OK;
+}
+
+int mkv_score_variance(const float* a_cumul, int64_t a_stride, int n_units, int length, float* out, void* stream) {
+    if (n_units < 0 || length < 0) return fail(MKV_ERR_INVALID_ARGUMENT, "layer_score_variance: bad shape");
+    if (n_units == 0) return MKV_OK;
+    if (length == 0) return fail(MKV_ERR_INVALID_ARGUMENT, "layer_score_variance: empty input");
+    if (!a_cumul || !out || a_stride < length) return fail(MKV_ERR_INVALID_ARGUMENT, "layer_score_variance: bad tensor");
+    if (int r = require_device()) return r;
+    CK(launch_score_variance(a_cumul, a_stride, n_units, length, out, static_cast<cudaStream_t>(stream)));
+    return MKV_OK;
+}
+
 // ---------------------------------------------------------------------------
 // K1 prefill attention
 // ---------------------------------------------------------------------------
@@ -322,7 +366,7 @@ int mkv_cache_bytes(const mkv_cache* c, uint64_t* page_bytes, uint64_t* residual
 int mkv_cache_unit_info(const mkv_cache* c, int u, int64_t* tq, int64_t* tr, int64_t* np, int64_t* nb) {
     if (!c) return fail(MKV_ERR_INVALID_ARGUMENT, "cache: null handle");
     if (u < 0 || u >= c->n_units) return fail(MKV_ERR_OUT_OF_RANGE, "cache: unit %d out of range", u);
-    if (tq) *tq = c->n_prefill[u] + (int64_t)(c->n_blocks[u] > 0 ? c->n_blocks[u] - 1 : 0) * c->n_r;
+    if (tq) *tq = c->n_prefill[u] + (int64_t)(c->n_blocks[u] - (c->n_prefill[u] > 0 ? 1 : 0)) * c->n_r;
     if (tr) *tr = c->n_res[u];
     if (np) *np = c->n_pages[u];
     if (nb) *nb = c->n_blocks[u];
@@ -596,8 +640,10 @@ int mkv_cache_append(mkv_cache* c, int ub, int n, const void* k_new, const void*
 static void block_list(const mkv_cache* c, int u, std::vector<int>& rows) {
     rows.clear();
     if (c->n_blocks[u] == 0) return;
-    rows.push_back(c->n_prefill[u]);
-    for (int b = 1; b < c->n_blocks[u]; ++b) rows.push_back(c->n_r);
+    // a prefill block (n_prefill > 0 rows; prefill never keeps zero) then n_r-row flush blocks
+    const int pre = c->n_prefill[u] > 0 ? 1 : 0;
+    if (pre) rows.push_back(c->n_prefill[u]);
+    for (int b = pre; b < c->n_blocks[u]; ++b) rows.push_back(c->n_r);
 }
 
 int mkv_cache_export_sizes(const mkv_cache* c, int u, int which, int64_t* n_words, int64_t* n_params,

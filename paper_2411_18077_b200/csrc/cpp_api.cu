@@ -1,0 +1,395 @@
+// cpp_api.cu -- the C++ host API (include/minikv_b200.hpp) over the C ABI.
+//
+// Host code only: uploads the reference-shaped host values (fp32 rounded once to
+// fp16, the device format), calls the C ABI on the default stream, synchronises and
+// returns reference-shaped results.  Status codes become the reference's exception
+// classes: invalid_argument, domain_error, runtime_error, out_of_range.
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <stdexcept>
+#include <string>
+
+#include "minikv_b200.h"
+#include "minikv_b200.hpp"
+
+namespace minikv_b200 {
+
+namespace {
+
+void throw_status(int st, const char* where) {
+    if (st == MKV_OK) return;
+    const std::string m = std::string(where) + ": " + mkv_last_error();
+    switch (st) {
+        case MKV_ERR_INVALID_ARGUMENT: throw std::invalid_argument(m);
+        case MKV_ERR_DOMAIN: throw std::domain_error(m);
+        case MKV_ERR_OUT_OF_RANGE: throw std::out_of_range(m);
+        default: throw std::runtime_error(m);  // RUNTIME, CUDA, UNSUPPORTED
+    }
+}
+
+void cuda_check(cudaError_t e, const char* where) {
+    if (e != cudaSuccess) throw std::runtime_error(std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+// RAII device buffer
+struct Dev {
+    void* p = nullptr;
+    explicit Dev(size_t bytes) { cuda_check(cudaMalloc(&p, std::max<size_t>(bytes, 16)), "cudaMalloc"); }
+    ~Dev() { cudaFree(p); }
+    Dev(const Dev&) = delete;
+    Dev& operator=(const Dev&) = delete;
+    Dev(Dev&& o) noexcept : p(o.p) { o.p = nullptr; }
+    template <typename T>
+    T* as() const { return static_cast<T*>(p); }
+};
+
+std::vector<__half> to_half(const float* x, size_t n) {
+    std::vector<__half> h(n);
+    for (size_t i = 0; i < n; ++i) h[i] = __float2half_rn(x[i]);
+    return h;
+}
+
+Dev upload_half(const float* x, size_t n) {
+    Dev d(n * sizeof(__half));
+    const std::vector<__half> h = to_half(x, n);
+    cuda_check(cudaMemcpy(d.p, h.data(), n * sizeof(__half), cudaMemcpyHostToDevice), "upload");
+    return d;
+}
+
+Dev upload_f32(const float* x, size_t n) {
+    Dev d(n * sizeof(float));
+    cuda_check(cudaMemcpy(d.p, x, n * sizeof(float), cudaMemcpyHostToDevice), "upload");
+    return d;
+}
+
+std::vector<float> download_half(const Dev& d, size_t n) {
+    std::vector<__half> h(n);
+    cuda_check(cudaMemcpy(h.data(), d.p, n * sizeof(__half), cudaMemcpyDeviceToHost), "download");
+    std::vector<float> out(n);
+    for (size_t i = 0; i < n; ++i) out[i] = __half2float(h[i]);
+    return out;
+}
+
+constexpr int kD = 128;  // the device head dimension
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// attention (attention.cpp:29-117)
+// ---------------------------------------------------------------------------
+AttentionResult selective_flash_attn(const Matrix& q, const Matrix& k, const Matrix& v, float scale, bool causal,
+                                     TileConfig) {
+    if (q.cols != k.cols) throw std::invalid_argument("selective_flash_attn: q/k width mismatch");
+    if (k.rows != v.rows) throw std::invalid_argument("selective_flash_attn: k/v length mismatch");
+    if (q.rows == 0 || k.rows == 0) throw std::invalid_argument("selective_flash_attn: empty input");
+    if (causal && q.rows > k.rows) throw std::invalid_argument("selective_flash_attn: causal requires l_query <= l_key");
+    if (q.cols != kD || v.cols != kD) throw std::invalid_argument("selective_flash_attn: the device kernel is d = 128");
+    const size_t lq = q.rows, lk = k.rows;
+    Dev dq = upload_half(q.data.data(), lq * kD), dk = upload_half(k.data.data(), lk * kD),
+        dv = upload_half(v.data.data(), lk * kD);
+    Dev dout(lq * kD * sizeof(__half)), dlse(lq * sizeof(float)), dacc(lk * sizeof(float));
+    mkv_prefill_args a{};
+    a.q = dq.p; a.q_st = kD; a.q_sh = (int64_t)lq * kD; a.q_sb = a.q_sh;
+    a.k = dk.p; a.k_st = kD; a.k_sh = (int64_t)lk * kD; a.k_sb = a.k_sh;
+    a.v = dv.p; a.v_st = kD; a.v_sh = (int64_t)lk * kD; a.v_sb = a.v_sh;
+    a.out = dout.p; a.o_st = kD; a.o_sh = (int64_t)lq * kD; a.o_sb = a.o_sh;
+    a.lse = dlse.as<float>(); a.a_cumul = dacc.as<float>();
+    a.batch = 1; a.n_q_heads = 1; a.n_kv_heads = 1;
+    a.len_q = (int)lq; a.len_k = (int)lk; a.head_dim = kD;
+    a.scale = scale; a.causal = causal ? 1 : 0;
+    throw_status(mkv_prefill_attn(&a, nullptr), "selective_flash_attn");
+    AttentionResult r;
+    r.output = Matrix(lq, kD);
+    r.output.data = download_half(dout, lq * kD);
+    r.lse.resize(lq);
+    r.a_cumul.resize(lk);
+    cuda_check(cudaMemcpy(r.lse.data(), dlse.p, lq * sizeof(float), cudaMemcpyDeviceToHost), "download");
+    cuda_check(cudaMemcpy(r.a_cumul.data(), dacc.p, lk * sizeof(float), cudaMemcpyDeviceToHost), "download");
+    r.aux_elements = lq + lk;  // LSE + A_cumul: linear in the sequence (attention.hpp:21-23)
+    return r;
+}
+
+// ---------------------------------------------------------------------------
+// selection (selection.cpp)
+// ---------------------------------------------------------------------------
+SelectionResult select_token_counts(const Vector& a_cumul, size_t hh_count, size_t rw_count) {
+    const size_t l = a_cumul.size();
+    SelectionResult res;
+    if (hh_count + rw_count >= l) {  // keep everything (selection.cpp:14-18)
+        res.clamped = hh_count + rw_count > l;
+        rw_count = std::min(rw_count, l);
+        hh_count = l - rw_count;
+    }
+    for (size_t i = l - rw_count; i < l; ++i) res.rw.push_back(i);
+    if (l == 0) return res;
+    if (l > (size_t)INT32_MAX || hh_count > (size_t)INT32_MAX) throw std::invalid_argument("select: length too large");
+    Dev da = upload_f32(a_cumul.data(), l);
+    Dev dk(l * sizeof(int32_t));
+    const int32_t hh = (int32_t)hh_count;
+    mkv_select_args s{};
+    s.a_cumul = da.as<float>(); s.a_stride = (int64_t)l; s.n_units = 1; s.length = (int)l;
+    s.hh_count = &hh; s.rw_count = (int)rw_count; s.kept = dk.as<int32_t>(); s.kept_stride = (int64_t)l;
+    throw_status(mkv_select(&s, nullptr), "select_token_counts");
+    const size_t n_kept = std::min(hh_count + rw_count, l);
+    std::vector<int32_t> kept(n_kept);
+    cuda_check(cudaMemcpy(kept.data(), dk.p, n_kept * sizeof(int32_t), cudaMemcpyDeviceToHost), "download");
+    res.kept.assign(kept.begin(), kept.end());
+    res.hh.assign(res.kept.begin(), res.kept.begin() + (n_kept - rw_count));
+    return res;
+}
+
+SelectionResult select_tokens(const Vector& a_cumul, const CacheBudget& budget, size_t l_prompt) {
+    if (a_cumul.size() != l_prompt) throw std::invalid_argument("select_tokens: a_cumul length != l_prompt");
+    if (budget.alpha_hh < 0 || budget.alpha_rw < 0) throw std::invalid_argument("select_tokens: negative budget");
+    const auto hh = static_cast<size_t>(std::floor(budget.alpha_hh * static_cast<double>(l_prompt)));
+    const auto rw = static_cast<size_t>(std::floor(budget.alpha_rw * static_cast<double>(l_prompt)));
+    return select_token_counts(a_cumul, hh, rw);
+}
+
+static LayerAllocation from_i64(const std::vector<int64_t>& v, bool fallback) {
+    LayerAllocation a;
+    a.per_layer_hh.assign(v.begin(), v.end());
+    a.uniform_fallback = fallback;
+    return a;
+}
+
+LayerAllocation allocate_uniform(size_t total_hh, size_t layers) {
+    if (layers < 1) throw std::invalid_argument("allocate_uniform: layers must be >= 1");
+    std::vector<int64_t> out(layers);
+    throw_status(mkv_allocate_uniform(total_hh, layers, out.data()), "allocate_uniform");
+    return from_i64(out, false);
+}
+
+LayerAllocation allocate_pyramid(size_t x, size_t layers, size_t depth, PyramidOrientation o) {
+    if (layers < 1) throw std::invalid_argument("allocate_pyramid: layers must be >= 1");
+    std::vector<int64_t> out(layers);
+    throw_status(mkv_allocate_pyramid(x, layers, depth, o == PyramidOrientation::BottomHeavy ? 1 : 0, out.data()),
+                 "allocate_pyramid");
+    return from_i64(out, false);
+}
+
+LayerAllocation allocate_variance(const Vector& var, size_t total_hh, VarianceMode mode) {
+    std::vector<int64_t> out(std::max<size_t>(var.size(), 1));
+    int fb = 0;
+    throw_status(mkv_allocate_variance(var.data(), var.size(), total_hh, mode == VarianceMode::Inv ? 1 : 0,
+                                       out.data(), &fb),
+                 "allocate_variance");
+    out.resize(var.size());
+    return from_i64(out, fb != 0);
+}
+
+float layer_score_variance(const Vector& a_cumul) {
+    if (a_cumul.empty()) throw std::invalid_argument("layer_score_variance: empty input");
+    Dev da = upload_f32(a_cumul.data(), a_cumul.size());
+    Dev dout(sizeof(float));
+    throw_status(mkv_score_variance(da.as<float>(), (int64_t)a_cumul.size(), 1, (int)a_cumul.size(),
+                                    dout.as<float>(), nullptr),
+                 "layer_score_variance");
+    float r = 0.0f;
+    cuda_check(cudaMemcpy(&r, dout.p, sizeof(float), cudaMemcpyDeviceToHost), "download");
+    return r;
+}
+
+// ---------------------------------------------------------------------------
+// quantized stream (quantizer.cpp:153-195)
+// ---------------------------------------------------------------------------
+Matrix dequantize_matrix(const QuantizedTensor& t) {
+    Matrix m(t.logical_rows, t.logical_cols);
+    size_t code = 0, group = 0, row0 = 0;
+    auto code_at = [&](size_t i) -> uint32_t { return (t.packed_words[i / 16] >> (2 * (i % 16))) & 3u; };
+    for (size_t R : t.block_rows) {
+        if (t.axis == GroupAxis::PerChannel) {
+            for (size_t c = 0; c < t.logical_cols; ++c)
+                for (size_t g0 = 0; g0 < R; g0 += t.group_size) {
+                    const GroupQuantParams p = t.params.at(group++);
+                    for (size_t r = g0; r < std::min(R, g0 + t.group_size); ++r) {
+                        const float prod = static_cast<float>(code_at(code++)) * p.scale;
+                        m.at(row0 + r, c) = prod + p.zero_point;
+                    }
+                }
+        } else {
+            for (size_t r = 0; r < R; ++r)
+                for (size_t c0 = 0; c0 < t.logical_cols; c0 += t.group_size) {
+                    const GroupQuantParams p = t.params.at(group++);
+                    for (size_t c = c0; c < std::min(t.logical_cols, c0 + t.group_size); ++c) {
+                        const float prod = static_cast<float>(code_at(code++)) * p.scale;
+                        m.at(row0 + r, c) = prod + p.zero_point;
+                    }
+                }
+        }
+        row0 += R;
+    }
+    return m;
+}
+
+// ---------------------------------------------------------------------------
+// device KV cache (cache_engine.cpp)
+// ---------------------------------------------------------------------------
+struct KVCacheLayer::Impl {
+    mkv_cache* h = nullptr;
+    ~Impl() {
+        if (h) mkv_cache_destroy(h);
+    }
+};
+
+KVCacheLayer::KVCacheLayer() = default;
+KVCacheLayer::~KVCacheLayer() = default;
+KVCacheLayer::KVCacheLayer(KVCacheLayer&&) noexcept = default;
+KVCacheLayer& KVCacheLayer::operator=(KVCacheLayer&&) noexcept = default;
+
+static mkv_cache* handle(const KVCacheLayer& c) {
+    if (!c.impl || !c.impl->h) throw std::runtime_error("KVCacheLayer: no device cache");
+    return c.impl->h;
+}
+
+static void create_device_cache(KVCacheLayer& c, size_t prefill_capacity) {
+    const int32_t cap = (int32_t)prefill_capacity;
+    mkv_cache_config cfg{};
+    cfg.n_units = 1;
+    cfg.head_dim = (int)c.d;
+    cfg.n_r = (int)c.n_r;
+    cfg.group_size = (int)c.group_size;
+    cfg.prefill_capacity = &cap;
+    cfg.max_decode_tokens = (int)c.decode_reserve;
+    cfg.keep_fp32_params = 1;  // exports carry the reference's fp32 (scale, zero) bit-exactly
+    c.impl.reset(new KVCacheLayer::Impl());
+    throw_status(mkv_cache_create(&cfg, &c.impl->h), "make_cache");
+}
+
+KVCacheLayer make_cache(size_t d, size_t n_r, size_t group_size) {
+    if (d < 1) throw std::invalid_argument("make_cache: d must be >= 1");
+    if (group_size < 1 || n_r == 0 || n_r % group_size != 0)
+        throw std::invalid_argument("make_cache: n_r must be a positive multiple of group_size");
+    KVCacheLayer c;
+    c.d = d;
+    c.n_r = n_r;
+    c.group_size = group_size;
+    create_device_cache(c, 0);
+    return c;
+}
+
+size_t KVCacheLayer::tokens_quantized() const {
+    int64_t tq = 0;
+    throw_status(mkv_cache_unit_info(handle(*this), 0, &tq, nullptr, nullptr, nullptr), "tokens_quantized");
+    return (size_t)tq;
+}
+
+size_t KVCacheLayer::tokens_residual() const {
+    int64_t tr = 0;
+    throw_status(mkv_cache_unit_info(handle(*this), 0, nullptr, &tr, nullptr, nullptr), "tokens_residual");
+    return (size_t)tr;
+}
+
+static QuantizedTensor export_tensor(const KVCacheLayer& c, int which) {
+    int64_t nw = 0, np = 0, nb = 0;
+    throw_status(mkv_cache_export_sizes(handle(c), 0, which, &nw, &np, &nb), "export");
+    QuantizedTensor t;
+    t.axis = which == 0 ? GroupAxis::PerChannel : GroupAxis::PerToken;
+    t.group_size = c.group_size;
+    t.logical_rows = c.tokens_quantized();
+    t.logical_cols = c.d;
+    t.packed_words.resize(std::max<int64_t>(nw, 1));
+    std::vector<float> params(std::max<int64_t>(2 * np, 2));
+    std::vector<int64_t> br(std::max<int64_t>(nb, 1));
+    throw_status(mkv_cache_export_reference(handle(c), 0, which, t.packed_words.data(), params.data(), br.data()),
+                 "export");
+    t.packed_words.resize(nw);
+    t.params.resize(np);
+    for (int64_t g = 0; g < np; ++g) t.params[g] = GroupQuantParams{params[2 * g], params[2 * g + 1]};
+    t.block_rows.assign(br.begin(), br.begin() + nb);
+    t.total_codes = t.logical_rows * t.logical_cols;
+    return t;
+}
+
+QuantizedTensor KVCacheLayer::q_key() const { return export_tensor(*this, 0); }
+QuantizedTensor KVCacheLayer::q_value() const { return export_tensor(*this, 1); }
+
+static Matrix residual(const KVCacheLayer& c, bool value) {
+    const size_t n = c.tokens_residual();
+    std::vector<uint16_t> rk(std::max<size_t>(n, 1) * c.d), rv(std::max<size_t>(n, 1) * c.d);
+    throw_status(mkv_cache_export_residual(handle(c), 0, rk.data(), rv.data()), "residual");
+    Matrix m(n, c.d);
+    const std::vector<uint16_t>& src = value ? rv : rk;
+    for (size_t i = 0; i < n * c.d; ++i) {
+        __half_raw r;
+        r.x = src[i];
+        m.data[i] = __half2float(__half(r));
+    }
+    return m;
+}
+
+Matrix KVCacheLayer::r_key() const { return residual(*this, false); }
+Matrix KVCacheLayer::r_value() const { return residual(*this, true); }
+
+std::uint64_t measured_bytes(const KVCacheLayer& c) {  // accounting.cpp:101-114
+    std::uint64_t bytes = 0;
+    for (int which = 0; which < 2; ++which) {
+        int64_t nw = 0, np = 0;
+        throw_status(mkv_cache_export_sizes(handle(c), 0, which, &nw, &np, nullptr), "measured_bytes");
+        bytes += (std::uint64_t)nw * 4 + (std::uint64_t)np * 4;  // (scale, zero) counted as 2 x fp16
+    }
+    bytes += (std::uint64_t)c.tokens_residual() * c.d * 2 * 2;
+    return bytes;
+}
+
+std::pair<KVCacheLayer, PrefillReport> prefill(const Matrix& k, const Matrix& v, const Vector& a_cumul,
+                                               size_t hh_count, size_t rw_count, size_t n_r, size_t group_size) {
+    if (k.rows != v.rows || k.rows != a_cumul.size()) throw std::invalid_argument("prefill: k/v/a_cumul length mismatch");
+    if (k.cols != v.cols) throw std::invalid_argument("prefill: k/v width mismatch");
+    if (hh_count + rw_count == 0) throw std::runtime_error("prefill: zero kept tokens");
+    KVCacheLayer c;
+    c.d = k.cols;
+    c.n_r = n_r;
+    c.group_size = group_size;
+    if (group_size < 1 || n_r == 0 || n_r % group_size != 0)
+        throw std::invalid_argument("make_cache: n_r must be a positive multiple of group_size");
+    const size_t l = k.rows;
+    const size_t n_kept = std::min(hh_count + rw_count, l);
+    create_device_cache(c, n_kept);
+    PrefillReport report;
+    report.kept = select_token_counts(a_cumul, hh_count, rw_count);
+    report.a_cumul = a_cumul;
+    report.bytes_before = (std::uint64_t)2 * l * k.cols * 2;  // K + V at fp16
+    if (l > 0) {
+        Dev dk = upload_half(k.data.data(), l * c.d), dv = upload_half(v.data.data(), l * c.d);
+        Dev da = upload_f32(a_cumul.data(), l);
+        const int32_t hh = (int32_t)hh_count;
+        mkv_prefill_select_args a{};
+        a.unit_begin = 0; a.n_units = 1; a.length = (int)l;
+        a.a_cumul = da.as<float>(); a.a_stride = (int64_t)l;
+        a.hh_count = &hh; a.rw_count = (int)rw_count;
+        a.k = dk.p; a.k_su = (int64_t)l * c.d; a.k_st = (int64_t)c.d;
+        a.v = dv.p; a.v_su = (int64_t)l * c.d; a.v_st = (int64_t)c.d;
+        throw_status(mkv_cache_prefill_select(handle(c), &a, nullptr), "prefill");
+        throw_status(mkv_cache_check(handle(c)), "prefill");  // non-finite input -> domain_error
+    }
+    report.bytes_after = measured_bytes(c);
+    return {std::move(c), std::move(report)};
+}
+
+void decode_append(KVCacheLayer& c, const Vector& t_k, const Vector& t_v) {
+    if (t_k.size() != c.d || t_v.size() != c.d) throw std::invalid_argument("decode_append: token dimension mismatch");
+    Dev dk = upload_half(t_k.data(), c.d), dv = upload_half(t_v.data(), c.d);
+    throw_status(mkv_cache_append(handle(c), 0, 1, dk.p, dv.p, nullptr), "decode_append");
+    throw_status(mkv_cache_check(handle(c)), "decode_append");
+}
+
+Vector decode_step(KVCacheLayer& c, const Vector& t_q, const Vector& t_k, const Vector& t_v, float scale) {
+    if (t_q.size() != c.d || t_k.size() != c.d || t_v.size() != c.d)
+        throw std::invalid_argument("decode_step: token dimension mismatch");
+    Dev dq = upload_half(t_q.data(), c.d), dk = upload_half(t_k.data(), c.d), dv = upload_half(t_v.data(), c.d);
+    Dev dout(c.d * sizeof(__half));
+    mkv_decode_args a{};
+    a.unit_begin = 0; a.n_units = 1; a.group = 1;
+    a.q = dq.p; a.k_new = dk.p; a.v_new = dv.p; a.out = dout.p; a.scale = scale;
+    throw_status(mkv_decode_step(handle(c), &a, nullptr), "decode_step");
+    throw_status(mkv_cache_check(handle(c)), "decode_step");
+    return download_half(dout, c.d);
+}
+
+Matrix stored_keys(const KVCacheLayer& c) { return dequantize_matrix(c.q_key()); }
+Matrix stored_values(const KVCacheLayer& c) { return dequantize_matrix(c.q_value()); }
+
+}  // namespace minikv_b200

@@ -40,6 +40,8 @@ struct SelectParams {
     int32_t* n_kept;    // may be null
 };
 cudaError_t launch_select(const SelectParams& p, cudaStream_t s);
+// layer_score_variance (selection.cpp:130-146) of n rows, fp64 two-pass, deterministic
+cudaError_t launch_score_variance(const float* a, int64_t a_stride, int n, int length, float* out, cudaStream_t s);
 
 // ---- K4: decode (decode.cu) ----
 struct ResidualParams {

@@ -416,6 +416,54 @@ __global__ void __launch_bounds__(kSelThreads) select_cluster_kernel(const Selec
     }
 }
 
+// ---------------------------------------------------------------------------
+// layer_score_variance (selection.cpp:130-146): population variance of A_cumul, the
+// per-layer statistic of variance-based budget allocation (allocate_variance,
+// selection.cpp:85-128).  One CTA per row; two fp64 passes (mean, then squared
+// deviations) like the reference, reduced in a fixed tree order (deterministic).
+// ---------------------------------------------------------------------------
+constexpr int kVarThreads = 512;
+
+__device__ __forceinline__ double block_sum_f64(double v, double* red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    double t = 0.0;
+    if (warp == 0) {
+        t = lane < kVarThreads / 32 ? red[lane] : 0.0;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (lane == 0) red[32] = t;
+    }
+    __syncthreads();
+    t = red[32];
+    __syncthreads();
+    return t;
+}
+
+__global__ void __launch_bounds__(kVarThreads) score_variance_kernel(const float* __restrict__ a, int64_t stride,
+                                                                     int length, float* __restrict__ out) {
+    __shared__ double red[33];
+    const float* row = a + (size_t)blockIdx.x * stride;
+    double s = 0.0;
+    for (int j = threadIdx.x; j < length; j += kVarThreads) s += (double)__ldg(row + j);
+    const double mean = block_sum_f64(s, red) / (double)length;
+    double q = 0.0;
+    for (int j = threadIdx.x; j < length; j += kVarThreads) {
+        const double d = (double)__ldg(row + j) - mean;
+        q = __dadd_rn(q, __dmul_rn(d, d));  // multiply then add, as the reference (no FMA)
+    }
+    const double var = block_sum_f64(q, red);
+    if (threadIdx.x == 0) out[blockIdx.x] = (float)(var / (double)length);
+}
+
+cudaError_t launch_score_variance(const float* a, int64_t a_stride, int n, int length, float* out, cudaStream_t s) {
+    score_variance_kernel<<<n, kVarThreads, 0, s>>>(a, a_stride, length, out);
+    return cudaGetLastError();
+}
+
 // cluster size per unit: spread few long units over the SMs (0 = single-CTA kernel)
 static int select_cluster_size(const SelectParams& p) {
     static int sms = 0;

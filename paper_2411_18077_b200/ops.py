@@ -136,6 +136,37 @@ def allocate_pyramid(mean_budget_x: int, layers: int, depth: int = 7, bottom_hea
     return [int(x) for x in out[:layers]]
 
 
+class VarianceMode:
+    """selection.hpp VarianceMode: shares proportional (Prop) or inverse (Inv) to variance."""
+    Prop = 0
+    Inv = 1
+
+
+def allocate_variance(per_layer_variance: Sequence[float], total_hh: int, mode: int = VarianceMode.Prop):
+    """selection.cpp:85-128 (host arithmetic in the C ABI, bit-exact).  Returns
+    (per_layer_hh, uniform_fallback)."""
+    v = (C.c_float * max(len(per_layer_variance), 1))(*[float(x) for x in per_layer_variance])
+    out = (C.c_int64 * max(len(per_layer_variance), 1))()
+    fb = C.c_int(0)
+    check(lib().mkv_allocate_variance(v, len(per_layer_variance), int(total_hh), int(mode), out, C.byref(fb)),
+          "allocate_variance")
+    return [int(x) for x in out[:len(per_layer_variance)]], bool(fb.value)
+
+
+def layer_score_variance(a_cumul: torch.Tensor, stream=None) -> torch.Tensor:
+    """selection.cpp:130-146 on the device: population variance of each row of an fp32
+    CUDA tensor [L] or [n, L] (fp64 two-pass) -> fp32 tensor [] or [n]."""
+    single = a_cumul.dim() == 1
+    a2 = a_cumul[None] if single else a_cumul
+    if a2.dtype != torch.float32 or not a2.is_cuda or a2.stride(-1) != 1:
+        raise _capi.InvalidArgument("layer_score_variance: a_cumul must be an fp32 CUDA tensor")
+    n, L = a2.shape
+    out = torch.empty(n, dtype=torch.float32, device=a2.device)
+    check(lib().mkv_score_variance(a2.data_ptr(), a2.stride(0), n, L, out.data_ptr(), _stream_ptr(stream)),
+          "layer_score_variance")
+    return out[0] if single else out
+
+
 def allocate_uniform(total_hh: int, layers: int):
     """selection.cpp:48-59."""
     out = (C.c_int64 * max(layers, 1))()

@@ -7,6 +7,7 @@ import os
 import re
 import subprocess
 
+import numpy as np
 import pytest
 import torch
 
@@ -55,6 +56,25 @@ def test_host_helpers_match_oracle_without_gpu():
         allocate_pyramid(10, 0)
     with pytest.raises(_capi.InvalidArgument):
         allocate_pyramid(10, 4, 0)
+
+
+def test_variance_allocation_matches_oracle_without_gpu():  # selection.cpp:85-128 (host, bit-exact)
+    from paper_2411_18077_b200 import VarianceMode, allocate_variance
+    P = oracle.port()
+    rng = np.random.default_rng(11)
+    for t in range(200):
+        layers, total = int(rng.integers(1, 33)), int(rng.integers(0, 300000))
+        v = (rng.random(layers) * 5).astype(np.float32)
+        if t % 5 == 0:
+            v[:] = 0.0
+        for mode in (VarianceMode.Prop, VarianceMode.Inv):
+            hh, fb = allocate_variance(v, total, mode)
+            exp, efb = P.allocate_variance(v, total, inverse=mode == VarianceMode.Inv)
+            assert hh == list(exp) and fb == efb
+    with pytest.raises(_capi.InvalidArgument):
+        allocate_variance([], 5)
+    with pytest.raises(_capi.InvalidArgument):
+        allocate_variance([1.0, -0.5], 5)
 
 
 @pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU failure path")

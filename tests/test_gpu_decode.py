@@ -135,3 +135,25 @@ def test_decode_attend_only_is_idempotent(mkv):
     assert [cache.unit_info(u)["tokens_residual"] for u in range(n)] == [20] * n
     rk, rv = cache.export_residual(0)
     assert rk.shape == (20, d)
+
+
+def test_append_only_cache_blocks_export_bit_exact(mkv):
+    """A cache that never had a prefill: every quantized block is an n_r flush block
+    (1000 appends -> 7 blocks + 104 residual rows, test_cache_engine.cpp:116-128), and
+    the export matches the oracle's QuantizedTensor stream bit for bit."""
+    d = 128
+    rng = np.random.default_rng(21)
+    cache = mkv.KVCache(1, 0, max_decode_tokens=1100, keep_fp32_params=True)
+    oc = oracle.port().cache()
+    for _ in range(1000):
+        t = rng.standard_normal((1, d)).astype(np.float16)
+        u = rng.standard_normal((1, d)).astype(np.float16)
+        cache.append(torch.from_numpy(t).cuda(), torch.from_numpy(u).cuda())
+        oc.append(f32(t[0]), f32(u[0]))
+    cache.check()
+    info = cache.unit_info(0)
+    assert info["tokens_quantized"] == 7 * 128 and info["tokens_residual"] == 104 and info["n_blocks"] == 7
+    for which in (0, 1):
+        w, p, br = cache.export_reference(0, which)
+        ew, ep, ebr = oc.export(which)
+        assert np.array_equal(w, ew) and np.array_equal(p.reshape(-1), ep.reshape(-1)) and list(br) == list(ebr)

@@ -213,3 +213,20 @@ def test_select_cluster_path_matches_oracle(mkv, monkeypatch, cluster, L, hh, rw
     kept = kept.cpu().numpy()
     for u in range(n):
         np.testing.assert_array_equal(kept[u, :nks[u]], oracle_select(a[u], hh, rw))
+
+
+
+def test_layer_score_variance_device(mkv):
+    """layer_score_variance (selection.cpp:130-146) on the device, batched over rows.
+    Known answers are exact; random rows agree with the oracle to 1e-6 relative (the
+    device sums in a fixed tree order instead of index order, both in fp64)."""
+    P = oracle.port()
+    assert float(mkv.layer_score_variance(torch.tensor([5.0, 5.0, 5.0]).cuda())) == 0.0
+    assert float(mkv.layer_score_variance(torch.tensor([0.0, 2.0]).cuda())) == 1.0
+    rng = np.random.default_rng(12)
+    for L in (1, 7, 1000, 32768, 131072):
+        a = (rng.random((5, L)) ** 3).astype(np.float32)
+        got = mkv.layer_score_variance(torch.from_numpy(a).cuda()).cpu().numpy()
+        for u in range(5):
+            exp = P.layer_score_variance(a[u])
+            assert abs(got[u] - exp) <= 1e-6 * max(abs(exp), 1e-30), (L, u, got[u], exp)

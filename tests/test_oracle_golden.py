@@ -113,6 +113,32 @@ def test_pyramid_known(P):  # test_selection.cpp:113-137
     assert list(P.allocate_uniform(33, 32)) == [2] + [1] * 31
 
 
+def test_variance_allocation_known(P):  # test_selection.cpp:151-179
+    for inv in (False, True):
+        hh, fb = P.allocate_variance([1, 1, 1, 1], 40, inverse=inv)
+        assert list(hh) == [10] * 4 and not fb
+    assert list(P.allocate_variance([3, 1], 40)[0]) == [30, 10]
+    hh, fb = P.allocate_variance([0, 0, 0], 30)
+    assert fb and list(hh) == [10] * 3
+    rng = np.random.default_rng(36)
+    for _ in range(100):
+        layers, total = int(rng.integers(1, 25)), int(rng.integers(0, 3000))
+        v = (rng.random(layers) * 4).astype(np.float32)
+        for inv in (False, True):
+            assert int(P.allocate_variance(v, total, inverse=inv)[0].sum()) == total
+    with pytest.raises(ValueError):
+        P.allocate_variance([], 10)
+    with pytest.raises(ValueError):
+        P.allocate_variance([1.0, -1.0], 10)
+
+
+def test_population_variance_known(P):  # test_selection.cpp:180-196
+    assert P.layer_score_variance([5, 5, 5]) == 0.0
+    assert P.layer_score_variance([0, 2]) == 1.0
+    a = np.random.default_rng(37).standard_normal(64).astype(np.float32)
+    assert abs(P.layer_score_variance(a) - float(np.var(a.astype(np.float64)))) < 1e-6
+
+
 def test_cache_flush_counts(P):  # test_cache_engine.cpp:116-128
     rng = np.random.default_rng(45)
     c = P.cache(d=16, n_r=128)

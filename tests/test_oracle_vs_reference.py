@@ -87,3 +87,22 @@ def test_cache_decode_random(PR):
         for which in (0, 1):
             for x, y in zip(pc.export(which), rc.export(which)):
                 assert np.array_equal(x, y)
+
+
+def test_variance_allocation_random(PR):  # selection.cpp:85-146, bit-identical allocations
+    P, R = PR
+    rng = np.random.default_rng(9)
+    for t in range(300):
+        layers, total = int(rng.integers(1, 40)), int(rng.integers(0, 100000))
+        v = (rng.random(layers) * (10.0 ** rng.integers(-6, 4))).astype(np.float32)
+        if t % 7 == 0:
+            v[rng.integers(0, layers)] = 0.0
+        if t % 11 == 0:
+            v[:] = v[0]  # equal shares -> fraction ties resolved to the lower layer
+        for inv in (False, True):
+            a, fa = P.allocate_variance(v, total, inverse=inv)
+            b, fb = R.allocate_variance(v, total, inverse=inv)
+            assert np.array_equal(a, b) and fa == fb
+    for _ in range(50):
+        a = (rng.random(int(rng.integers(1, 5000))) * 3).astype(np.float32)
+        assert P.layer_score_variance(a) == R.layer_score_variance(a)
