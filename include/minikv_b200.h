@@ -215,6 +215,22 @@ int mkv_cache_export_residual(const mkv_cache* cache, int unit, uint16_t* r_key_
 int mkv_cache_check(mkv_cache* cache);
 
 /* ------------------------------------------------------------------------ */
+/* MKVC snapshots of one unit (the reference's on-disk cache format).        */
+/* replaces: save_cache(const KVCacheLayer&, path) / load_cache(path)        */
+/*           snapshot.hpp:11-24, snapshot.cpp:71-198 (little-endian "MKVC" */
+/*           v1: d, n_r, group_size, mode, tokens_quantized, K then V        */
+/*           QuantizedTensor streams, identity stores, fp32 residuals).      */
+/* save: synchronous; byte-identical to the reference's save_cache for the  */
+/* same cache when the handle keeps fp32 params (else fp16 params widened). */
+/* load: replaces unit `unit` with the snapshot (2-bit mode; d, n_r and     */
+/* group_size must match the handle; pages rebuilt in the device layout;    */
+/* residual rows rounded to fp16).  Errors as the reference: bad magic /    */
+/* version / truncation -> MKV_ERR_RUNTIME.                                 */
+/* ------------------------------------------------------------------------ */
+int mkv_cache_save_mkvc(const mkv_cache* cache, int unit, const char* path);
+int mkv_cache_load_mkvc(mkv_cache* cache, int unit, const char* path);
+
+/* ------------------------------------------------------------------------ */
 /* Synthetic inputs (benchmarks/tests): the integer-exact approximate-N(0,1) */
 /* fp16 generator of oracle/minikv_oracle.h, bit-identical on device.        */
 /* ------------------------------------------------------------------------ */

@@ -340,6 +340,8 @@ class RefOracle(_Lib):
             f.argtypes = [C.c_void_p, C.c_int]
             f.restype = _sz
         L.mkr_cache_export.argtypes = [C.c_void_p, C.c_int, _u32p, _f32p, _i64p]
+        L.mkr_cache_save.argtypes = [C.c_void_p, C.c_char_p]
+        L.mkr_cache_load.argtypes = [C.c_char_p, C.POINTER(C.c_void_p)]
         L.mkr_decode_set_create.argtypes = [_sz, _sz, _sz, _sz, _i64p, _sz, _sz, _sz, C.c_uint64,
                                             np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS"),
                                             C.c_int, C.POINTER(C.c_void_p)]
@@ -376,6 +378,12 @@ class RefOracle(_Lib):
                                           C.byref(h)), "prefill")
         return RefCache(self, h, k.shape[1])
 
+    def load_cache(self, path, d=128) -> "RefCache":
+        """load_cache (snapshot.cpp:159-198)."""
+        h = C.c_void_p()
+        _check(self.lib.mkr_cache_load(os.fsencode(path), C.byref(h)), "load_cache")
+        return RefCache(self, h, d)
+
 
 class RefCache:
     def __init__(self, ref: RefOracle, h, d):
@@ -402,6 +410,10 @@ class RefCache:
     @property
     def tokens_residual(self):
         return self.ref.lib.mkr_cache_tokens_residual(self.h)
+
+    def save(self, path):
+        """save_cache (snapshot.cpp:71-157)."""
+        _check(self.ref.lib.mkr_cache_save(self.h, os.fsencode(path)), "save_cache")
 
     def export(self, which: int):
         L = self.ref.lib

@@ -23,6 +23,7 @@
 
 #include "minikv/attention.hpp"
 #include "minikv/cache_engine.hpp"
+#include "minikv/snapshot.hpp"
 #include "minikv/quantizer.hpp"
 #include "minikv/selection.hpp"
 #include "minikv_oracle.h"
@@ -212,6 +213,12 @@ int mkr_cache_decode_step(mkr_cache* c, const float* tq, const float* tk, const 
                                scale);
         std::memcpy(out, o.data(), sizeof(float) * d);
     })
+}
+
+// snapshot.cpp:71-198
+int mkr_cache_save(const mkr_cache* c, const char* path) { GUARD({ save_cache(c->layer, std::string(path)); }) }
+int mkr_cache_load(const char* path, mkr_cache** out) {
+    GUARD({ *out = new mkr_cache{load_cache(std::string(path))}; })
 }
 
 size_t mkr_cache_tokens_quantized(const mkr_cache* c) { return c->layer.tokens_quantized; }

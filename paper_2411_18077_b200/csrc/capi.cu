@@ -769,6 +769,260 @@ int mkv_cache_check(mkv_cache* c) {
 }
 
 // ---------------------------------------------------------------------------
+// MKVC snapshots (snapshot.cpp:71-198)
+// ---------------------------------------------------------------------------
+namespace {
+void put_u32(std::vector<uint8_t>& b, uint32_t v) {
+    for (int i = 0; i < 4; ++i) b.push_back(static_cast<uint8_t>((v >> (8 * i)) & 0xFF));
+}
+void put_u64(std::vector<uint8_t>& b, uint64_t v) {
+    for (int i = 0; i < 8; ++i) b.push_back(static_cast<uint8_t>((v >> (8 * i)) & 0xFF));
+}
+void put_f32(std::vector<uint8_t>& b, float f) {
+    uint32_t u;
+    memcpy(&u, &f, 4);
+    put_u32(b, u);
+}
+struct Reader {
+    const std::vector<uint8_t>& b;
+    size_t pos = 0;
+    bool ok = true;
+    uint64_t get(int bytes) {
+        if (pos + bytes > b.size()) {
+            ok = false;
+            return 0;
+        }
+        uint64_t v = 0;
+        for (int i = 0; i < bytes; ++i) v |= static_cast<uint64_t>(b[pos + i]) << (8 * i);
+        pos += bytes;
+        return v;
+    }
+    uint32_t u32() { return static_cast<uint32_t>(get(4)); }
+    uint64_t u64() { return get(8); }
+    float f32() {
+        const uint32_t u = u32();
+        float f;
+        memcpy(&f, &u, 4);
+        return f;
+    }
+};
+struct SnapTensor {
+    uint32_t axis = 0;
+    uint64_t rows = 0;
+    std::vector<uint64_t> blocks;
+    std::vector<uint32_t> words;
+    std::vector<float> params;  // (scale, zero) pairs
+};
+bool read_tensor(Reader& r, SnapTensor& t, uint64_t d) {
+    t.axis = r.u32();
+    t.rows = r.u64();
+    const uint64_t nb = r.u64();
+    if (!r.ok || nb > r.b.size()) return false;
+    t.blocks.resize(nb);
+    uint64_t codes = 0;
+    for (auto& x : t.blocks) {
+        x = r.u64();
+        codes += x * d;
+    }
+    const uint64_t nw = r.u64();
+    if (!r.ok || nw > r.b.size()) return false;
+    t.words.resize(nw);
+    for (auto& w : t.words) w = r.u32();
+    const uint64_t np = r.u64();
+    if (!r.ok || np > r.b.size()) return false;
+    t.params.resize(2 * np);
+    for (auto& p : t.params) p = r.f32();
+    return r.ok && nw == (codes + 15) / 16;  // snapshot.cpp:126-131
+}
+}  // namespace
+
+int mkv_cache_save_mkvc(const mkv_cache* c, int u, const char* path) {
+    if (int r = check_range(c, u, 1)) return r;
+    if (!path) return fail(MKV_ERR_INVALID_ARGUMENT, "snapshot: null path");
+    int64_t tq = 0;
+    mkv_cache_unit_info(c, u, &tq, nullptr, nullptr, nullptr);
+    std::vector<uint8_t> b;
+    b.insert(b.end(), {'M', 'K', 'V', 'C'});
+    put_u32(b, 1);
+    put_u64(b, c->d);
+    put_u64(b, c->n_r);
+    put_u64(b, c->gs);
+    put_u64(b, 0);  // QuantMode::TwoBit
+    put_u64(b, (uint64_t)tq);
+    for (int which = 0; which < 2; ++which) {
+        int64_t nw = 0, np = 0, nb = 0;
+        if (int r = mkv_cache_export_sizes(c, u, which, &nw, &np, &nb)) return r;
+        std::vector<uint32_t> words(std::max<int64_t>(nw, 1));
+        std::vector<float> params(std::max<int64_t>(2 * np, 2));
+        std::vector<int64_t> br(std::max<int64_t>(nb, 1));
+        if (int r = mkv_cache_export_reference(c, u, which, words.data(), params.data(), br.data())) return r;
+        put_u32(b, which == 0 ? 0u : 1u);  // PerChannel keys, PerToken values
+        put_u64(b, (uint64_t)tq);
+        put_u64(b, (uint64_t)nb);
+        for (int64_t i = 0; i < nb; ++i) put_u64(b, (uint64_t)br[i]);
+        put_u64(b, (uint64_t)nw);
+        for (int64_t i = 0; i < nw; ++i) put_u32(b, words[i]);
+        put_u64(b, (uint64_t)np);
+        for (int64_t i = 0; i < 2 * np; ++i) put_f32(b, params[i]);
+    }
+    put_u64(b, 0);  // identity-mode key / value stores: empty in 2-bit mode
+    put_u64(b, 0);
+    const int rows = c->n_res[u];
+    std::vector<uint16_t> rk((size_t)std::max(rows, 1) * c->d), rv(rk.size());
+    if (int r = mkv_cache_export_residual(c, u, rk.data(), rv.data())) return r;
+    auto half_to_float = [](uint16_t h) { __half_raw x; x.x = h; return __half2float(__half(x)); };
+    for (const auto* m : {&rk, &rv}) {
+        put_u64(b, (uint64_t)rows);
+        for (size_t i = 0; i < (size_t)rows * c->d; ++i) put_f32(b, half_to_float((*m)[i]));
+    }
+    FILE* f = fopen(path, "wb");
+    if (!f) return fail(MKV_ERR_RUNTIME, "snapshot: cannot open %s", path);
+    const size_t w = fwrite(b.data(), 1, b.size(), f);
+    const int cl = fclose(f);
+    if (w != b.size() || cl != 0) return fail(MKV_ERR_RUNTIME, "snapshot: write failed");
+    return MKV_OK;
+}
+
+int mkv_cache_load_mkvc(mkv_cache* c, int u, const char* path) {
+    if (int r = check_range(c, u, 1)) return r;
+    if (!path) return fail(MKV_ERR_INVALID_ARGUMENT, "snapshot: null path");
+    if (int r = require_device()) return r;
+    std::vector<uint8_t> buf;
+    {
+        FILE* f = fopen(path, "rb");
+        if (!f) return fail(MKV_ERR_RUNTIME, "snapshot: cannot open %s", path);
+        uint8_t tmp[1 << 16];
+        size_t n;
+        while ((n = fread(tmp, 1, sizeof(tmp), f)) > 0) buf.insert(buf.end(), tmp, tmp + n);
+        fclose(f);
+    }
+    if (buf.size() < 4 || memcmp(buf.data(), "MKVC", 4) != 0) return fail(MKV_ERR_RUNTIME, "snapshot: bad magic");
+    Reader r{buf};
+    r.pos = 4;
+    const uint32_t version = r.u32();
+    if (!r.ok) return fail(MKV_ERR_RUNTIME, "snapshot: truncated file");
+    if (version != 1) return fail(MKV_ERR_RUNTIME, "snapshot: unsupported version");
+    const uint64_t d = r.u64(), n_r = r.u64(), gs = r.u64(), mode = r.u64(), tq = r.u64();
+    if (!r.ok) return fail(MKV_ERR_RUNTIME, "snapshot: truncated file");
+    if (mode != 0) return fail(MKV_ERR_UNSUPPORTED, "snapshot: identity-mode caches have no device form");
+    if (d != (uint64_t)c->d || n_r != (uint64_t)c->n_r || gs != (uint64_t)c->gs)
+        return fail(MKV_ERR_INVALID_ARGUMENT, "snapshot: d/n_r/group_size %llu/%llu/%llu differ from the cache",
+                    (unsigned long long)d, (unsigned long long)n_r, (unsigned long long)gs);
+    SnapTensor tk, tv;
+    if (!read_tensor(r, tk, d) || !read_tensor(r, tv, d)) {
+        if (!r.ok) return fail(MKV_ERR_RUNTIME, "snapshot: truncated file");
+        return fail(MKV_ERR_RUNTIME, "snapshot: packed word count inconsistent");
+    }
+    const uint64_t fk = r.u64();
+    if (fk) return fail(MKV_ERR_UNSUPPORTED, "snapshot: identity stores in a 2-bit snapshot");
+    const uint64_t fv = r.u64();
+    if (fv) return fail(MKV_ERR_UNSUPPORTED, "snapshot: identity stores in a 2-bit snapshot");
+    const uint64_t rrows = r.u64();
+    if (!r.ok || rrows > n_r) return fail(MKV_ERR_RUNTIME, "snapshot: truncated file");
+    std::vector<float> res_k(rrows * d), res_v;
+    for (auto& x : res_k) x = r.f32();
+    const uint64_t rrows_v = r.u64();
+    if (!r.ok || rrows_v > n_r) return fail(MKV_ERR_RUNTIME, "snapshot: truncated file");
+    res_v.resize(rrows_v * d);
+    for (auto& x : res_v) x = r.f32();
+    if (!r.ok) return fail(MKV_ERR_RUNTIME, "snapshot: truncated file");
+    if (rrows != rrows_v || rrows >= n_r) return fail(MKV_ERR_RUNTIME, "snapshot: residual buffer state invalid");
+    // device form: an optional first block of any size (the prefill block), then n_r-row blocks
+    if (tk.blocks != tv.blocks || tk.axis != 0 || tv.axis != 1)
+        return fail(MKV_ERR_UNSUPPORTED, "snapshot: key/value block structure not produced by the cache engine");
+    uint64_t rows_total = 0;
+    for (size_t b = 0; b < tk.blocks.size(); ++b) {
+        if (tk.blocks[b] == 0 || (b > 0 && tk.blocks[b] != n_r))
+            return fail(MKV_ERR_UNSUPPORTED, "snapshot: block %zu of %llu rows (device blocks: prefill, then n_r)", b,
+                        (unsigned long long)tk.blocks[b]);
+        rows_total += tk.blocks[b];
+    }
+    if (rows_total != tq || tk.rows != tq) return fail(MKV_ERR_RUNTIME, "snapshot: token counts inconsistent");
+    const int nb = (int)tk.blocks.size();
+    const int n_prefill = nb ? (int)tk.blocks[0] : 0;
+    const int n_pages = nb ? (n_prefill + kGroup - 1) / kGroup + (nb - 1) * (c->n_r / kGroup) : 0;
+    if (n_pages > c->cap_pages[u]) return fail(MKV_ERR_OUT_OF_RANGE, "snapshot: %d pages exceed the unit's capacity", n_pages);
+    // rebuild the pages in the device layout (inverse of mkv_cache_export_reference)
+    std::vector<uint8_t> pages((size_t)std::max(n_pages, 1) * kPageBytes, 0);
+    std::vector<float> shadow(c->shadow ? (size_t)std::max(n_pages, 1) * kShadowBytes / 4 : 0, 0.0f);
+    auto code_at = [](const std::vector<uint32_t>& w, uint64_t i) { return (w[i / 16] >> (2 * (i % 16))) & 3u; };
+    auto half_bits = [](float f) { __half h = __float2half_rn(f); return *reinterpret_cast<uint16_t*>(&h); };
+    uint64_t kc0 = 0, kg0 = 0, vc0 = 0, vg0 = 0;
+    int page0 = 0;
+    for (int b = 0; b < nb; ++b) {
+        const int R = (int)tk.blocks[b], gpr = (R + kGroup - 1) / kGroup;
+        for (int g = 0; g < gpr; ++g) {
+            uint8_t* pg = pages.data() + (size_t)(page0 + g) * kPageBytes;
+            uint32_t* kwords = reinterpret_cast<uint32_t*>(pg + kKC);
+            uint32_t* vwords = reinterpret_cast<uint32_t*>(pg + kVC);
+            uint16_t* ks = reinterpret_cast<uint16_t*>(pg + kKS);
+            uint16_t* kz = reinterpret_cast<uint16_t*>(pg + kKZ);
+            uint16_t* vs = reinterpret_cast<uint16_t*>(pg + kVS);
+            uint16_t* vz = reinterpret_cast<uint16_t*>(pg + kVZ);
+            float* sh = c->shadow ? shadow.data() + (size_t)(page0 + g) * (kShadowBytes / 4) : nullptr;
+            const int valid = std::min(kGroup, R - kGroup * g);
+            for (int ch = 0; ch < c->d; ++ch) {  // keys: PerChannel groups (channel-major within the block)
+                const uint64_t gi = kg0 + (uint64_t)ch * gpr + g;
+                const float sc = tk.params[2 * gi], zp = tk.params[2 * gi + 1];
+                ks[k_param_idx(ch)] = half_bits(sc);
+                kz[k_param_idx(ch)] = half_bits(zp);
+                if (sh) { sh[2 * ch] = sc; sh[2 * ch + 1] = zp; }
+                for (int t = 0; t < valid; ++t) {
+                    const CodePos cp = k_code_pos(t, ch);
+                    kwords[cp.word] |= code_at(tk.words, kc0 + (uint64_t)ch * R + kGroup * g + t) << cp.shift;
+                }
+            }
+            for (int t = 0; t < valid; ++t) {  // values: PerToken groups (token-major)
+                const uint64_t row = (uint64_t)kGroup * g + t;
+                for (int vg = 0; vg < c->d / kGroup; ++vg) {
+                    const uint64_t gi = vg0 + row * (c->d / kGroup) + vg;
+                    const float sc = tv.params[2 * gi], zp = tv.params[2 * gi + 1];
+                    vs[vs_param_idx(t, vg)] = half_bits(sc);
+                    vz[vz_param_idx(t, vg)] = half_bits(zp);
+                    if (sh) { sh[256 + 2 * (t * 8 + vg)] = sc; sh[256 + 2 * (t * 8 + vg) + 1] = zp; }
+                    for (int cc = 0; cc < kGroup; ++cc) {
+                        const int ch = kGroup * vg + cc;
+                        const CodePos cp = v_code_pos(t, ch);
+                        vwords[cp.word] |= code_at(tv.words, vc0 + row * c->d + ch) << cp.shift;
+                    }
+                }
+            }
+        }
+        kc0 += (uint64_t)R * c->d;
+        kg0 += (uint64_t)c->d * gpr;
+        vc0 += (uint64_t)R * c->d;
+        vg0 += (uint64_t)R * (c->d / kGroup);
+        page0 += gpr;
+    }
+    if (kg0 * 2 != tk.params.size() || vg0 * 2 != tv.params.size())
+        return fail(MKV_ERR_RUNTIME, "snapshot: parameter count inconsistent");
+    CK(cudaDeviceSynchronize());
+    if (n_pages) {
+        CK(cudaMemcpy(c->d_pool + (size_t)c->page_base[u] * kPageBytes, pages.data(), (size_t)n_pages * kPageBytes,
+                      cudaMemcpyHostToDevice));
+        if (c->shadow)
+            CK(cudaMemcpy(c->d_shadow + (size_t)c->page_base[u] * (kShadowBytes / 4), shadow.data(),
+                          (size_t)n_pages * kShadowBytes, cudaMemcpyHostToDevice));
+    }
+    if (rrows) {
+        std::vector<__half> hk(rrows * d), hv(rrows * d);
+        for (size_t i = 0; i < hk.size(); ++i) {
+            hk[i] = __float2half_rn(res_k[i]);
+            hv[i] = __float2half_rn(res_v[i]);
+        }
+        CK(cudaMemcpy(c->d_res_k + (size_t)u * c->n_r * c->d, hk.data(), hk.size() * 2, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(c->d_res_v + (size_t)u * c->n_r * c->d, hv.data(), hv.size() * 2, cudaMemcpyHostToDevice));
+    }
+    c->n_prefill[u] = n_prefill;
+    c->n_pages[u] = n_pages;
+    c->n_blocks[u] = nb;
+    c->n_res[u] = (int)rrows;
+    CK(c->upload_meta(u, 1, 0));
+    CK(cudaDeviceSynchronize());
+    return MKV_OK;
+}
+
+// ---------------------------------------------------------------------------
 // synthetic inputs
 // ---------------------------------------------------------------------------
 int mkv_synth_fp16(void* out, int64_t n, uint64_t seed, uint64_t stream_id, void* stream) {

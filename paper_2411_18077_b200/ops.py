@@ -14,6 +14,7 @@ DomainError, std::runtime_error -> RuntimeFailure, std::out_of_range -> OutOfRan
 from __future__ import annotations
 
 import ctypes as C
+import os
 import math
 from dataclasses import dataclass
 from typing import Optional, Sequence
@@ -280,6 +281,14 @@ class KVCache:
         check(lib().mkv_cache_export_reference(self.h, unit, which, words.ctypes.data, params.ctypes.data,
                                                br.ctypes.data), "export")
         return words[:nw.value], params[:2 * npar.value].reshape(-1, 2), br[:nb.value]
+
+    def save_mkvc(self, unit: int, path: str):
+        """save_cache (snapshot.cpp:71-198): the unit as a reference MKVC v1 file."""
+        check(lib().mkv_cache_save_mkvc(self.h, unit, os.fsencode(path)), "save_cache")
+
+    def load_mkvc(self, unit: int, path: str):
+        """load_cache (snapshot.cpp:159-198) into unit `unit` (pages rebuilt on the device)."""
+        check(lib().mkv_cache_load_mkvc(self.h, unit, os.fsencode(path)), "load_cache")
 
     def export_residual(self, unit: int):
         import numpy as np
