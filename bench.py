@@ -228,12 +228,7 @@ def run_mkv(args, rank, world):
             do_step(s)
         ev1.record(stream)
         torch.cuda.synchronize()
-    ms = ev0.elapsed_time(ev1)
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = dist_max(ev0.elapsed_time(ev1), world)
     ms_per_step = ms / args.steps
     bytes_timed = sum(step_bytes(s) for s in range(args.warmup, steps_total))
     tokens_per_s = world * B * args.steps / (ms / 1e3)
@@ -314,7 +309,7 @@ def run_mkv(args, rank, world):
         if s >= 1:
             out_read[(s - 1) % 2].synchronize()  # the host reads step s-1's result
     out_read[(e2e_steps - 1) % 2].synchronize()
-    e2e_s = time.perf_counter() - t0
+    e2e_s = dist_max(time.perf_counter() - t0, world)
     res["e2e"] = dict(value=world * B * e2e_steps / e2e_s, unit=UNIT,
                       h2d_bytes_per_step=int(dq[0].numel() * 2 + dk[0].numel() * 2 + dv[0].numel() * 2),
                       d2h_bytes_per_step=int(dout[0].numel() * 2),
@@ -433,6 +428,18 @@ def cpu_reference_decode(steps, warmup, threads=None, sample_units_per_layer=4, 
             "sample_step_s": t_sample, "setup_s": setup}
 
 
+def dist_max(x: float, world: int) -> float:
+    """Max of a per-rank scalar over all ranks (device timings are max-over-ranks)."""
+    if world <= 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    dev = "cpu" if dist.get_backend() == "gloo" else "cuda"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", "0"))
@@ -440,8 +447,10 @@ def main():
     if world > 1 and args.impl == "mkv":
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
-        dist.init_process_group("nccl")
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")) % max(torch.cuda.device_count(), 1))
+        # NCCL for the barrier / max-over-ranks reduction; MKV_DIST_BACKEND=gloo lets several
+        # ranks share one GPU (the 1-GPU validation of the N > 1 path)
+        dist.init_process_group(os.environ.get("MKV_DIST_BACKEND", "nccl"))
     hbm_peak, bf16_peak, bf16_sust, peak_kind = load_peaks()
     cfg_desc = {"workload": "Llama-3-8B GQA decode, 32 layers, 32q/8kv heads, d=128, 32K context, "
                             "20% pyramid budget (10% HH depth-7 + 10% RW), n_r=128, group=16",
