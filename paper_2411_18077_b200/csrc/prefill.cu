@@ -19,6 +19,8 @@
 // Warp roles (192 threads): warps 0-3 softmax / exp (thread = TMEM lane = row),
 // warp 4 TMA producer, warp 5 TMEM allocator + single-thread MMA issuer.
 #include <cudaTypedefs.h>
+#include <stdio.h>
+#include <stdlib.h>
 
 #include "mkv_kernels.h"
 #include "mkv_sm100.cuh"
@@ -38,6 +40,12 @@ constexpr uint32_t kIdescPV = idesc_f16(128, 128, true);   // O += P[K-major] * 
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr float kRescaleThreshold = 8.0f;  // lazy rescale (log2 units): P <= 2^8 in fp16
+
+// slot c of every 8 exponentials runs on the FMA pipe when it is one of kPoly spread slots
+template <int kPoly>
+__host__ __device__ constexpr bool poly_slot(int c) {
+    return kPoly <= 0 ? false : ((c & 7) * kPoly) % 8 + kPoly >= 8;
+}
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
     return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
@@ -77,6 +85,7 @@ struct FwdBars {
 constexpr int kFwdThreads = 320;  // warps 0-3 softmax A, 4-7 softmax B, 8 TMA, 9 MMA
 constexpr int kFwdSmem = 6 * kTileB + 1024 + 256;  // Q[2], K[2], V[2] + alignment slack + barriers
 
+template <int kPoly>
 __global__ void __launch_bounds__(kFwdThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                     const __grid_constant__ CUtensorMap tv, const PrefillAttnParams P) {
@@ -249,8 +258,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 #pragma unroll
             for (int cc = 0; cc < 128; cc += 2) {
                 const float a0 = fmaf(__uint_as_float(x[cc]), sl2, -m), a1 = fmaf(__uint_as_float(x[cc + 1]), sl2, -m);
-                const float p0 = ((cc & 7) == 6) ? exp2_fma(a0) : fast_exp2(a0);
-                const float p1 = fast_exp2(a1);
+                const float p0 = poly_slot<kPoly>(cc) ? exp2_fma(a0) : fast_exp2(a0);
+                const float p1 = poly_slot<kPoly>(cc + 1) ? exp2_fma(a1) : fast_exp2(a1);
                 ls += p0 + p1;
                 x[cc >> 1] = pack_half2(p0, p1);
             }
@@ -321,6 +330,10 @@ struct AcBars {
 };
 constexpr int kAcSmem = (1 + kQStages) * kTileB + 1024 + (int)sizeof(AcBars) + 64;
 
+// kPoly of every 8 exponentials run as a polynomial on the FMA pipe (the rest on MUFU):
+// per element the pass costs 1 exp + ~2 FMA-pipe ops, so splitting the exponentials
+// balances the two pipes.
+template <int kPoly>
 __global__ void __launch_bounds__(kAcThreads, 1)
     acumul_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                   const PrefillAttnParams P) {
@@ -404,16 +417,22 @@ __global__ void __launch_bounds__(kAcThreads, 1)
         const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16) + 128 * wg;
         const float sl2 = P.scale * kLog2e;
         float acc = 0.0f;
+        // the LSE of the query row this thread stages is loaded one item ahead (its global
+        // latency then hides behind the previous item's exponentials)
+        auto load_lse = [&](int item) -> float {
+            if (item >= n_items) return INFINITY;
+            const int g = item / per_head, t = t_first + item % per_head;
+            const int i = t * kTile + kr;
+            return (i < P.lq) ? __ldg(P.lse + ((size_t)b * P.hq + hk * G + g) * P.lq + i) * kLog2e : INFINITY;
+        };
+        float lse_next = load_lse(wg);
         for (int it = wg; it < n_items; it += 2) {
-            const int g = it / per_head, t = t_first + it % per_head;
-            const int hq = hk * G + g;
+            const int t = t_first + it % per_head;
             const int k = it >> 1;  // use count of this TMEM buffer
             float* l2 = B.lse2[wg][k & 1];
-            {
-                const int i = t * kTile + kr;
-                l2[kr] = (i < P.lq) ? P.lse[((size_t)b * P.hq + hq) * P.lq + i] * kLog2e : INFINITY;
-            }
+            l2[kr] = lse_next;
             named_bar_sync(1 + wg, 128);
+            lse_next = load_lse(it + 2);
             mbar_wait(&B.s_full[wg], k & 1);
             tc_fence_after();
             // query i = t*128 + c visible iff kj <= offset + i  <=>  c >= kj - offset - t*128
@@ -434,14 +453,14 @@ __global__ void __launch_bounds__(kAcThreads, 1)
 #pragma unroll
                     for (int c = 0; c < 64; ++c) {
                         const float v = fmaf(__uint_as_float(x[c]), sl2, -l2[64 * half + c]);
-                        part += (c & 3) == 3 ? exp2_fma(v) : fast_exp2(v);
+                        part += poly_slot<kPoly>(c) ? exp2_fma(v) : fast_exp2(v);
                     }
                 } else {
 #pragma unroll
                     for (int c = 0; c < 64; ++c) {
                         const int col = 64 * half + c;
                         const float v = fmaf(__uint_as_float(x[c]), sl2, -l2[col]);
-                        const float e = (c & 3) == 3 ? exp2_fma(v) : fast_exp2(v);
+                        const float e = poly_slot<kPoly>(c) ? exp2_fma(v) : fast_exp2(v);
                         part += (col >= c_min) ? e : 0.0f;
                     }
                 }
@@ -490,26 +509,45 @@ bool make_map(CUtensorMap* m, const __half* base, int64_t sb, int64_t sh, int64_
 
 }  // namespace
 
+template <int KF, int KA>
+static cudaError_t launch_prefill_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                                   const PrefillAttnParams& p, cudaStream_t s) {
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel<KF>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFwdSmem);
+        if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(acumul_kernel<KA>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAcSmem);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    const int n_qt = (p.lq + kTile - 1) / kTile, n_kt = (p.lk + kTile - 1) / kTile;
+    attn_fwd_kernel<KF><<<dim3((n_qt + 1) / 2, p.hq, p.batch), kFwdThreads, kFwdSmem, s>>>(tq, tk, tv, p);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    acumul_kernel<KA><<<dim3(n_kt, p.hkv, p.batch), kAcThreads, kAcSmem, s>>>(tq, tk, p);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_prefill_attn(const PrefillAttnParams& p, cudaStream_t s) {
     CUtensorMap tq, tk, tv;
     if (!make_map(&tq, p.q, p.q_sb, p.q_sh, p.q_st, p.lq, p.hq, p.batch) ||
         !make_map(&tk, p.k, p.k_sb, p.k_sh, p.k_st, p.lk, p.hkv, p.batch) ||
         !make_map(&tv, p.v, p.v_sb, p.v_sh, p.v_st, p.lk, p.hkv, p.batch))
         return cudaErrorInvalidValue;
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFwdSmem);
-        if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(acumul_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kAcSmem);
-        if (e != cudaSuccess) return e;
-        configured = true;
+    // exponentials per 8 on the FMA pipe (fwd, A_cumul); MKV_PREFILL_POLY="f,a" selects a variant
+    static int kf = 1, ka = 2;
+    static bool parsed = false;
+    if (!parsed) {
+        if (const char* e = getenv("MKV_PREFILL_POLY")) sscanf(e, "%d,%d", &kf, &ka);
+        parsed = true;
     }
-    const int n_qt = (p.lq + kTile - 1) / kTile, n_kt = (p.lk + kTile - 1) / kTile;
-    attn_fwd_kernel<<<dim3((n_qt + 1) / 2, p.hq, p.batch), kFwdThreads, kFwdSmem, s>>>(tq, tk, tv, p);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    acumul_kernel<<<dim3(n_kt, p.hkv, p.batch), kAcThreads, kAcSmem, s>>>(tq, tk, p);
-    return cudaGetLastError();
+    if (kf == 1 && ka == 2) return launch_prefill_t<1, 2>(tq, tk, tv, p, s);
+    if (kf == 1 && ka == 3) return launch_prefill_t<1, 3>(tq, tk, tv, p, s);
+    if (kf == 1 && ka == 4) return launch_prefill_t<1, 4>(tq, tk, tv, p, s);
+    if (kf == 2 && ka == 3) return launch_prefill_t<2, 3>(tq, tk, tv, p, s);
+    if (kf == 2 && ka == 2) return launch_prefill_t<2, 2>(tq, tk, tv, p, s);
+    if (kf == 0 && ka == 2) return launch_prefill_t<0, 2>(tq, tk, tv, p, s);
+    return launch_prefill_t<1, 2>(tq, tk, tv, p, s);
 }
 
 }  // namespace mkv
