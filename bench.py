@@ -374,6 +374,29 @@ def run_prefill_bench(args):
     out["pack_ms"] = t3
     out["pack_gbs"] = Hkv * n_kept * (4 * d + 4 + d) / (t3 / 1e3) / 1e9
     cache.close()
+    # configs[3] budget sweep: total budget 10..50%, split evenly between HH and RW
+    sweep = []
+    for frac in (0.10, 0.20, 0.30, 0.40, 0.50):
+        hh = rw = int(math.floor(frac / 2 * L))
+        c2 = mkv.KVCache(Hkv, hh + rw, 0)
+        kept, nk = mkv.select_token_counts(ac, hh, rw)
+        c2.prefill_kept(kk, vv, kept, nk)
+        torch.cuda.synchronize()
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        e[0].record()
+        for _ in range(3):
+            kept, nk = mkv.select_token_counts(ac, hh, rw)
+        e[1].record()
+        for _ in range(3):
+            c2.prefill_kept(kk, vv, kept, nk)
+        e[2].record()
+        torch.cuda.synchronize()
+        ts, tp = e[0].elapsed_time(e[1]) / 3, e[1].elapsed_time(e[2]) / 3
+        sweep.append({"budget": frac, "kept_per_kv_head": hh + rw, "select_ms": round(ts, 4), "pack_ms": round(tp, 4),
+                      "pack_gbs": round(Hkv * (hh + rw) * (4 * d + 4 + d) / (tp / 1e3) / 1e9, 1),
+                      "cache_bytes": int(Hkv * (hh + rw) * d)})
+        c2.close()
+    out["budget_sweep"] = sweep
     return out
 
 

@@ -171,18 +171,42 @@ __device__ __forceinline__ bool quantize_group16(const float* v, int n, uint8_t*
         hi = (hi < x) ? x : hi;
     }
     const float sc = __fdiv_rn(__fsub_rn(hi, lo), 3.0f);
-    // q = roundf((v - lo) / sc) with the IEEE quotient.  The quotient is computed with a
-    // reciprocal multiply (|error| < 1e-6 on [0, 3]); only when that lands within 1e-4 of a
-    // half-integer -- where rounding could differ -- is the exact division evaluated.  The
-    // resulting codes are identical to the reference's for every input.
-    const float rcp = __frcp_rn(sc);
+    // code = round_half_away(fl(fl(v - lo) / sc)), clamped to [0, 3].  fl(dv / sc) is
+    // monotone in dv, so code = #{k in 1..3 : dv >= T_k} with T_k the smallest float whose
+    // IEEE quotient reaches k - 0.5.  Each T_k is found next to fl((k - 0.5) * sc) with a
+    // couple of exact divisions; then every value costs one subtraction and three compares.
+    // Identical codes to the reference for every input (per-value exact fallback if a
+    // threshold search does not settle, which no finite scale triggers).
+    bool thr_ok = sc > 0.0f && isfinite(sc);
+    float T[3] = {0.0f, 0.0f, 0.0f};
+    if (thr_ok) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const float c = static_cast<float>(k) + 0.5f;
+            float x = __fmul_rn(c, sc);
+            int guard = 0;
+            if (__fdiv_rn(x, sc) >= c) {
+                for (;;) {
+                    const float pv = nextafterf(x, 0.0f);
+                    if (pv == x || __fdiv_rn(pv, sc) < c || ++guard > 8) break;
+                    x = pv;
+                }
+            } else {
+                do {
+                    x = nextafterf(x, INFINITY);
+                } while (__fdiv_rn(x, sc) < c && ++guard <= 8);
+            }
+            thr_ok &= guard <= 8;
+            T[k] = x;
+        }
+    }
     for (int i = 0; i < n; ++i) {
         uint8_t c = 0;
-        if (sc > 0.0f) {
+        if (thr_ok) {
             const float dv = __fsub_rn(v[i], lo);
-            float q = __fmul_rn(dv, rcp);
-            const float fr = q - floorf(q);
-            if (fabsf(fr - 0.5f) < 1e-4f) q = __fdiv_rn(dv, sc);
+            c = static_cast<uint8_t>((dv >= T[0]) + (dv >= T[1]) + (dv >= T[2]));
+        } else if (sc > 0.0f) {
+            float q = __fdiv_rn(__fsub_rn(v[i], lo), sc);
             q = roundf(q);
             c = static_cast<uint8_t>(q < 0.0f ? 0.0f : (q > 3.0f ? 3.0f : q));
         }

@@ -163,7 +163,7 @@ def test_synth_matches_oracle(mkv):
         np.testing.assert_array_equal(u[r], oracle.port().synth_uniform(SEED, 99 + r, 500))
 
 
-@pytest.mark.parametrize("kind", ["half_points", "tiny_range", "huge_range", "constant_rows"])
+@pytest.mark.parametrize("kind", ["half_points", "tiny_range", "huge_range", "constant_rows", "near_thresholds"])
 def test_quantizer_rounding_edges_bit_exact(mkv, kind):
     """Quotients on/near the .5 rounding points, tiny and huge group ranges, constant groups:
     codes and params must equal the reference's exact fp32 arithmetic (quantizer.cpp:28-53)."""
@@ -175,6 +175,19 @@ def test_quantizer_rounding_edges_bit_exact(mkv, kind):
         k = (1000.0 + rng.integers(0, 4, (1, L, d)) * 0.5).astype(np.float16)
     elif kind == "huge_range":
         k = (rng.standard_normal((1, L, d)) * 3000.0).astype(np.float16)
+    elif kind == "near_thresholds":  # values at (j + 0.5) / 3 of the range, nudged by +-1, 2 fp16 ulps
+        base = rng.standard_normal((1, L, d)).astype(np.float16)
+        span = np.abs(rng.standard_normal((1, 1, d))).astype(np.float16) + np.float16(0.25)
+        frac = rng.choice(np.array([0.0, 0.5 / 3, 1.5 / 3, 2.5 / 3, 1.0], np.float32), (1, L, d))
+        k = (base * 0 + (span * frac)).astype(np.float16)
+        k[:, ::16] = np.float16(0.0)   # every 16-token group holds its minimum ...
+        k[:, 1::16] = span             # ... and its maximum
+        nudge = rng.integers(-2, 3, (1, L, d)).astype(np.int16)
+        bits = k.view(np.int16) + nudge * (rng.random((1, L, d)) < 0.5)
+        bits[:, ::16] = k.view(np.int16)[:, ::16]
+        bits[:, 1::16] = k.view(np.int16)[:, 1::16]
+        k = bits.astype(np.int16).view(np.float16)
+        k[~np.isfinite(k)] = np.float16(0.0)
     else:
         k = np.repeat(rng.standard_normal((1, L, 1)).astype(np.float16), d, axis=2)
     v = k[:, ::-1].copy()
