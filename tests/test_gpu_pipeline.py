@@ -1,0 +1,28 @@
+"""Toy end-to-end pipeline on the B200 path (pipeline.cpp:65-235):
+K1 prefill -> per-layer variance -> budget policy -> K2 + K3 -> multi-layer K4 decode,
+against a full-precision keep-all pipeline run side by side (the reference's
+deviation trace; cf. test_cache_engine.cpp:192-218: 0 < max_dev < 1)."""
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("policy", ["uniform", "pyramid", "var_prop", "var_inv"])
+def test_toy_pipeline_policies(policy):
+    from paper_2411_18077_b200.pipeline import RunConfig, run_from_config
+    cfg = RunConfig(seed=5, layers=3, n_heads=2, l_prompt=300, steps=140, alpha_hh=0.2, alpha_rw=0.1,
+                    policy=policy, n_r=128)
+    t = run_from_config(cfg)
+    mean_hh, rw = int(0.2 * 300), int(0.1 * 300)
+    assert len(t.layers) == 3 and len(t.decode) == 140 and len(t.per_layer_a_cumul) == 3
+    if policy == "uniform":
+        assert t.per_layer_hh == [mean_hh] * 3
+    if policy.startswith("var"):
+        assert sum(t.per_layer_hh) == 3 * mean_hh
+    for e, hh in zip(t.layers, t.per_layer_hh):
+        assert e["kept_tokens"] == 2 * min(hh + rw, 300)
+        assert 0 < e["bytes_after"] < e["bytes_before"]
+    assert 0.0 < t.max_abs_dev < 1.0  # 2-bit decode tracks the fp pipeline
+    assert t.analytic_dev_bound > 0.0
+    for a in t.per_layer_a_cumul:  # head-averaged A_cumul columns sum to l_prompt
+        assert abs(float(a.sum()) - 300) < 0.5
