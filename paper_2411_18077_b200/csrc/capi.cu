@@ -102,6 +102,7 @@ struct mkv_cache {
     float* d_part_ml = nullptr;
     float* d_part_o = nullptr;
     uint64_t* d_trace = nullptr;  // diagnostics only (MKV_DECODE_TRACE)
+    uint64_t trace_seq = 0;
     int part_slots = 0;
     std::unordered_map<uint64_t, Plan> plans;  // key: (unit_begin, n_units)
 
@@ -515,6 +516,19 @@ static int get_plan(mkv_cache* c, int ub, int n, cudaStream_t s, Plan** out) {
     return MKV_OK;
 }
 
+// Diagnostics (MKV_DECODE_TRACE): two alternating slots (consecutive decode calls), each
+// [page-kernel warps x 4 stamps][finish CTAs x 4 stamps] of globaltimer values.
+static size_t trace_slot_words() { return 4 * ((size_t)num_sms() * kMaxPagesWarps + kTraceFinishCtas); }
+static uint64_t* trace_slot(mkv_cache* c) {
+    static const bool tracing = getenv("MKV_DECODE_TRACE") != nullptr;
+    if (!tracing) return nullptr;
+    if (!c->d_trace) {
+        if (cudaMalloc(&c->d_trace, sizeof(uint64_t) * 2 * trace_slot_words()) != cudaSuccess) return nullptr;
+        cudaMemset(c->d_trace, 0, sizeof(uint64_t) * 2 * trace_slot_words());
+    }
+    return c->d_trace + (c->trace_seq & 1) * trace_slot_words();
+}
+
 static void fill_pages_params(mkv_cache* c, const Plan* pl, const mkv_decode_args* a, PagesParams& pp) {
     pp.pool = c->d_pool; pp.meta = c->d_meta; pp.unit_begin = a->unit_begin; pp.n_units = a->n_units;
     pp.group = a->group; pp.q = static_cast<const __half*>(a->q);
@@ -522,12 +536,7 @@ static void fill_pages_params(mkv_cache* c, const Plan* pl, const mkv_decode_arg
     pp.n_warps = pl->grid * pages_config().warps;
     pp.part_ml = c->d_part_ml; pp.part_o = c->d_part_o;
     pp.scale_log2 = a->scale * 1.4426950408889634f;
-    pp.trace = nullptr;
-    static const bool tracing = getenv("MKV_DECODE_TRACE") != nullptr;
-    if (tracing) {  // per-warp timeline of the most recent page kernel (mkv_debug_decode_trace)
-        if (!c->d_trace) cudaMalloc(&c->d_trace, sizeof(uint64_t) * 4 * num_sms() * kMaxPagesWarps);
-        pp.trace = c->d_trace;
-    }
+    pp.trace = trace_slot(c);
 }
 
 static int decode_impl(mkv_cache* c, const mkv_decode_args* a, bool attend, cudaStream_t s) {
@@ -573,6 +582,7 @@ static int decode_impl(mkv_cache* c, const mkv_decode_args* a, bool attend, cuda
     rp.part_ml = c->d_part_ml; rp.part_o = c->d_part_o; rp.out = static_cast<__half*>(a->out);
     rp.scale_log2 = a->scale * 1.4426950408889634f;
     rp.status = c->d_status;
+    rp.trace = nullptr;
     // flush steps (or append-only calls): append (+ quantize the full block) before the page pass
     if (append && (any_flush || !attend)) {
         CK(launch_append(rp, s));
@@ -587,7 +597,10 @@ static int decode_impl(mkv_cache* c, const mkv_decode_args* a, bool attend, cuda
         fill_pages_params(c, pl, a, pp);
         CK(launch_pages(pp, pl->grid, s));
     }
+    rp.trace = trace_slot(c);
+    if (rp.trace) rp.trace += 4 * (size_t)num_sms() * kMaxPagesWarps;
     CK(launch_finish(rp, pl->d_pref, std::max(pl->chunk, 1), pl->total > 0, s));
+    ++c->trace_seq;
     return MKV_OK;
 }
 
@@ -595,7 +608,7 @@ int mkv_debug_decode_trace(const mkv_cache* c, uint64_t* out, int max_words) {
     if (!c || !out) return fail(MKV_ERR_INVALID_ARGUMENT, "trace: null");
     if (!c->d_trace) return fail(MKV_ERR_RUNTIME, "trace: run with MKV_DECODE_TRACE set");
     CK(cudaDeviceSynchronize());
-    const int n = std::min(max_words, 4 * num_sms() * kMaxPagesWarps);
+    const int n = (int)std::min<size_t>(max_words, 2 * trace_slot_words());
     CK(cudaMemcpy(out, c->d_trace, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost));
     return n;
 }

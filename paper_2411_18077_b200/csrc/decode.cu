@@ -538,6 +538,14 @@ __global__ void __launch_bounds__(kFinishThreads, 2) finish_kernel(const Residua
     const int h0 = 2 * tig, h1 = 2 * tig + 1;
     // the next layer's page kernel may start its prologue and first page loads on SMs this
     // grid leaves free (it reads nothing this kernel writes before its own griddepcontrol.wait)
+    auto fstamp = [&](int k) {
+        if (P.trace != nullptr && tid == 0 && i < kTraceFinishCtas) {
+            uint64_t t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            P.trace[(size_t)i * 4 + k] = t;
+        }
+    };
+    fstamp(0);
     if (tid == 0) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 
     // ---- residual attention (overlaps the page kernel): warp w owns tiles w, w + 4 ----
@@ -642,7 +650,9 @@ __global__ void __launch_bounds__(kFinishThreads, 2) finish_kernel(const Residua
     }
     if (app && tid == 0) P.meta[u].n_res = n;  // only this CTA reads this unit's n_res after the append
     // ---- the page partials are complete past this point ----
+    fstamp(1);
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    fstamp(2);
     __syncthreads();  // residual warp partials visible
     // Single-round merge: every thread loads (m, l, o) of up to 16 page partials at once and
     // folds them with an online max (no global-max pass, no further barriers).
@@ -692,6 +702,8 @@ __global__ void __launch_bounds__(kFinishThreads, 2) finish_kernel(const Residua
         const float li = 1.0f / L;
         reinterpret_cast<__half2*>(P.out + ((size_t)i * G + h) * d)[c2] = __floats2half2_rn(ax * li, ay * li);
     }
+    __syncthreads();
+    fstamp(3);
 }
 
 cudaError_t launch_finish(const ResidualParams& p, const int32_t* pref, int chunk, bool after_pages, cudaStream_t s) {

@@ -59,7 +59,9 @@ struct ResidualParams {
     __half* out;          // [n_units][G][d]
     float scale_log2;
     uint32_t* status;
+    uint64_t* trace;      // diagnostics: per CTA {start, residual done, wait released, end}, or null
 };
+constexpr int kTraceFinishCtas = 8192;  // finish-kernel CTAs recorded per trace slot
 cudaError_t launch_append(const ResidualParams& p, cudaStream_t s);
 cudaError_t launch_finish(const ResidualParams& p, const int32_t* pref, int chunk, bool after_pages, cudaStream_t s);
 

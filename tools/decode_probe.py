@@ -76,19 +76,31 @@ for fn, name in ((attend, "attend-only"), (step, "append+attend")):
 if os.environ.get("MKV_DECODE_TRACE"):
     import numpy as np
     W = int(os.environ.get("MKV_PAGES_CFG", "12x2").split("x")[0])
-    for l in range(min(NL, 4)):
-        cache.decode_step(q[l], None, None, scale, unit_begin=l * upl, out=out[l])
-        torch.cuda.synchronize()
-        buf = np.zeros(4 * 148 * 12, np.uint64)
-        _capi.lib().mkv_debug_decode_trace(cache.h, buf.ctypes.data, buf.size)
-        t = buf.reshape(-1, 4).astype(np.int64)
-        nw = int((t[:, 1] > 0).sum())
-        t = t[:nw]
-        t0 = t[:, 0].min()
-        done = (t[:, 2] - t0) / 1e3
-        tc = done[:(nw // W) * W].reshape(-1, W)
-        rel = tc - np.median(tc, 1, keepdims=True)
-        q_ = lambda a: " ".join(f"{np.percentile(a, p):6.2f}" for p in (0, 10, 50, 90, 100))
-        print(f"layer {l}: warps {nw}; done [us] pct 0/10/50/90/100: {q_(done)}")
-        print("  intra-CTA spread median %.2f p90 %.2f" % (np.median(np.ptp(tc, 1)), np.percentile(np.ptp(tc, 1), 90)))
-        print("  mean (done - CTA median) by warp index:", " ".join(f"{x:5.2f}" for x in rel.mean(0)))
+    attend()  # one multi-layer call: the last two layers' timelines are in the two slots
+    torch.cuda.synchronize()
+    n = 2 * 4 * (148 * 12 + 8192)
+    buf = np.zeros(n, np.uint64)
+    got = _capi.lib().mkv_debug_decode_trace(cache.h, buf.ctypes.data, n)
+    slot = got // 2
+    pw = 4 * 148 * 12
+    lay = []
+    for sidx in range(2):
+        t = buf[sidx * slot:(sidx + 1) * slot].astype(np.int64)
+        pg = t[:pw].reshape(-1, 4)
+        pg = pg[pg[:, 1] > 0]
+        fn = t[pw:].reshape(-1, 4)
+        fn = fn[fn[:, 0] > 0]
+        lay.append((pg, fn))
+    order = sorted(range(2), key=lambda i: lay[i][0][:, 0].min())
+    t0 = lay[order[0]][0][:, 0].min()
+    q_ = lambda a: " ".join(f"{(np.percentile(a, p) - t0) / 1e3:7.2f}" for p in (0, 50, 100))
+    for name, i in (("layer n-2", order[0]), ("layer n-1", order[1])):
+        pg, fn = lay[i]
+        print(f"{name}: page kernel warps {len(pg)}, finish CTAs {len(fn)}   [us from layer n-2 start: min/median/max]")
+        print("  pages start      ", q_(pg[:, 0]))
+        print("  pages after wait ", q_(pg[:, 1]))
+        print("  pages done       ", q_(pg[:, 2]))
+        print("  finish start     ", q_(fn[:, 0]))
+        print("  finish resid done", q_(fn[:, 1]))
+        print("  finish wait rel. ", q_(fn[:, 2]))
+        print("  finish end       ", q_(fn[:, 3]))
