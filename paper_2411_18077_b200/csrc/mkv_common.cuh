@@ -162,55 +162,56 @@ __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 // Returns false if a value is non-finite (the reference throws std::domain_error).
 __device__ __forceinline__ bool quantize_group16(const float* v, int n, uint8_t* codes,
                                                  float* scale_out, float* zero_out) {
+    // fixed 16-trip loops (entries past n are ignored / produce unused codes): the value and
+    // code arrays stay in registers instead of local memory
     float lo = v[0], hi = v[0];
     bool finite = true;
-    for (int i = 0; i < n; ++i) {
-        const float x = v[i];
-        finite &= isfinite(x);
-        lo = (x < lo) ? x : lo;
-        hi = (hi < x) ? x : hi;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        if (i < n) {
+            const float x = v[i];
+            finite &= isfinite(x);
+            lo = (x < lo) ? x : lo;
+            hi = (hi < x) ? x : hi;
+        }
     }
     const float sc = __fdiv_rn(__fsub_rn(hi, lo), 3.0f);
     // code = round_half_away(fl(fl(v - lo) / sc)), clamped to [0, 3].  fl(dv / sc) is
     // monotone in dv, so code = #{k in 1..3 : dv >= T_k} with T_k the smallest float whose
-    // IEEE quotient reaches k - 0.5.  Each T_k is found next to fl((k - 0.5) * sc) with a
-    // couple of exact divisions; then every value costs one subtraction and three compares.
-    // Identical codes to the reference for every input (per-value exact fallback if a
-    // threshold search does not settle, which no finite scale triggers).
-    bool thr_ok = sc > 0.0f && isfinite(sc);
+    // IEEE quotient reaches c = k - 0.5.  fl(y) >= c  <=>  y > m  or  (y == m and c has an
+    // even mantissa -- 0.5, 1.5, 2.5 all do), m = the midpoint of c and its predecessor, so
+    // T_k = the smallest float >= m * sc, where m * sc (25 x 24 significant bits) is exact
+    // in double.  Per group: three double products; per value: one subtraction and three
+    // compares.  Identical codes to the reference's division for every finite input.
+    const bool thr_ok = sc > 0.0f && isfinite(sc);
     float T[3] = {0.0f, 0.0f, 0.0f};
     if (thr_ok) {
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
             const float c = static_cast<float>(k) + 0.5f;
-            float x = __fmul_rn(c, sc);
-            int guard = 0;
-            if (__fdiv_rn(x, sc) >= c) {
-                for (;;) {
-                    const float pv = nextafterf(x, 0.0f);
-                    if (pv == x || __fdiv_rn(pv, sc) < c || ++guard > 8) break;
-                    x = pv;
-                }
-            } else {
-                do {
-                    x = nextafterf(x, INFINITY);
-                } while (__fdiv_rn(x, sc) < c && ++guard <= 8);
-            }
-            thr_ok &= guard <= 8;
+            const double m = 0.5 * (static_cast<double>(nextafterf(c, 0.0f)) + static_cast<double>(c));
+            const double prod = m * static_cast<double>(sc);  // exact
+            float x = __double2float_rn(prod);
+            if (static_cast<double>(x) < prod) x = nextafterf(x, INFINITY);
             T[k] = x;
         }
     }
-    for (int i = 0; i < n; ++i) {
-        uint8_t c = 0;
-        if (thr_ok) {
+    if (thr_ok) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
             const float dv = __fsub_rn(v[i], lo);
-            c = static_cast<uint8_t>((dv >= T[0]) + (dv >= T[1]) + (dv >= T[2]));
-        } else if (sc > 0.0f) {
-            float q = __fdiv_rn(__fsub_rn(v[i], lo), sc);
-            q = roundf(q);
-            c = static_cast<uint8_t>(q < 0.0f ? 0.0f : (q > 3.0f ? 3.0f : q));
+            codes[i] = static_cast<uint8_t>((dv >= T[0]) + (dv >= T[1]) + (dv >= T[2]));
         }
-        codes[i] = c;
+    } else {  // scale 0 (constant group) -> codes 0; non-finite scale -> the reference's formula
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            uint8_t c = 0;
+            if (sc > 0.0f) {
+                float q = roundf(__fdiv_rn(__fsub_rn(v[i], lo), sc));
+                c = static_cast<uint8_t>(q < 0.0f ? 0.0f : (q > 3.0f ? 3.0f : q));
+            }
+            codes[i] = c;
+        }
     }
     *scale_out = sc;
     *zero_out = lo;

@@ -5,19 +5,20 @@
 // values (PerToken) as ONE block of n_kept rows (quantizer.cpp:102-136).  Key
 // groups are 16 consecutive *kept* tokens; the last group of the
 // block may be short and is quantized over its own tokens only.  No gathered
-// intermediate is materialised: each warp gathers its page's 16 rows straight
-// from K/V into shared memory and writes one finished 2 KB page with 16-byte
-// coalesced stores.
+// intermediate is materialised: each warp reads its page's 16 kept rows straight
+// from K/V in global memory (keys as coalesced column runs, values as 32-byte
+// group runs), stages only the codes, and writes one finished 2 KB page with
+// 16-byte coalesced stores.
 #include "mkv_kernels.h"
 #include "mkv_page.cuh"
 
 namespace mkv {
 
-constexpr int kQuantWarps = 4;
+constexpr int kQuantWarps = 8;
 
 __global__ void __launch_bounds__(kQuantWarps * 32) prefill_pages_kernel(const PrefillPagesParams P) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
-    PageScratch* scratch = reinterpret_cast<PageScratch*>(smem_raw);
+    PageScratchLite* scratch = reinterpret_cast<PageScratchLite*>(smem_raw);
     const int warp = threadIdx.x >> 5, lane = lane_id();
     const int i = blockIdx.y;
     const int u = P.unit_begin + i;
@@ -27,30 +28,17 @@ __global__ void __launch_bounds__(kQuantWarps * 32) prefill_pages_kernel(const P
     const int pages = (n_kept + 15) >> 4;
     if (p >= pages) return;
     const int valid = min(16, n_kept - 16 * p);
-    PageScratch& s = scratch[warp];
-    const int32_t* kept = P.kept + (size_t)i * P.kept_stride + 16 * p;
-    const __half* kbase = P.k + (size_t)i * P.k_su;
-    const __half* vbase = P.v + (size_t)i * P.v_su;
-    // gather: 16 rows x 16 uint4 per tensor, 8 per lane
-#pragma unroll
-    for (int e = lane; e < 256; e += 32) {
-        const int r = e >> 4, c16 = e & 15;
-        if (r < valid) {
-            const int64_t t = __ldg(kept + r);
-            reinterpret_cast<uint4*>(s.k[r])[c16] = __ldg(reinterpret_cast<const uint4*>(kbase + t * P.k_st) + c16);
-            reinterpret_cast<uint4*>(s.v[r])[c16] = __ldg(reinterpret_cast<const uint4*>(vbase + t * P.v_st) + c16);
-        }
-    }
-    __syncwarp();
     const int64_t page = meta.page_base + p;
-    const bool ok = build_page(s, valid, P.pool + (size_t)page * kPageBytes,
-                               P.shadow ? P.shadow + (size_t)page * (kShadowBytes / 4) : nullptr);
+    const bool ok = build_page_gather(scratch[warp], valid, P.k + (size_t)i * P.k_su, P.k_st, P.v + (size_t)i * P.v_su,
+                                      P.v_st, P.kept + (size_t)i * P.kept_stride + 16 * p,
+                                      P.pool + (size_t)page * kPageBytes,
+                                      P.shadow ? P.shadow + (size_t)page * (kShadowBytes / 4) : nullptr);
     if (!ok && lane == 0) atomicOr(P.status, kStatusNonFinite);
 }
 
 cudaError_t launch_prefill_pages(const PrefillPagesParams& p, cudaStream_t s) {
     if (p.n_units == 0 || p.max_pages == 0) return cudaSuccess;
-    const size_t smem = sizeof(PageScratch) * kQuantWarps;
+    const size_t smem = sizeof(PageScratchLite) * kQuantWarps;
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(prefill_pages_kernel,
