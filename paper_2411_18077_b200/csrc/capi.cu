@@ -78,7 +78,7 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 // cache object
 // ---------------------------------------------------------------------------
 struct Plan {
-    uint64_t hash = 0;
+    std::vector<int32_t> sig;  // per unit (pages, prefill rows) the plan was built for
     int total = 0, chunk = 0, grid = 0;
     int32_t* d_pref = nullptr;    // [n_units + 1] local page prefix, then [warps] first unit per warp
     int32_t* d_wstart = nullptr;
@@ -457,20 +457,23 @@ int mkv_cache_prefill_select(mkv_cache* c, const mkv_prefill_select_args* a, voi
 // ---------------------------------------------------------------------------
 // K4 decode
 // ---------------------------------------------------------------------------
-static uint64_t range_hash(const mkv_cache* c, int ub, int n) {
-    uint64_t h = 1469598103934665603ull;
+// The plan depends on every unit's page count and prefill rows (its partial last page);
+// it is reused while that signature is unchanged (exact compare: a hash of many units'
+// counts can collide).
+static void range_signature(const mkv_cache* c, int ub, int n, std::vector<int32_t>& sig) {
+    sig.resize(2 * (size_t)n);
     for (int i = 0; i < n; ++i) {
-        h ^= (uint64_t)(uint32_t)c->n_pages[ub + i] | ((uint64_t)(uint32_t)c->n_prefill[ub + i] << 32);
-        h *= 1099511628211ull;
+        sig[2 * i] = c->n_pages[ub + i];
+        sig[2 * i + 1] = c->n_prefill[ub + i];
     }
-    return h;
 }
 
 static int get_plan(mkv_cache* c, int ub, int n, cudaStream_t s, Plan** out) {
     const uint64_t key = ((uint64_t)(uint32_t)ub << 32) | (uint32_t)n;
     Plan& pl = c->plans[key];
-    const uint64_t h = range_hash(c, ub, n);
-    if (pl.d_pref && pl.hash == h) {
+    thread_local std::vector<int32_t> sig;
+    range_signature(c, ub, n, sig);
+    if (pl.d_pref && pl.sig == sig) {
         *out = &pl;
         return MKV_OK;
     }
@@ -508,7 +511,7 @@ static int get_plan(mkv_cache* c, int ub, int n, cudaStream_t s, Plan** out) {
     pl.d_rec = reinterpret_cast<UnitRec*>(pl.d_pref + ints);
     CK(cudaMemcpyAsync(pl.d_rec, rec.data(), sizeof(UnitRec) * n, cudaMemcpyHostToDevice, s));
     pl.d_wstart = pl.d_pref + n + 1;
-    pl.hash = h;
+    pl.sig = sig;
     pl.total = total;
     pl.chunk = chunk;
     pl.grid = (warps + wpc - 1) / wpc;
