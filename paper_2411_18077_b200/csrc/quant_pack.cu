@@ -16,7 +16,7 @@ namespace mkv {
 
 constexpr int kQuantWarps = 8;
 
-__global__ void __launch_bounds__(kQuantWarps * 32) prefill_pages_kernel(const PrefillPagesParams P) {
+__global__ void __launch_bounds__(kQuantWarps * 32, 4) prefill_pages_kernel(const PrefillPagesParams P) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
     PageScratchLite* scratch = reinterpret_cast<PageScratchLite*>(smem_raw);
     const int warp = threadIdx.x >> 5, lane = lane_id();
