@@ -115,7 +115,7 @@ typedef struct mkv_cache mkv_cache;
 
 typedef struct {
     int n_units;
-    int head_dim;               /* 128 (64 also accepted) */
+    int head_dim;               /* 128 (the device layout; other values: MKV_ERR_UNSUPPORTED) */
     int n_r;                    /* residual flush period; multiple of group_size (cache_engine.cpp:13-15) */
     int group_size;             /* 16 (the only device grouping) */
     const int32_t* prefill_capacity; /* host [n_units]: max kept tokens at prefill */

@@ -2,11 +2,13 @@
 //
 // Restates selective_flash_attn (attention.cpp:29-117) for [B, H, L, 128]
 // fp16 tensors with GQA:
-//   pass 1  attn_fwd_kernel   one CTA per (128-query tile, q-head, batch):
+//   pass 1  attn_fwd_kernel   one CTA per (pair of 128-query tiles, q-head, batch):
 //           online softmax over 128-key tiles -> X_O (fp16) and LSE (fp32,
 //           natural log, attention.cpp:98).  S = Q K^T and O += P V are
-//           tcgen05.mma (M = N = 128, K = 16 steps) with operands staged by TMA
-//           (SWIZZLE_128B) and accumulators in TMEM; P goes registers -> smem.
+//           tcgen05.mma (M = N = 128, K = 16 steps) with K/V staged by TMA
+//           (SWIZZLE_128B, shared by both query tiles) and S / O in TMEM; the two
+//           tiles ping-pong (one's MMAs run under the other's softmax) and P is
+//           written back over S in TMEM as the A operand of P V (TS-MMA).
 //   pass 2  acumul_kernel     one CTA per (128-key block, kv-head, batch): the
 //           paper's column-parallel pass.  S^T = K_blk Q^T
 //           is recomputed on tcgen05 into TMEM, each thread owns ONE key row and
@@ -16,8 +18,10 @@
 // Causal convention: query i sees keys 0 .. lk - lq + i (attention.cpp:42,60);
 // masked pairs contribute exactly 0.
 //
-// Warp roles (192 threads): warps 0-3 softmax / exp (thread = TMEM lane = row),
-// warp 4 TMA producer, warp 5 TMEM allocator + single-thread MMA issuer.
+// Warp roles (320 threads): pass 1 -- warps 0-3 / 4-7 softmax of query tile A / B
+// (thread = TMEM lane = row), warp 8 TMA producer, warp 9 TMEM allocator +
+// single-thread MMA issuer; pass 2 -- warps 0-3 / 4-7 two exp warpgroups on
+// alternating query tiles (thread = key row), warp 8 TMA, warp 9 MMA.
 #include <cudaTypedefs.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -34,7 +38,6 @@ namespace {
 constexpr int kTile = 128;
 constexpr int kHalf = kTile * 128;   // one [128 rows x 64 fp16] swizzled TMA box = 16 KB
 constexpr int kTileB = 2 * kHalf;    // [128 x 128] fp16 tile = 32 KB
-constexpr int kThreads = 192;
 constexpr uint32_t kIdescS = idesc_f16(128, 128, false);   // S = A[K-major] * B[K-major]
 constexpr uint32_t kIdescPV = idesc_f16(128, 128, true);   // O += P[K-major] * V[MN-major]
 constexpr float kLog2e = 1.4426950408889634f;
