@@ -157,3 +157,20 @@ def test_append_only_cache_blocks_export_bit_exact(mkv):
         w, p, br = cache.export_reference(0, which)
         ew, ep, ebr = oc.export(which)
         assert np.array_equal(w, ew) and np.array_equal(p.reshape(-1), ep.reshape(-1)) and list(br) == list(ebr)
+
+
+@pytest.mark.parametrize("seed", [11, 12, 13])
+def test_decode_randomized_configs(mkv, seed):
+    """Randomized parity sweep: unit count, GQA group, n_r, per-unit budgets and step count
+    drawn at random (partial pages, flushes, residual-only stretches), every output checked."""
+    rng = np.random.default_rng(seed)
+    n_units = int(rng.integers(1, 24))
+    G = int(rng.choice([1, 2, 4, 8]))
+    n_r = int(rng.choice([16, 32, 64, 128]))
+    L = int(rng.integers(20, 900))
+    rw = int(rng.integers(0, L // 4 + 1))
+    hh = [int(rng.integers(0 if rw else 1, L // 3 + 2)) for _ in range(n_units)]
+    steps = int(rng.integers(1, 2 * n_r + 5))
+    worst = run_decode(mkv, n_units=n_units, G=G, L=L, hh=0, rw=rw, steps=steps, n_r=n_r,
+                       check_every=max(1, steps // 12), hh_per_unit=hh, seed=seed)
+    assert worst <= TOL, (n_units, G, n_r, L, rw, steps, worst)
