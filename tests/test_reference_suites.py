@@ -1,0 +1,47 @@
+"""The reference's own doctest suites (proj/tests/test_*.cpp, unmodified).
+
+dropin/Makefile compiles them where /root/reference exists, into oracle/_ref/suites/:
+  ref_<s>     each suite linked with the reference's own core sources.  Every case must
+              pass on the CPU -- this pins oracle/doctest_shim (the doctest subset the
+              suites use; doctest itself is vendored under proj/vendor/, absent here).
+  dropin_<s>  the suite linked through dropin/minikv_reference_adapter.cpp: the reference
+              core's hot-path symbols are weakened, so select_tokens / select_token_counts /
+              allocate_* / layer_score_variance resolve to the adapter and run on the B200
+              (libminikv_b200.so).  The selection suite is bit-exact by construction (fp32
+              score keys, lowest-index ties), so all of it must pass on the GPU.
+The binaries are prebuilt here and travel to the GPU box; nothing reads /root/reference
+at run time.  Suites needing pipeline.cpp (nlohmann/json, also un-vendored) are not built.
+"""
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SUITES = os.path.join(ROOT, "oracle", "_ref", "suites")
+
+
+def _run(name):
+    path = os.path.join(SUITES, name)
+    if not os.path.exists(path):
+        pytest.skip(f"{name} not built (needs /root/reference at build time)")
+    r = subprocess.run([path], capture_output=True, text=True, timeout=900)
+    return r.returncode, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("suite", ["selection", "quantizer", "attention", "accounting", "numerics"])
+def test_reference_suite_on_reference_core(suite):
+    code, out = _run(f"ref_{suite}")
+    assert code == 0, out[-4000:]
+    assert "0 failed" in out
+
+
+@pytest.mark.gpu
+def test_reference_selection_suite_through_dropin_adapter():
+    code, out = _run("dropin_selection")
+    assert code == 0, out[-4000:]
+    # the full suite ran (no case aborted by an exception): same assertion count as on the CPU core
+    _, ref_out = _run("ref_selection")
+    count = [ln for ln in out.splitlines() if ln.startswith("[doctest-shim] assertions")]
+    ref_count = [ln for ln in ref_out.splitlines() if ln.startswith("[doctest-shim] assertions")]
+    assert count and count == ref_count, (count, ref_count)
