@@ -10,7 +10,8 @@ dropin/Makefile compiles them where /root/reference exists, into oracle/_ref/sui
               (libminikv_b200.so).  The selection suite is bit-exact by construction (fp32
               score keys, lowest-index ties), so all of it must pass on the GPU.
 The binaries are prebuilt here and travel to the GPU box; nothing reads /root/reference
-at run time.  Suites needing pipeline.cpp (nlohmann/json, also un-vendored) are not built.
+at run time.  pipeline.cpp's <json.hpp> (nlohmann, also un-vendored) comes from the copy
+bundled with cudnn_frontend in this image.
 """
 import os
 import subprocess
@@ -29,7 +30,7 @@ def _run(name):
     return r.returncode, r.stdout + r.stderr
 
 
-@pytest.mark.parametrize("suite", ["selection", "quantizer", "attention", "accounting", "numerics"])
+@pytest.mark.parametrize("suite", ["selection", "quantizer", "attention", "accounting", "numerics", "cache_engine", "harness"])
 def test_reference_suite_on_reference_core(suite):
     code, out = _run(f"ref_{suite}")
     assert code == 0, out[-4000:]
