@@ -9,7 +9,7 @@
 //   append_kernel  (only on steps where some unit's residual fills up)
 //                  decode_append + flush of the n_r block through the K3 page
 //                  builder, so the new pages are visible to pages_kernel.
-//   pages_kernel   persistent, 12 warps/CTA, each warp an independent worker
+//   pages_kernel   persistent, 8 warps/CTA, each warp an independent worker
 //                  over a contiguous range of the global page sequence; pages
 //                  stream HBM -> smem with cp.async.bulk (2-stage ring of
 //                  4-page batches per warp), are dequantized in registers and
@@ -242,6 +242,13 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pages_kernel(const PagesParams
             const int n = min(kBatch, uend_real - cg);
             const int pfirst = cg - upre;
             mbar_wait(&bars[stage], phase);
+#ifdef MKV_AB_STREAM_ONLY  // A/B probe (tools/abbuild.sh): data movement only, no compute
+            __syncwarp();
+            issue(stage);
+            cg += kBatch;
+            if (++stage == kStages) { stage = 0; phase ^= 1u; }
+            continue;
+#endif
             const uint8_t* buf = ring + (size_t)stage * kBatch * kPageBytes;
 
             // ---- key zero-point bias: Kb[page][h] = sum_c z[page][c] q[h][c] (rows = pages) ----
@@ -407,7 +414,10 @@ static cudaError_t launch_pages_t(const PagesParams& p, int grid, cudaStream_t s
 // (warps per CTA, ring stages) of the page kernel; MKV_PAGES_CFG=WxS selects a variant
 PagesConfig pages_config() {
     static PagesConfig cfg = [] {
-        PagesConfig c{12, 2};
+        // 8 warps: the page pass is ~2% slower than with 12 (same SM sub-partition
+        // throughput) but the step is ~3% faster: a third fewer
+        // (warp, unit) partials to write and merge.
+        PagesConfig c{8, 2};
         if (const char* e = getenv("MKV_PAGES_CFG")) {
             int w = 0, s = 0;
             if (sscanf(e, "%dx%d", &w, &s) == 2 &&

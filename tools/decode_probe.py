@@ -75,7 +75,7 @@ for fn, name in ((attend, "attend-only"), (step, "append+attend")):
 
 if os.environ.get("MKV_DECODE_TRACE"):
     import numpy as np
-    W = int(os.environ.get("MKV_PAGES_CFG", "12x2").split("x")[0])
+    W = int(os.environ.get("MKV_PAGES_CFG", "8x2").split("x")[0])
     attend()  # one multi-layer call: the last two layers' timelines are in the two slots
     torch.cuda.synchronize()
     n = 2 * 4 * (148 * 12 + 8192)
