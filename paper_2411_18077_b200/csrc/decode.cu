@@ -225,6 +225,11 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pages_kernel(const PagesParams
                 qb[kc][1] = hmul2_u32(qb[kc][1], s2);
             }
         }
+        uint32_t qa[8][4];  // K-bias A operand: rows = heads (gid), k = channels, rows 8-15 zero
+#pragma unroll
+        for (int kc = 0; kc < 8; ++kc) {
+            qa[kc][0] = qb[kc][0]; qa[kc][1] = 0u; qa[kc][2] = qb[kc][1]; qa[kc][3] = 0u;
+        }
         if (seg_end < end) {
             int nu = unit + 1;
             while (rec_pend(nu) == seg_end) ++nu;
@@ -251,23 +256,23 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pages_kernel(const PagesParams
 #endif
             const uint8_t* buf = ring + (size_t)stage * kBatch * kPageBytes;
 
-            // ---- key zero-point bias: Kb[page][h] = sum_c z[page][c] q[h][c] (rows = pages) ----
+            // ---- key zero-point bias Kb^T[h][page] = sum_c q[h][c] z[page][c]: A = the unit's q
+            // fragments (built once per unit), B = z pairs straight from LDS (no fragment
+            // assembly per batch); columns are pages gid & 3 ----
             float Kb[4] = {0.0f, 0.0f, 0.0f, 0.0f}, Kb2[4] = {0.0f, 0.0f, 0.0f, 0.0f};
             {
                 uint4 z[4];
                 const uint8_t* zp = buf + (gid & (kBatch - 1)) * kPageBytes + kKZ + tig * 16;
 #pragma unroll
-                for (int j = 0; j < 4; ++j) z[j] = lds128(zp + 64 * j);  // rows >= kBatch: unused
+                for (int j = 0; j < 4; ++j) z[j] = lds128(zp + 64 * j);  // columns >= kBatch: unused
                 const uint32_t* zz = reinterpret_cast<const uint32_t*>(z);
 #pragma unroll
                 for (int kc = 0; kc < 8; kc += 2) {
-                    const uint32_t a0[4] = {zz[2 * kc], 0u, zz[2 * kc + 1], 0u};
-                    const uint32_t a1[4] = {zz[2 * kc + 2], 0u, zz[2 * kc + 3], 0u};
-                    mma_16816(Kb, a0, qb[kc][0], qb[kc][1]);
-                    mma_16816(Kb2, a1, qb[kc + 1][0], qb[kc + 1][1]);
+                    mma_16816(Kb, qa[kc], zz[2 * kc], zz[2 * kc + 1]);
+                    mma_16816(Kb2, qa[kc + 1], zz[2 * kc + 2], zz[2 * kc + 3]);
                 }
-#pragma unroll
-                for (int r = 0; r < 4; ++r) Kb[r] += Kb2[r];
+                Kb[0] += Kb2[0];
+                Kb[1] += Kb2[1];
             }
 
             // ---- scores for the 4 pages, interleaved: S[j][t][h] = sum_c code * q'' ----
@@ -296,8 +301,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pages_kernel(const PagesParams
             float mx0 = -INFINITY, mx1 = -INFINITY;
 #pragma unroll
             for (int j = 0; j < kBatch; ++j) {
-                const float kb0 = __shfl_sync(0xffffffffu, Kb[0], 4 * j + tig);
-                const float kb1 = __shfl_sync(0xffffffffu, Kb[1], 4 * j + tig);
+                // Kb^T[h][page = 2 t + e] sits in Kb[e] of lane 4 h + t
+                const float kb0 = __shfl_sync(0xffffffffu, Kb[j & 1], 8 * tig + (j >> 1));
+                const float kb1 = __shfl_sync(0xffffffffu, Kb[j & 1], 8 * tig + 4 + (j >> 1));
                 x[j][0] = fmaf(S[j][0], sk, kb0);
                 x[j][1] = fmaf(S[j][1], sk, kb1);
                 x[j][2] = fmaf(S[j][2], sk, kb0);
@@ -421,8 +427,7 @@ PagesConfig pages_config() {
         if (const char* e = getenv("MKV_PAGES_CFG")) {
             int w = 0, s = 0;
             if (sscanf(e, "%dx%d", &w, &s) == 2 &&
-                ((w == 12 && s == 2) || (w == 8 && s == 3) || (w == 10 && s == 2) || (w == 6 && s == 4) ||
-                 (w == 8 && s == 2)))
+                ((w == 12 && s == 2) || (w == 8 && s == 3) || (w == 8 && s == 2)))
                 c = PagesConfig{w, s};
         }
         return c;
@@ -433,10 +438,8 @@ PagesConfig pages_config() {
 cudaError_t launch_pages(const PagesParams& p, int grid, cudaStream_t s) {
     const PagesConfig c = pages_config();
     if (c.warps == 8 && c.stages == 3) return launch_pages_t<8, 3>(p, grid, s);
-    if (c.warps == 10 && c.stages == 2) return launch_pages_t<10, 2>(p, grid, s);
-    if (c.warps == 6 && c.stages == 4) return launch_pages_t<6, 4>(p, grid, s);
-    if (c.warps == 8 && c.stages == 2) return launch_pages_t<8, 2>(p, grid, s);
-    return launch_pages_t<12, 2>(p, grid, s);
+    if (c.warps == 12 && c.stages == 2) return launch_pages_t<12, 2>(p, grid, s);
+    return launch_pages_t<8, 2>(p, grid, s);
 }
 
 // ---------------------------------------------------------------------------
