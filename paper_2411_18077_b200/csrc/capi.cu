@@ -540,9 +540,12 @@ static void fill_pages_params(mkv_cache* c, const Plan* pl, const mkv_decode_arg
     pp.part_ml = c->d_part_ml; pp.part_o = c->d_part_o;
     pp.scale_log2 = a->scale * 1.4426950408889634f;
     pp.trace = trace_slot(c);
+    pp.early = 0;
 }
 
-static int decode_impl(mkv_cache* c, const mkv_decode_args* a, bool attend, cudaStream_t s) {
+// early: a later layer of one mkv_decode_step_layers call -- its q was written before the
+// call, so the page kernel may read it while the previous layer's finish kernel still runs
+static int decode_impl(mkv_cache* c, const mkv_decode_args* a, bool attend, cudaStream_t s, bool early = false) {
     const int ub = a->unit_begin, n = a->n_units;
     if (int r = check_range(c, ub, n)) return r;
     if (n == 0) return MKV_OK;
@@ -598,6 +601,7 @@ static int decode_impl(mkv_cache* c, const mkv_decode_args* a, bool attend, cuda
     if (pl->total > 0) {
         PagesParams pp;
         fill_pages_params(c, pl, a, pp);
+        pp.early = early && !any_flush ? 1 : 0;
         CK(launch_pages(pp, pl->grid, s));
     }
     rp.trace = trace_slot(c);
@@ -639,7 +643,7 @@ int mkv_decode_pages_only(mkv_cache* c, const mkv_decode_args* a, void* stream) 
 int mkv_decode_step_layers(mkv_cache* c, int n_layers, const mkv_decode_args* a, void* stream) {
     if (!a || n_layers < 0) return fail(MKV_ERR_INVALID_ARGUMENT, "decode_step: bad layer list");
     for (int l = 0; l < n_layers; ++l)
-        if (int r = decode_impl(c, a + l, true, static_cast<cudaStream_t>(stream))) return r;
+        if (int r = decode_impl(c, a + l, true, static_cast<cudaStream_t>(stream), l > 0)) return r;
     return MKV_OK;
 }
 

@@ -192,7 +192,12 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pages_kernel(const PagesParams
     // writes these pages (the append kernel of a flush step is a full-dependency launch)
     // or the plan/meta fields read here; q is read and partials are written after the wait.
     for (int s = 0; s < kStages; ++s) issue(s);
-    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    // P.early (every layer of a multi-layer call but the first): q is an input of the call,
+    // so the whole page pass may run while the previous layer's finish kernel is still
+    // merging; the only conflict is the partial buffers that kernel reads, so the wait
+    // moves to the first partial write.  Otherwise wait here, before touching q.
+    bool waited = !P.early;
+    if (waited) asm volatile("griddepcontrol.wait;\n" ::: "memory");
     if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     stamp(1);
     prefetch_q(ci);
@@ -378,6 +383,10 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pages_kernel(const PagesParams
             l0 += __shfl_xor_sync(0xffffffffu, l0, o);
             l1 += __shfl_xor_sync(0xffffffffu, l1, o);
         }
+        if (!waited) {  // the previous layer's finish kernel has read the partial buffers
+            asm volatile("griddepcontrol.wait;\n" ::: "memory");
+            waited = true;
+        }
         const int slot = wg + unit;
         float* pml = P.part_ml + (size_t)slot * 2 * kMaxG;
         float* po = P.part_o + (size_t)slot * kMaxG * kHeadDim;
@@ -511,7 +520,11 @@ cudaError_t launch_append(const ResidualParams& p, cudaStream_t s) {
 // Finish kernel (one CTA per unit, launched with PDL): decode_append and the exact fp16
 // residual attention first, then -- after griddepcontrol.wait -- a single-round split-K
 // merge of the residual and page partials (online max, no extra barriers).
-constexpr int kFinishWarps = 8;
+// 4 warps at <= 96 registers and 33 KB of shared memory: a finish CTA fits on an SM beside a
+// page-kernel CTA (208 x 256 registers, 141 KB), so layer l's finish runs its residual
+// attention while layer l's pages are still in flight and layer l + 1's pages overlap its merge.
+constexpr int kFinishWarps = 4;
+constexpr int kMergeBatch = 8;  // page partials folded per online-max round
 constexpr int kFinishThreads = kFinishWarps * 32;
 
 struct FinishSmem {
@@ -527,7 +540,7 @@ __device__ __forceinline__ void ldmatrix_x4_trans(uint32_t (&r)[4], const void* 
                  : "r"(smem_u32(p)));
 }
 
-__global__ void __launch_bounds__(kFinishThreads, 2) finish_kernel(const ResidualParams P, const int32_t* __restrict__ pref,
+__global__ void __launch_bounds__(kFinishThreads, 5) finish_kernel(const ResidualParams P, const int32_t* __restrict__ pref,
                                                                    int chunk) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
     FinishSmem& S = *reinterpret_cast<FinishSmem*>(smem_raw);
@@ -561,7 +574,7 @@ __global__ void __launch_bounds__(kFinishThreads, 2) finish_kernel(const Residua
     fstamp(0);
     if (tid == 0) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 
-    // ---- residual attention (overlaps the page kernel): warp w owns tiles w, w + 4 ----
+    // ---- residual attention (overlaps the page kernel): warp w owns tiles w, w + kFinishWarps, ... ----
     uint32_t qb[8][2];
 #pragma unroll
     for (int kc = 0; kc < 8; ++kc)
@@ -667,8 +680,8 @@ __global__ void __launch_bounds__(kFinishThreads, 2) finish_kernel(const Residua
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
     fstamp(2);
     __syncthreads();  // residual warp partials visible
-    // Single-round merge: every thread loads (m, l, o) of up to 16 page partials at once and
-    // folds them with an online max (no global-max pass, no further barriers).
+    // Merge: every thread loads (m, l, o) of kMergeBatch page partials at once and folds them
+    // with an online max (no global-max pass, no further barriers).
     for (int e = tid; e < G * (d / 2); e += kFinishThreads) {
         const int h = e / (d / 2), c2 = e % (d / 2);
         float M = -INFINITY, L = 0.0f, ax = 0.0f, ay = 0.0f;
@@ -685,11 +698,11 @@ __global__ void __launch_bounds__(kFinishThreads, 2) finish_kernel(const Residua
                 M = nm;
             }
         }
-        for (int p0 = 0; p0 < n_part; p0 += 16) {
-            float pm[16], pl[16];
-            float2 po[16];
+        for (int p0 = 0; p0 < n_part; p0 += kMergeBatch) {
+            float pm[kMergeBatch], pl[kMergeBatch];
+            float2 po[kMergeBatch];
 #pragma unroll
-            for (int k = 0; k < 16; ++k) {
+            for (int k = 0; k < kMergeBatch; ++k) {
                 const int slot = w_first + p0 + k + i;
                 const bool ok = p0 + k < n_part;
                 pm[k] = ok ? __ldcg(P.part_ml + (size_t)slot * 2 * kMaxG + h) : -INFINITY;
@@ -699,12 +712,12 @@ __global__ void __launch_bounds__(kFinishThreads, 2) finish_kernel(const Residua
             }
             float cm = pm[0];
 #pragma unroll
-            for (int k = 1; k < 16; ++k) cm = fmaxf(cm, pm[k]);
+            for (int k = 1; k < kMergeBatch; ++k) cm = fmaxf(cm, pm[k]);
             const float nm = fmaxf(M, cm);
             const float f = fast_exp2(M - nm);
             ax *= f; ay *= f; L *= f;
 #pragma unroll
-            for (int k = 0; k < 16; ++k) {
+            for (int k = 0; k < kMergeBatch; ++k) {
                 const float s = fast_exp2(pm[k] - nm);  // 0 for absent partials (m = -inf)
                 ax = fmaf(po[k].x, s, ax);
                 ay = fmaf(po[k].y, s, ay);

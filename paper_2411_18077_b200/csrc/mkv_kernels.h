@@ -86,6 +86,7 @@ struct PagesParams {
     float* part_o;          // [slots][kMaxG][d]
     float scale_log2;
     uint64_t* trace;        // diagnostics: per warp {start, after wait, done} (globaltimer), or null
+    int early;              // q may be read before griddepcontrol.wait (see pages_kernel)
 };
 constexpr int kMaxPagesWarps = 12;  // partial-slot sizing
 struct PagesConfig {
