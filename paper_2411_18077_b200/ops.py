@@ -249,6 +249,24 @@ class KVCache:
         check(lib().mkv_decode_step(self.h, C.byref(args), _stream_ptr(stream)), "decode_step")
         return out
 
+    def decode_step_layers(self, q: torch.Tensor, k_new: Optional[torch.Tensor], v_new: Optional[torch.Tensor],
+                           scale: float, unit_begin: int = 0, out: Optional[torch.Tensor] = None, stream=None):
+        """All layers of one decode step in one call: q fp16 [L, n, G, d], k_new/v_new fp16 [L, n, d]
+        (None: attend only); layer l owns units unit_begin + l*n .. + n.  Every q must be written
+        before the call: layers after the first start their page pass while the previous layer's
+        finish kernel is still merging (mkv_decode_step_layers)."""
+        L, n, G, d = q.shape
+        if out is None:
+            out = torch.empty_like(q)
+        args = (_capi.DecodeArgs * L)()
+        for l in range(L):
+            args[l] = _capi.DecodeArgs(unit_begin + l * n, n, G, q[l].data_ptr(),
+                                       k_new[l].data_ptr() if k_new is not None else None,
+                                       v_new[l].data_ptr() if v_new is not None else None,
+                                       out[l].data_ptr(), float(scale))
+        check(lib().mkv_decode_step_layers(self.h, L, args, _stream_ptr(stream)), "decode_step_layers")
+        return out
+
     def append(self, k_new: torch.Tensor, v_new: torch.Tensor, unit_begin: int = 0, stream=None):
         """decode_append (cache_engine.cpp:79-90)."""
         check(lib().mkv_cache_append(self.h, unit_begin, k_new.shape[0], k_new.data_ptr(), v_new.data_ptr(),

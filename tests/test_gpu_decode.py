@@ -174,3 +174,36 @@ def test_decode_randomized_configs(mkv, seed):
     worst = run_decode(mkv, n_units=n_units, G=G, L=L, hh=0, rw=rw, steps=steps, n_r=n_r,
                        check_every=max(1, steps // 12), hh_per_unit=hh, seed=seed)
     assert worst <= TOL, (n_units, G, n_r, L, rw, steps, worst)
+
+
+def test_decode_step_layers_matches_per_layer_calls(mkv):
+    """mkv_decode_step_layers overlaps layer l's finish kernel with layer l+1's page pass (q of
+    later layers read before griddepcontrol.wait, partial buffers shared by all layers): its
+    outputs must be bit-identical to one mkv_decode_step per layer, through a flush and with
+    very uneven layer sizes (partials of consecutive layers land in the same slots)."""
+    d, n, G, L, layers, n_r = 128, 12, 4, 2000, 6, 32
+    rng = np.random.default_rng(21)
+    budgets = [1500, 40, 900, 16, 1200, 300]  # hh per layer: long, tiny, long, ...
+    caps = [budgets[l] + 64 for l in range(layers) for _ in range(n)]
+    k = torch.from_numpy(rng.standard_normal((layers * n, L, d)).astype(np.float16)).cuda()
+    v = torch.from_numpy(rng.standard_normal((layers * n, L, d)).astype(np.float16)).cuda()
+    a = torch.from_numpy(rng.random((layers * n, L)).astype(np.float32)).cuda()
+    caches = []
+    for _ in range(2):
+        c = mkv.KVCache(layers * n, caps, max_decode_tokens=80, n_r=n_r)
+        for l in range(layers):
+            c.prefill(k[l * n:(l + 1) * n], v[l * n:(l + 1) * n], a[l * n:(l + 1) * n], budgets[l], 64,
+                      unit_begin=l * n)
+        caches.append(c)
+    scale = 1.0 / np.sqrt(d)
+    for s in range(40):  # n_r = 32: one flush at step 31
+        q = torch.from_numpy(rng.standard_normal((layers, n, G, d)).astype(np.float16)).cuda()
+        tk = torch.from_numpy(rng.standard_normal((layers, n, d)).astype(np.float16)).cuda()
+        tv = torch.from_numpy(rng.standard_normal((layers, n, d)).astype(np.float16)).cuda()
+        fused = caches[0].decode_step_layers(q, tk, tv, scale)
+        ref = torch.stack([caches[1].decode_step(q[l], tk[l], tv[l], scale, unit_begin=l * n)
+                           for l in range(layers)])
+        assert torch.equal(fused, ref), f"step {s}: max diff {(fused.float() - ref.float()).abs().max()}"
+    for c in caches:
+        c.check()
+    assert caches[0].unit_info(0) == caches[1].unit_info(0)
