@@ -280,7 +280,7 @@ def run_mkv(args, rank, world):
     in_ready = [ev() for _ in range(2)]
     computed = [ev() for _ in range(2)]
     out_read = [ev() for _ in range(2)]
-    e2e_steps = min(args.steps, 20)
+    e2e_steps = args.steps
 
     def issue_h2d(s_):
         bsel, src = s_ % 2, (args.warmup + s_) % steps_total

@@ -172,6 +172,11 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pages_kernel(const PagesParams
     auto issue = [&](int stage) {
         if (pg >= end) return;
         const int n = min(kBatch, p_rend - pg);  // batches never straddle units or warp ranges
+#ifdef MKV_AB_COMPUTE_ONLY  // A/B probe: after the first ring fill, batches reuse stale smem
+        if (pg >= start + kStages * kBatch) {
+            if (lane == 0) mbar_expect_tx(&bars[stage], 0);
+        } else
+#endif
         if (lane == 0) {
             mbar_expect_tx(&bars[stage], n * kPageBytes);
             bulk_g2s(ring + (size_t)stage * kBatch * kPageBytes, p_base + (size_t)pg * kPageBytes, n * kPageBytes,
