@@ -318,12 +318,18 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pages_kernel(const PagesParams
                 x[j][1] = fmaf(S[j][1], sk, kb1);
                 x[j][2] = fmaf(S[j][2], sk, kb0);
                 x[j][3] = fmaf(S[j][3], sk, kb1);
-                if (special) {
+            }
+            if (special) {  // one branch per batch: short batch or the prefill block's partial page
+#pragma unroll
+                for (int j = 0; j < kBatch; ++j) {
                     const int lp = pfirst + j;
                     const int valid = (j >= n) ? 0 : ((lp == partial_page) ? partial_valid : 16);
                     if (gid >= valid) { x[j][0] = -INFINITY; x[j][1] = -INFINITY; }
                     if (gid + 8 >= valid) { x[j][2] = -INFINITY; x[j][3] = -INFINITY; }
                 }
+            }
+#pragma unroll
+            for (int j = 0; j < kBatch; ++j) {
                 mx0 = fmaxf(mx0, fmaxf(x[j][0], x[j][2]));
                 mx1 = fmaxf(mx1, fmaxf(x[j][1], x[j][3]));
             }
