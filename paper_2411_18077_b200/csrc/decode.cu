@@ -105,7 +105,9 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
 // pages kernel
 // ---------------------------------------------------------------------------
 template <int kWarps, int kStages>
-__global__ void __launch_bounds__(kWarps * 32, 1) pages_kernel(const PagesParams P) {
+// <= 208 registers (x 256 threads = 53248): leaves 12288 registers of the SM's 65536 for one
+// co-resident finish CTA (4 warps x 96).
+__global__ void __maxnreg__(208) pages_kernel(const PagesParams P) {
     constexpr int kWarpSmem = warp_smem<kStages>();
     extern __shared__ __align__(128) uint8_t smem[];
     const int warp = threadIdx.x >> 5, lane = lane_id();
@@ -440,14 +442,14 @@ static cudaError_t launch_pages_t(const PagesParams& p, int grid, cudaStream_t s
 // (warps per CTA, ring stages) of the page kernel; MKV_PAGES_CFG=WxS selects a variant
 PagesConfig pages_config() {
     static PagesConfig cfg = [] {
-        // 8 warps: the page pass is ~2% slower than with 12 (same SM sub-partition
-        // throughput) but the step is ~3% faster: a third fewer
-        // (warp, unit) partials to write and merge.
+        // 8 warps: a 12-warp CTA ran the page pass ~2% faster (same SM sub-partition
+        // throughput) but needs the whole register file, so no finish CTA
+        // could share its SM; 8 warps also leave a third fewer partials to merge.
         PagesConfig c{8, 2};
         if (const char* e = getenv("MKV_PAGES_CFG")) {
             int w = 0, s = 0;
             if (sscanf(e, "%dx%d", &w, &s) == 2 &&
-                ((w == 12 && s == 2) || (w == 8 && s == 3) || (w == 8 && s == 2)))
+                ((w == 8 && s == 3) || (w == 8 && s == 2)))
                 c = PagesConfig{w, s};
         }
         return c;
@@ -458,7 +460,6 @@ PagesConfig pages_config() {
 cudaError_t launch_pages(const PagesParams& p, int grid, cudaStream_t s) {
     const PagesConfig c = pages_config();
     if (c.warps == 8 && c.stages == 3) return launch_pages_t<8, 3>(p, grid, s);
-    if (c.warps == 12 && c.stages == 2) return launch_pages_t<12, 2>(p, grid, s);
     return launch_pages_t<8, 2>(p, grid, s);
 }
 
