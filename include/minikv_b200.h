@@ -107,6 +107,29 @@ int mkv_allocate_variance(const float* per_layer_variance, size_t layers, size_t
 int mkv_score_variance(const float* a_cumul, int64_t a_stride, int n_units, int length, float* out,
                        void* stream);
 
+/* replaces: H2OBaselineTrace h2o_dynamic_baseline(prompt_k, prompt_scores, decode_qs,    */
+/*           decode_ks, hh_budget, rw_budget, scale)  harness.hpp:33-43,              */
+/*           harness.cpp:83-150 -- the step-wise greedy H2O comparison policy on the    */
+/* device (one CTA).  All pointers are device fp32: prompt_k [l_prompt, d] (row stride   */
+/* ld_k), prompt_scores [l_prompt], qs / ks [steps, d].  Output kept [steps + 1,         */
+/* kept_stride] int32 (ascending original positions; row 0 = after the prompt eviction)  */
+/* and kept_count [steps + 1]; kept_stride >= min(l_prompt + steps, hh + rw).  Same      */
+/* arithmetic order as the reference, so the kept sets are bit-identical to it.         */
+typedef struct {
+    const float* prompt_k;
+    int64_t ld_k;
+    const float* prompt_scores;
+    const float* qs;
+    const float* ks;
+    int l_prompt, d, steps;
+    int64_t hh_budget, rw_budget;
+    float scale;
+    int32_t* kept;
+    int64_t kept_stride;
+    int32_t* kept_count;
+} mkv_h2o_args;
+int mkv_h2o_dynamic_baseline(const mkv_h2o_args* args, void* stream);
+
 /* ------------------------------------------------------------------------ */
 /* Device KV cache: one handle owns n_units (seq, layer, kv-head) caches.    */
 /* replaces: KVCacheLayer make_cache(d, n_r, gs, mode)  cache_engine.hpp:44-46 */

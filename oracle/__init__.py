@@ -101,6 +101,10 @@ class _Lib:
         av.argtypes = [_f32p, _sz, _sz, C.c_int, _i64p, C.POINTER(C.c_int)]
         lv = getattr(L, p + "layer_score_variance")
         lv.argtypes = [_f32p, _sz, C.POINTER(C.c_float)]
+        h2 = getattr(L, p + "h2o_dynamic_baseline")
+        h2.argtypes = [_f32p, _sz, _sz, _f32p, _f32p, _f32p, _sz, _sz, _sz, C.c_float,
+                       np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS"), _sz,
+                       np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")]
 
     def fn(self, name):
         return getattr(self.lib, self.prefix + name)
@@ -183,6 +187,21 @@ class _Lib:
         r = C.c_float(0)
         _check(self.fn("layer_score_variance")(a, len(a), C.byref(r)), "layer_score_variance")
         return r.value
+
+    # harness.cpp:108-150 -> list of kept position lists (post-prefill set first)
+    def h2o_dynamic_baseline(self, prompt_k, prompt_scores, qs, ks, hh, rw, scale):
+        pk, sc = _f32(prompt_k), _f32(np.asarray(prompt_scores, np.float32))
+        qs, ks = _f32(qs), _f32(ks)
+        l, d = pk.shape
+        steps = qs.shape[0]
+        stride = max(1, min(l + steps, hh + rw))
+        kept = np.zeros((steps + 1) * stride, np.int32)
+        cnt = np.zeros(steps + 1, np.int32)
+        _check(self.fn("h2o_dynamic_baseline")(pk, l, d, sc, qs.reshape(-1) if steps else np.zeros(1, np.float32),
+                                               ks.reshape(-1) if steps else np.zeros(1, np.float32), steps, hh, rw,
+                                               scale, kept, stride, cnt), "h2o_dynamic_baseline")
+        kept = kept.reshape(steps + 1, stride)
+        return [kept[s, :cnt[s]].tolist() for s in range(steps + 1)]
 
     # selection.cpp:48-59
     def allocate_uniform(self, total, layers):

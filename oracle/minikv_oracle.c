@@ -488,6 +488,78 @@ int mko_layer_score_variance(const float* a, size_t n, float* out) {
 }
 
 /* ------------------------------------------------------------------ */
+/* H2O comparison baseline (harness.cpp:75-150)                        */
+/* ------------------------------------------------------------------ */
+
+/* evict_to_budget (harness.cpp:83-106): drop the first lowest score outside the rw most
+   recent entries until n <= budget; the kept list holds original positions in order */
+static size_t h2o_evict(size_t* pos, const double* score, size_t n, size_t budget, size_t rw) {
+    while (n > budget) {
+        const size_t protect_from = n > rw ? n - rw : 0;
+        size_t victim = n;
+        double best = INFINITY;
+        for (size_t i = 0; i < protect_from; ++i)
+            if (score[pos[i]] < best) {
+                best = score[pos[i]];
+                victim = i;
+            }
+        if (victim == n) break;
+        memmove(pos + victim, pos + victim + 1, (n - victim - 1) * sizeof(size_t));
+        --n;
+    }
+    return n;
+}
+
+/* h2o_dynamic_baseline (harness.cpp:108-150): scores per original position in double;
+   attn = scale * dot (matrix.cpp:60-66), softmax_inplace (matrix.cpp:83-99) with expf */
+int mko_h2o_dynamic_baseline(const float* pk, size_t l, size_t d, const float* scores, const float* qs,
+                             const float* ks, size_t steps, size_t hh, size_t rw, float scale, int32_t* kept,
+                             size_t stride, int32_t* counts) {
+    if (hh + rw < 1) return MKO_INVALID;
+    const size_t total = l + steps, budget = hh + rw;
+    size_t* pos = (size_t*)malloc((total + 1) * sizeof(size_t));
+    double* score = (double*)malloc((total + 1) * sizeof(double));
+    float* attn = (float*)malloc((total + 1) * sizeof(float));
+    if (!pos || !score || !attn) {
+        free(pos); free(score); free(attn);
+        return MKO_INVALID;
+    }
+    for (size_t i = 0; i < l; ++i) {
+        pos[i] = i;
+        score[i] = (double)scores[i];
+    }
+    size_t n = h2o_evict(pos, score, l, budget, rw);
+    for (size_t i = 0; i < n; ++i) kept[i] = (int32_t)pos[i];
+    counts[0] = (int32_t)n;
+    for (size_t s = 0; s < steps; ++s) {
+        pos[n] = l + s;
+        score[l + s] = 0.0;
+        ++n;
+        const float* q = qs + s * d;
+        for (size_t j = 0; j < n; ++j) {
+            const size_t p = pos[j];
+            const float* key = p < l ? pk + p * d : ks + (p - l) * d;
+            float acc = 0.0f;
+            for (size_t c = 0; c < d; ++c) acc += q[c] * key[c];
+            attn[j] = scale * acc;
+        }
+        float m = attn[0];
+        for (size_t j = 1; j < n; ++j) m = attn[j] > m ? attn[j] : m;
+        float sum = 0.0f;
+        for (size_t j = 0; j < n; ++j) {
+            attn[j] = expf(attn[j] - m);
+            sum += attn[j];
+        }
+        for (size_t j = 0; j < n; ++j) score[pos[j]] += (double)(attn[j] / sum);
+        n = h2o_evict(pos, score, n, budget, rw);
+        for (size_t i = 0; i < n; ++i) kept[(s + 1) * stride + i] = (int32_t)pos[i];
+        counts[s + 1] = (int32_t)n;
+    }
+    free(pos); free(score); free(attn);
+    return MKO_OK;
+}
+
+/* ------------------------------------------------------------------ */
 /* cache engine (cache_engine.cpp)                                    */
 /* ------------------------------------------------------------------ */
 

@@ -79,6 +79,10 @@ int mko_allocate_variance(const float* variance, size_t layers, size_t total_hh,
                           int64_t* out, int* uniform_fallback);
 /* selection.cpp:130-146: population variance, two double passes in index order. */
 int mko_layer_score_variance(const float* a_cumul, size_t n, float* out);
+/* harness.cpp:108-150: kept [(steps + 1) x stride] ascending positions, counts [steps + 1] */
+int mko_h2o_dynamic_baseline(const float* prompt_k, size_t l, size_t d, const float* prompt_scores,
+                             const float* qs, const float* ks, size_t steps, size_t hh, size_t rw, float scale,
+                             int32_t* kept, size_t stride, int32_t* counts);
 int mko_allocate_pyramid(size_t mean_x, size_t layers, size_t depth, int bottom_heavy,
                          int64_t* out);                                            /* :61-83 */
 

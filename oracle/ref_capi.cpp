@@ -23,6 +23,7 @@
 
 #include "minikv/attention.hpp"
 #include "minikv/cache_engine.hpp"
+#include "minikv/harness.hpp"
 #include "minikv/snapshot.hpp"
 #include "minikv/quantizer.hpp"
 #include "minikv/selection.hpp"
@@ -180,6 +181,25 @@ int mkr_allocate_variance(const float* variance, size_t layers, size_t total, in
 // selection.cpp:130-146
 int mkr_layer_score_variance(const float* a, size_t n, float* out) {
     GUARD({ *out = layer_score_variance(Vector(a, a + n)); })
+}
+
+// harness.cpp:108-150
+int mkr_h2o_dynamic_baseline(const float* pk, size_t l, size_t d, const float* scores, const float* qs,
+                             const float* ks, size_t steps, size_t hh, size_t rw, float scale, int32_t* kept,
+                             size_t stride, int32_t* counts) {
+    GUARD({
+        std::vector<Vector> q, k;
+        for (size_t s = 0; s < steps; ++s) {
+            q.emplace_back(qs + s * d, qs + (s + 1) * d);
+            k.emplace_back(ks + s * d, ks + (s + 1) * d);
+        }
+        const H2OBaselineTrace t = h2o_dynamic_baseline(mat(pk, l, d), Vector(scores, scores + l), q, k, hh, rw, scale);
+        for (size_t s = 0; s < t.kept_per_step.size(); ++s) {
+            counts[s] = static_cast<int32_t>(t.kept_per_step[s].size());
+            for (size_t i = 0; i < t.kept_per_step[s].size(); ++i)
+                kept[s * stride + i] = static_cast<int32_t>(t.kept_per_step[s][i]);
+        }
+    })
 }
 
 // ---- cache engine: an opaque KVCacheLayer handle ----

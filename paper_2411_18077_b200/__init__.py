@@ -8,13 +8,15 @@ reference C++ operator interface (namespace minikv) on torch device tensors.
 """
 from ._capi import (CudaError, DomainError, InvalidArgument, MkvError, OutOfRange,  # noqa: F401
                     RuntimeFailure, Unsupported)
-from .ops import (AttentionResult, KVCache, VarianceMode, allocate_pyramid, allocate_uniform,  # noqa: F401
-                  allocate_variance, default_scale, layer_score_variance, select_token_counts,
+from .ops import (AttentionResult, H2OBaselineTrace, KVCache, PersistenceReport, VarianceMode,  # noqa: F401
+                  allocate_pyramid, allocate_uniform, allocate_variance, default_scale, h2o_dynamic_baseline,
+                  layer_score_variance, persistence_analysis, select_token_counts,
                   select_tokens, selective_flash_attn, synth_fp16, synth_uniform)
 
 __all__ = [
     "AttentionResult", "KVCache", "VarianceMode", "allocate_pyramid", "allocate_uniform", "allocate_variance",
-    "layer_score_variance", "default_scale",
+    "layer_score_variance", "default_scale", "H2OBaselineTrace", "PersistenceReport", "h2o_dynamic_baseline",
+    "persistence_analysis",
     "select_token_counts", "select_tokens", "selective_flash_attn", "synth_fp16", "synth_uniform",
     "MkvError", "InvalidArgument", "DomainError", "RuntimeFailure", "OutOfRange", "CudaError",
     "Unsupported",

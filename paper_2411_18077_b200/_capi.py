@@ -97,6 +97,12 @@ class PrefillSelectArgs(C.Structure):
                 ("v", vp), ("v_su", i64), ("v_st", i64)]
 
 
+class H2OArgs(C.Structure):
+    _fields_ = [("prompt_k", vp), ("ld_k", i64), ("prompt_scores", vp), ("qs", vp), ("ks", vp),
+                ("l_prompt", i32), ("d", i32), ("steps", i32), ("hh_budget", i64), ("rw_budget", i64),
+                ("scale", C.c_float), ("kept", vp), ("kept_stride", i64), ("kept_count", vp)]
+
+
 class DecodeArgs(C.Structure):
     _fields_ = [("unit_begin", i32), ("n_units", i32), ("group", i32),
                 ("q", vp), ("k_new", vp), ("v_new", vp), ("out", vp), ("scale", C.c_float)]
@@ -111,7 +117,7 @@ EXPORTS = [
     "mkv_cache_prefill", "mkv_cache_prefill_select", "mkv_decode_step", "mkv_cache_append",
     "mkv_decode_step_layers", "mkv_debug_decode_trace", "mkv_decode_pages_only", "mkv_cache_export_sizes", "mkv_cache_export_reference",
     "mkv_cache_export_residual", "mkv_cache_check", "mkv_cache_save_mkvc", "mkv_cache_load_mkvc",
-    "mkv_synth_fp16", "mkv_synth_fp16_rows", "mkv_synth_uniform_f32",
+    "mkv_synth_fp16", "mkv_synth_fp16_rows", "mkv_synth_uniform_f32", "mkv_h2o_dynamic_baseline",
 ]
 
 _lib = None
@@ -133,6 +139,8 @@ def lib():
     L.mkv_allocate_uniform.argtypes = [C.c_size_t, C.c_size_t, C.POINTER(C.c_int64)]
     L.mkv_allocate_variance.argtypes = [vp, C.c_size_t, C.c_size_t, i32, C.POINTER(C.c_int64), C.POINTER(C.c_int)]
     L.mkv_score_variance.argtypes = [vp, i64, i32, i32, vp, vp]
+    if hasattr(L, "mkv_h2o_dynamic_baseline"):
+        L.mkv_h2o_dynamic_baseline.argtypes = [C.POINTER(H2OArgs), vp]
     L.mkv_cache_create.argtypes = [C.POINTER(CacheConfig), C.POINTER(vp)]
     L.mkv_cache_destroy.argtypes = [vp]
     L.mkv_cache_bytes.argtypes = [vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]

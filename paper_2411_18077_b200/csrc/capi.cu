@@ -216,6 +216,42 @@ int mkv_score_variance(const float* a_cumul, int64_t a_stride, int n_units, int 
 }
 
 // ---------------------------------------------------------------------------
+// H2O baseline (harness.cpp:83-150)
+// ---------------------------------------------------------------------------
+int mkv_h2o_dynamic_baseline(const mkv_h2o_args* a, void* stream) {
+    if (!a) return fail(MKV_ERR_INVALID_ARGUMENT, "h2o_dynamic_baseline: null args");
+    if (a->hh_budget < 0 || a->rw_budget < 0 || a->hh_budget + a->rw_budget < 1)
+        return fail(MKV_ERR_INVALID_ARGUMENT, "h2o_dynamic_baseline: budget must be >= 1");
+    if (a->l_prompt < 0 || a->steps < 0 || a->d < 1) return fail(MKV_ERR_INVALID_ARGUMENT, "h2o_dynamic_baseline: bad shape");
+    const int64_t total = (int64_t)a->l_prompt + a->steps;
+    if (total > INT32_MAX / 2 || a->hh_budget + a->rw_budget > INT32_MAX)
+        return fail(MKV_ERR_INVALID_ARGUMENT, "h2o_dynamic_baseline: too long");
+    const int64_t need = std::min<int64_t>(total, a->hh_budget + a->rw_budget);
+    if (a->kept_stride < need || !a->kept || !a->kept_count)
+        return fail(MKV_ERR_INVALID_ARGUMENT, "h2o_dynamic_baseline: kept buffer stride %lld < %lld",
+                    (long long)a->kept_stride, (long long)need);
+    if ((a->l_prompt > 0 && (!a->prompt_k || !a->prompt_scores || a->ld_k < a->d)) || (a->steps > 0 && (!a->qs || !a->ks)))
+        return fail(MKV_ERR_INVALID_ARGUMENT, "h2o_dynamic_baseline: null tensor");
+    if (int r = require_device()) return r;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const size_t n = (size_t)std::max<int64_t>(total, 1);
+    void* ws = nullptr;
+    CK(cudaMallocAsync(&ws, n * (sizeof(double) + sizeof(int) + sizeof(float)), s));
+    H2OParams p;
+    p.prompt_k = a->prompt_k; p.ld_k = a->ld_k; p.prompt_scores = a->prompt_scores;
+    p.qs = a->qs; p.ks = a->ks; p.l_prompt = a->l_prompt; p.d = a->d; p.steps = a->steps;
+    p.hh_budget = (int)a->hh_budget; p.rw_budget = (int)std::min<int64_t>(a->rw_budget, INT32_MAX);
+    p.scale = a->scale; p.kept = a->kept; p.kept_stride = a->kept_stride; p.kept_count = a->kept_count;
+    p.ws_score = static_cast<double*>(ws);
+    p.ws_pos = reinterpret_cast<int*>(p.ws_score + n);
+    p.ws_attn = reinterpret_cast<float*>(p.ws_pos + n);
+    const cudaError_t e = launch_h2o(p, s);
+    cudaFreeAsync(ws, s);
+    CK(e);
+    return MKV_OK;
+}
+
+// ---------------------------------------------------------------------------
 // K1 prefill attention
 // ---------------------------------------------------------------------------
 int mkv_prefill_attn(const mkv_prefill_args* a, void* stream) {

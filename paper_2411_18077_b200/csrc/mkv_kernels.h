@@ -95,6 +95,24 @@ struct PagesConfig {
 PagesConfig pages_config();
 cudaError_t launch_pages(const PagesParams& p, int grid, cudaStream_t s);
 
+// ---- H2O baseline (h2o.cu) ----
+struct H2OParams {
+    const float* prompt_k;
+    int64_t ld_k;
+    const float* prompt_scores;
+    const float* qs;
+    const float* ks;
+    int l_prompt, d, steps, hh_budget, rw_budget;
+    float scale;
+    int32_t* kept;
+    int64_t kept_stride;
+    int32_t* kept_count;
+    int* ws_pos;       // [l_prompt + steps]
+    double* ws_score;  // [l_prompt + steps]
+    float* ws_attn;    // [l_prompt + steps]
+};
+cudaError_t launch_h2o(const H2OParams& p, cudaStream_t s);
+
 // ---- utilities (synth.cu) ----
 cudaError_t launch_synth_fp16(__half* out, int64_t n_rows, int64_t row_len, int64_t ld,
                               uint64_t seed, uint64_t stream_base, uint64_t stream_step,

@@ -17,7 +17,7 @@ import ctypes as C
 import os
 import math
 from dataclasses import dataclass
-from typing import Optional, Sequence
+from typing import List, Optional, Sequence
 
 import torch
 
@@ -173,6 +173,72 @@ def allocate_uniform(total_hh: int, layers: int):
     out = (C.c_int64 * max(layers, 1))()
     check(lib().mkv_allocate_uniform(total_hh, layers, out), "allocate_uniform")
     return [int(x) for x in out[:layers]]
+
+
+# ---------------------------------------------------------------------------
+# H2O comparison baseline + persistence (harness.hpp:33-52, harness.cpp:83-169)
+# ---------------------------------------------------------------------------
+@dataclass
+class H2OBaselineTrace:
+    """harness.hpp:35-38: kept_per_step[0] is the post-prefill set, one entry per decode step
+    follows; each entry is the ascending list of original token positions kept."""
+    kept_per_step: List[List[int]]
+
+
+@dataclass
+class PersistenceReport:
+    """harness.hpp:45-48."""
+    fractions: List[float]
+    final_fraction: float
+
+
+def h2o_dynamic_baseline(prompt_k: torch.Tensor, prompt_scores: torch.Tensor, decode_qs: torch.Tensor,
+                         decode_ks: torch.Tensor, hh_budget: int, rw_budget: int, scale: float,
+                         stream=None) -> H2OBaselineTrace:
+    """h2o_dynamic_baseline (harness.cpp:108-150) on the device: fp32 CUDA tensors prompt_k
+    [L, d], prompt_scores [L], decode_qs / decode_ks [steps, d].  Kept sets are bit-identical to
+    the reference (same arithmetic order, see csrc/h2o.cu)."""
+    L = prompt_k.shape[0]
+    d = prompt_k.shape[1] if prompt_k.dim() == 2 else decode_qs.shape[-1]
+    if prompt_scores.numel() != L:
+        raise _capi.InvalidArgument("h2o_dynamic_baseline: prompt score length mismatch")
+    if decode_qs.shape[0] != decode_ks.shape[0]:
+        raise _capi.InvalidArgument("h2o_dynamic_baseline: decode stream length mismatch")
+    steps = decode_qs.shape[0]
+    if steps and (decode_qs.shape[1] != d or decode_ks.shape[1] != d):
+        raise _capi.InvalidArgument("append_row: width mismatch")
+    for t in (prompt_k, prompt_scores, decode_qs, decode_ks):
+        if t.numel() and (t.dtype != torch.float32 or not t.is_cuda or t.stride(-1) != 1):
+            raise _capi.InvalidArgument("h2o_dynamic_baseline: fp32 CUDA tensors with unit stride expected")
+    qs, ks = decode_qs.contiguous(), decode_ks.contiguous()
+    stride = max(1, min(L + steps, hh_budget + rw_budget))
+    kept = torch.empty((steps + 1, stride), dtype=torch.int32, device=prompt_scores.device)
+    count = torch.empty(steps + 1, dtype=torch.int32, device=prompt_scores.device)
+    args = _capi.H2OArgs(prompt_k.data_ptr() if L else None, prompt_k.stride(0) if L else d,
+                         prompt_scores.data_ptr() if L else None, qs.data_ptr() if steps else None,
+                         ks.data_ptr() if steps else None, L, d, steps, int(hh_budget), int(rw_budget),
+                         float(scale), kept.data_ptr(), stride, count.data_ptr())
+    check(lib().mkv_h2o_dynamic_baseline(C.byref(args), _stream_ptr(stream)), "h2o_dynamic_baseline")
+    kh, ch = kept.cpu().tolist(), count.cpu().tolist()
+    return H2OBaselineTrace([kh[s][:ch[s]] for s in range(steps + 1)])
+
+
+def persistence_analysis(trace: H2OBaselineTrace, prefill_hh: Sequence[int]) -> PersistenceReport:
+    """persistence_analysis (harness.cpp:152-169): per trace entry, the fraction of the prefill
+    heavy hitters still kept (host arithmetic on the device-produced kept sets)."""
+    if len(prefill_hh) == 0:
+        raise _capi.RuntimeFailure("persistence_analysis: empty prefill heavy-hitter set")
+    import bisect
+
+    import numpy as np
+    fr = []
+    for kept in trace.kept_per_step:
+        hit = 0
+        for idx in prefill_hh:
+            j = bisect.bisect_left(kept, idx)
+            hit += 1 if j < len(kept) and kept[j] == idx else 0
+        fr.append(float(np.float32(hit) / np.float32(len(prefill_hh))))  # float / float as the reference
+    return PersistenceReport(fr, fr[-1])
 
 
 # ---------------------------------------------------------------------------

@@ -106,3 +106,20 @@ def test_variance_allocation_random(PR):  # selection.cpp:85-146, bit-identical 
     for _ in range(50):
         a = (rng.random(int(rng.integers(1, 5000))) * 3).astype(np.float32)
         assert P.layer_score_variance(a) == R.layer_score_variance(a)
+
+
+def test_h2o_dynamic_baseline_random(PR):  # harness.cpp:83-150: identical kept sets at every step
+    P, R = PR
+    rng = np.random.default_rng(41)
+    for _ in range(40):
+        l = int(rng.integers(1, 300))
+        d = int(rng.choice([2, 8, 16, 64, 128]))
+        steps = int(rng.integers(0, 60))
+        hh, rw = int(rng.integers(0, 200)), int(rng.integers(0, 50))
+        hh = max(hh, 1 - rw)
+        pk = rng.standard_normal((l, d)).astype(np.float32)
+        sc = rng.random(l).astype(np.float32)
+        qs = rng.standard_normal((steps, d)).astype(np.float32)
+        ks = rng.standard_normal((steps, d)).astype(np.float32)
+        assert P.h2o_dynamic_baseline(pk, sc, qs, ks, hh, rw, 1 / np.sqrt(d)) == \
+            R.h2o_dynamic_baseline(pk, sc, qs, ks, hh, rw, 1 / np.sqrt(d))
