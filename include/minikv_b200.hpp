@@ -83,6 +83,19 @@ LayerAllocation allocate_pyramid(std::size_t mean_budget_x, std::size_t layers, 
 LayerAllocation allocate_variance(const Vector& per_layer_variance, std::size_t total_hh, VarianceMode mode);
 float layer_score_variance(const Vector& a_cumul);  // on the device (fp64 two-pass)
 
+// ---- harness.hpp:33-52: the H2O comparison baseline (device) and persistence ----
+struct H2OBaselineTrace {
+    std::vector<std::vector<std::size_t>> kept_per_step;  // [0] = post-prefill set
+};
+H2OBaselineTrace h2o_dynamic_baseline(const Matrix& prompt_k, const Vector& prompt_scores,
+                                      const std::vector<Vector>& decode_qs, const std::vector<Vector>& decode_ks,
+                                      std::size_t hh_budget, std::size_t rw_budget, float scale);
+struct PersistenceReport {
+    Vector fractions;
+    double final_fraction = 0.0;
+};
+PersistenceReport persistence_analysis(const H2OBaselineTrace& trace, const std::vector<std::size_t>& prefill_hh);
+
 // ---- quantizer.hpp:15-42: the reference's QuantizedTensor stream format ----
 enum class GroupAxis { PerChannel, PerToken };
 struct GroupQuantParams {

@@ -192,6 +192,59 @@ float layer_score_variance(const Vector& a_cumul) {
     return r;
 }
 
+// harness.cpp:108-150 on the device (mkv_h2o_dynamic_baseline)
+H2OBaselineTrace h2o_dynamic_baseline(const Matrix& prompt_k, const Vector& prompt_scores,
+                                      const std::vector<Vector>& decode_qs, const std::vector<Vector>& decode_ks,
+                                      size_t hh_budget, size_t rw_budget, float scale) {
+    if (prompt_k.rows != prompt_scores.size())
+        throw std::invalid_argument("h2o_dynamic_baseline: prompt score length mismatch");
+    if (decode_qs.size() != decode_ks.size())
+        throw std::invalid_argument("h2o_dynamic_baseline: decode stream length mismatch");
+    if (hh_budget + rw_budget < 1) throw std::invalid_argument("h2o_dynamic_baseline: budget must be >= 1");
+    const size_t L = prompt_k.rows, steps = decode_qs.size();
+    const size_t d = prompt_k.cols ? prompt_k.cols : (steps ? decode_ks[0].size() : 1);
+    std::vector<float> qs(steps * d), ks(steps * d);
+    for (size_t s = 0; s < steps; ++s) {
+        if (decode_ks[s].size() != d) throw std::invalid_argument("append_row: width mismatch");
+        if (decode_qs[s].size() != d) throw std::invalid_argument("h2o_dynamic_baseline: query width mismatch");
+        std::copy(decode_qs[s].begin(), decode_qs[s].end(), qs.begin() + s * d);
+        std::copy(decode_ks[s].begin(), decode_ks[s].end(), ks.begin() + s * d);
+    }
+    const size_t stride = std::max<size_t>(1, std::min(L + steps, hh_budget + rw_budget));
+    Dev dk = upload_f32(prompt_k.data.data(), L * d), dsc = upload_f32(prompt_scores.data(), L);
+    Dev dq = upload_f32(qs.data(), steps * d), dks = upload_f32(ks.data(), steps * d);
+    Dev dkept((steps + 1) * stride * sizeof(int32_t)), dcnt((steps + 1) * sizeof(int32_t));
+    mkv_h2o_args a{};
+    a.prompt_k = dk.as<float>(); a.ld_k = (int64_t)d; a.prompt_scores = dsc.as<float>();
+    a.qs = dq.as<float>(); a.ks = dks.as<float>();
+    a.l_prompt = (int)L; a.d = (int)d; a.steps = (int)steps;
+    a.hh_budget = (int64_t)hh_budget; a.rw_budget = (int64_t)rw_budget; a.scale = scale;
+    a.kept = dkept.as<int32_t>(); a.kept_stride = (int64_t)stride; a.kept_count = dcnt.as<int32_t>();
+    throw_status(mkv_h2o_dynamic_baseline(&a, nullptr), "h2o_dynamic_baseline");
+    std::vector<int32_t> kept((steps + 1) * stride), cnt(steps + 1);
+    cuda_check(cudaMemcpy(kept.data(), dkept.p, kept.size() * sizeof(int32_t), cudaMemcpyDeviceToHost), "download");
+    cuda_check(cudaMemcpy(cnt.data(), dcnt.p, cnt.size() * sizeof(int32_t), cudaMemcpyDeviceToHost), "download");
+    H2OBaselineTrace t;
+    t.kept_per_step.resize(steps + 1);
+    for (size_t s = 0; s <= steps; ++s)
+        t.kept_per_step[s].assign(kept.begin() + s * stride, kept.begin() + s * stride + cnt[s]);
+    return t;
+}
+
+// harness.cpp:152-169 (host arithmetic on the device-produced kept sets)
+PersistenceReport persistence_analysis(const H2OBaselineTrace& trace, const std::vector<size_t>& prefill_hh) {
+    if (prefill_hh.empty()) throw std::runtime_error("persistence_analysis: empty prefill heavy-hitter set");
+    PersistenceReport r;
+    for (const auto& kept : trace.kept_per_step) {
+        size_t hit = 0;
+        for (size_t idx : prefill_hh)
+            if (std::binary_search(kept.begin(), kept.end(), idx)) ++hit;
+        r.fractions.push_back(static_cast<float>(hit) / static_cast<float>(prefill_hh.size()));
+    }
+    r.final_fraction = r.fractions.back();
+    return r;
+}
+
 // ---------------------------------------------------------------------------
 // quantized stream (quantizer.cpp:153-195)
 // ---------------------------------------------------------------------------

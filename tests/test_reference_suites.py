@@ -4,11 +4,13 @@ dropin/Makefile compiles them where /root/reference exists, into oracle/_ref/sui
   ref_<s>     each suite linked with the reference's own core sources.  Every case must
               pass on the CPU -- this pins oracle/doctest_shim (the doctest subset the
               suites use; doctest itself is vendored under proj/vendor/, absent here).
-  dropin_<s>  the suite linked through dropin/minikv_reference_adapter.cpp: the reference
-              core's hot-path symbols are weakened, so select_tokens / select_token_counts /
-              allocate_* / layer_score_variance resolve to the adapter and run on the B200
-              (libminikv_b200.so).  The selection suite is bit-exact by construction (fp32
-              score keys, lowest-index ties), so all of it must pass on the GPU.
+  dropin_<s>  the suite linked through a reference-side adapter: the reference core's
+              hot-path symbols are weakened, so they resolve to the adapter and run on the
+              B200 (libminikv_b200.so).  selection (dropin/minikv_reference_adapter.cpp:
+              select_tokens / select_token_counts / allocate_* / layer_score_variance) is
+              bit-exact by construction (fp32 score keys, lowest-index ties); harness
+              (dropin/minikv_reference_adapter_harness.cpp: the H2O baseline and persistence)
+              keeps the reference's arithmetic order.  Both must pass in full on the GPU.
 The binaries are prebuilt here and travel to the GPU box; nothing reads /root/reference
 at run time.  pipeline.cpp's <json.hpp> (nlohmann, also un-vendored) comes from the copy
 bundled with cudnn_frontend in this image.
@@ -38,11 +40,12 @@ def test_reference_suite_on_reference_core(suite):
 
 
 @pytest.mark.gpu
-def test_reference_selection_suite_through_dropin_adapter():
-    code, out = _run("dropin_selection")
+@pytest.mark.parametrize("suite", ["selection", "harness"])
+def test_reference_suite_through_dropin_adapter(suite):
+    code, out = _run(f"dropin_{suite}")
     assert code == 0, out[-4000:]
     # the full suite ran (no case aborted by an exception): same assertion count as on the CPU core
-    _, ref_out = _run("ref_selection")
+    _, ref_out = _run(f"ref_{suite}")
     count = [ln for ln in out.splitlines() if ln.startswith("[doctest-shim] assertions")]
     ref_count = [ln for ln in ref_out.splitlines() if ln.startswith("[doctest-shim] assertions")]
     assert count and count == ref_count, (count, ref_count)
