@@ -256,64 +256,68 @@ def run_mkv(args, rank, world):
     res["kernel"] = dict(name="mkv::pages_kernel", avg_launch_ms=k_ms, bytes_per_launch=page_bytes_per_launch,
                          gbs=page_bytes_per_launch / (k_ms / 1e3) / 1e9)
     # ---- e2e through the C ABI with host buffers (pinned), copies inside the timed region.
-    #      Serving-style pipelining: step s+1's inputs are copied in (H2D stream) and step
-    #      s-1's outputs copied out (D2H stream) while step s computes; double-buffered
-    #      device inputs/outputs, every dependency through CUDA events; the host reads step
-    #      s-1's result (event sync) before issuing step s+1.  Wall clock over all steps. ----
+    #      Serving-style pipelining: step s+2's inputs are copied in (H2D stream, 3 input
+    #      buffers) and step s's outputs copied out (D2H stream, 2 output buffers) while the
+    #      GPU computes; every dependency through CUDA events; the host reads step s-1's
+    #      result (event sync) before issuing step s+1.  Wall clock over all steps. ----
+    NIN, NOUT = 3, 2
     hq = qs[:, :, :, :, :].cpu().pin_memory()
     hk = ks.cpu().pin_memory()
     hv = vs.cpu().pin_memory()
-    hout = [torch.empty((NL, upl, G, d), dtype=torch.float16).pin_memory() for _ in range(2)]
-    dq = [torch.empty((NL, upl, G, d), dtype=torch.float16, device=dev) for _ in range(2)]
-    dk = [torch.empty((NL, upl, d), dtype=torch.float16, device=dev) for _ in range(2)]
-    dv = [torch.empty((NL, upl, d), dtype=torch.float16, device=dev) for _ in range(2)]
-    dout = [torch.empty((NL, upl, G, d), dtype=torch.float16, device=dev) for _ in range(2)]
-    e2e_args = []
-    for bsel in range(2):
-        arr = (_capi.DecodeArgs * NL)()
-        for l in range(NL):
-            arr[l] = _capi.DecodeArgs(l * upl, upl, G, dq[bsel][l].data_ptr(), dk[bsel][l].data_ptr(),
-                                      dv[bsel][l].data_ptr(), dout[bsel][l].data_ptr(), scale)
-        e2e_args.append(arr)
+    hout = [torch.empty((NL, upl, G, d), dtype=torch.float16).pin_memory() for _ in range(NOUT)]
+    dq = [torch.empty((NL, upl, G, d), dtype=torch.float16, device=dev) for _ in range(NIN)]
+    dk = [torch.empty((NL, upl, d), dtype=torch.float16, device=dev) for _ in range(NIN)]
+    dv = [torch.empty((NL, upl, d), dtype=torch.float16, device=dev) for _ in range(NIN)]
+    dout = [torch.empty((NL, upl, G, d), dtype=torch.float16, device=dev) for _ in range(NOUT)]
+    e2e_args = {}
+    for bi in range(NIN):
+        for bo in range(NOUT):
+            arr = (_capi.DecodeArgs * NL)()
+            for l in range(NL):
+                arr[l] = _capi.DecodeArgs(l * upl, upl, G, dq[bi][l].data_ptr(), dk[bi][l].data_ptr(),
+                                          dv[bi][l].data_ptr(), dout[bo][l].data_ptr(), scale)
+            e2e_args[bi, bo] = arr
     h2d, d2h = torch.cuda.Stream(), torch.cuda.Stream()
-    ev = lambda: torch.cuda.Event()  # noqa: E731
-    in_ready = [ev() for _ in range(2)]
-    computed = [ev() for _ in range(2)]
-    out_read = [ev() for _ in range(2)]
     e2e_steps = args.steps
+    ev = lambda: [torch.cuda.Event() for _ in range(e2e_steps)]  # noqa: E731
+    in_ready, computed, out_read = ev(), ev(), ev()
 
     def issue_h2d(s_):
-        bsel, src = s_ % 2, (args.warmup + s_) % steps_total
+        bi, src = s_ % NIN, (args.warmup + s_) % steps_total
         with torch.cuda.stream(h2d):
-            h2d.wait_event(computed[bsel])  # step s_-2 has finished reading this input buffer
-            dq[bsel].copy_(hq[src], non_blocking=True)
-            dk[bsel].copy_(hk[src], non_blocking=True)
-            dv[bsel].copy_(hv[src], non_blocking=True)
-            in_ready[bsel].record(h2d)
+            if s_ >= NIN:
+                h2d.wait_event(computed[s_ - NIN])  # the step that last read this input buffer
+            dq[bi].copy_(hq[src], non_blocking=True)
+            dk[bi].copy_(hk[src], non_blocking=True)
+            dv[bi].copy_(hv[src], non_blocking=True)
+            in_ready[s_].record(h2d)
 
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    issue_h2d(0)
+    for s in range(min(NIN - 1, e2e_steps)):
+        issue_h2d(s)
     for s in range(e2e_steps):
-        bsel = s % 2
-        stream.wait_event(in_ready[bsel])
-        stream.wait_event(out_read[bsel])  # step s-2's output has left this buffer
-        _capi.check(L_.mkv_decode_step_layers(cache.h, NL, e2e_args[bsel], sp), "decode")
-        computed[bsel].record(stream)
-        if s + 1 < e2e_steps:
-            issue_h2d(s + 1)
+        bi, bo = s % NIN, s % NOUT
+        stream.wait_event(in_ready[s])
+        if s >= NOUT:
+            stream.wait_event(out_read[s - NOUT])  # that step's output has left this buffer
+        _capi.check(L_.mkv_decode_step_layers(cache.h, NL, e2e_args[bi, bo], sp), "decode")
+        computed[s].record(stream)
+        if s + NIN - 1 < e2e_steps:
+            issue_h2d(s + NIN - 1)
         with torch.cuda.stream(d2h):
-            d2h.wait_event(computed[bsel])
-            hout[bsel].copy_(dout[bsel], non_blocking=True)
-            out_read[bsel].record(d2h)
+            d2h.wait_event(computed[s])
+            hout[bo].copy_(dout[bo], non_blocking=True)
+            out_read[s].record(d2h)
         if s >= 1:
-            out_read[(s - 1) % 2].synchronize()  # the host reads step s-1's result
-    out_read[(e2e_steps - 1) % 2].synchronize()
+            out_read[s - 1].synchronize()  # the host reads step s-1's result
+    out_read[e2e_steps - 1].synchronize()
     e2e_s = dist_max(time.perf_counter() - t0, world)
     res["e2e"] = dict(value=world * B * e2e_steps / e2e_s, unit=UNIT,
                       h2d_bytes_per_step=int(dq[0].numel() * 2 + dk[0].numel() * 2 + dv[0].numel() * 2),
                       d2h_bytes_per_step=int(dout[0].numel() * 2),
-                      pipelining="H2D of step s+1 and D2H of step s-1 overlap step s (2 copy streams, events)")
+                      pipelining="H2D of step s+2 (3 input buffers) and D2H of step s-1 overlap step s "
+                                 "(2 copy streams, events)")
     res["units"] = n_units
     res["pages"] = base_pages
     cache.close()
