@@ -11,6 +11,6 @@ ARCH="-gencode arch=compute_100a,code=sm_100a"
 FL="$ARCH -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3 -Iinclude -Xptxas -warn-spills"
 for s in decode capi; do nvcc $FL "$@" -c -o $out/$s.o paper_2411_18077_b200/csrc/$s.cu & done; wait
 objs="$out/decode.o $out/capi.o"
-for s in quant_pack select synth prefill cpp_api; do objs="$objs paper_2411_18077_b200/build/$s.o"; done
+for o in paper_2411_18077_b200/build/*.o; do case $(basename $o) in decode.o|capi.o) ;; *) objs="$objs $o";; esac; done
 nvcc $ARCH -shared -o $out/libminikv_b200.so $objs
 echo "built $out/libminikv_b200.so"
