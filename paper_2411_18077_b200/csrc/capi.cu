@@ -223,6 +223,7 @@ int mkv_h2o_dynamic_baseline(const mkv_h2o_args* a, void* stream) {
     if (a->hh_budget < 0 || a->rw_budget < 0 || a->hh_budget + a->rw_budget < 1)
         return fail(MKV_ERR_INVALID_ARGUMENT, "h2o_dynamic_baseline: budget must be >= 1");
     if (a->l_prompt < 0 || a->steps < 0 || a->d < 1) return fail(MKV_ERR_INVALID_ARGUMENT, "h2o_dynamic_baseline: bad shape");
+    if (a->d > 8192) return fail(MKV_ERR_UNSUPPORTED, "h2o_dynamic_baseline: d %d > 8192 (query staged in shared memory)", a->d);
     const int64_t total = (int64_t)a->l_prompt + a->steps;
     if (total > INT32_MAX / 2 || a->hh_budget + a->rw_budget > INT32_MAX)
         return fail(MKV_ERR_INVALID_ARGUMENT, "h2o_dynamic_baseline: too long");
