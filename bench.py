@@ -39,6 +39,21 @@ SEED = 2024
 
 CFG = dict(batch=16, layers=32, n_q_heads=32, n_kv_heads=8, head_dim=128, context=32768,
            alpha_hh=0.10, alpha_rw=0.10, pyramid_depth=7, n_r=128, group_size=16)
+# configs[4] (LWM-Text-7B, 32-head MHA, 256K context, batch 8 over 8 GPUs): one GPU's shard is one
+# sequence; `--workload lwm-7b` measures that shard (decode + the 256K MHA prefill layer)
+WORKLOADS = {
+    "llama3-8b": dict(cfg=CFG, metric=METRIC,
+                      desc="Llama-3-8B GQA decode, 32 layers, 32q/8kv heads, d=128, 32K context, "
+                           "20% pyramid budget (10% HH depth-7 + 10% RW), n_r=128, group=16",
+                      prefill=dict(name="Mistral-7B layer, 128K causal prefill (32q/8kv, d=128)", hq=32, hkv=8,
+                                   L=131072)),
+    "lwm-7b": dict(cfg=dict(CFG, batch=1, n_q_heads=32, n_kv_heads=32, context=262144),
+                   metric="2-bit-KV decode attn tokens/s (LWM-Text-7B MHA, 256K ctx, 20% pyramid budget)",
+                   desc="LWM-Text-7B MHA decode, 32 layers, 32 heads, d=128, 256K context, 20% pyramid budget "
+                        "(10% HH depth-7 + 10% RW), n_r=128, group=16; one GPU's shard of configs[4]",
+                   prefill=dict(name="LWM-Text-7B layer, 256K causal prefill (32 MHA heads, d=128)", hq=32, hkv=32,
+                                L=262144)),
+}
 
 
 def parse():
@@ -49,8 +64,12 @@ def parse():
     p.add_argument("--impl", default="mkv", choices=["mkv", "reference"])
     p.add_argument("--no-prefill", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--batch", type=int, default=CFG["batch"])
-    return p.parse_args()
+    p.add_argument("--batch", type=int, default=None)
+    p.add_argument("--workload", default="llama3-8b", choices=sorted(WORKLOADS))
+    a = p.parse_args()
+    if a.batch is None:
+        a.batch = WORKLOADS[a.workload]["cfg"]["batch"]
+    return a
 
 
 def budgets(cfg):
@@ -149,7 +168,7 @@ def run_mkv(args, rank, world):
     torch.cuda.set_device(rank % max(torch.cuda.device_count(), 1))
     dev = torch.device("cuda")
     _capi.check(_capi.lib().mkv_device_check(torch.cuda.current_device()), "device")
-    cfg = dict(CFG)
+    cfg = dict(WORKLOADS[args.workload]["cfg"])
     cfg["batch"] = args.batch
     B, NL, Hq, Hkv, d, L = cfg["batch"], cfg["layers"], cfg["n_q_heads"], cfg["n_kv_heads"], cfg["head_dim"], cfg["context"]
     G = Hq // Hkv
@@ -325,10 +344,12 @@ def run_mkv(args, rank, world):
 
 
 def run_prefill_bench(args):
-    """K1 + K2 + K3 on the Mistral-7B-shaped 128K layer (configs[3])."""
+    """K1 + K2 + K3 on the Mistral-7B-shaped 128K layer (configs[3]), or with --workload lwm-7b
+    the LWM-Text-7B 256K MHA layer (configs[4])."""
     import torch
     import paper_2411_18077_b200 as mkv
-    B, Hq, Hkv, d, L = 1, 32, 8, 128, 131072
+    pw = WORKLOADS[args.workload]["prefill"]
+    B, Hq, Hkv, d, L = 1, pw["hq"], pw["hkv"], 128, pw["L"]
     seed = SEED
     q = mkv.synth_fp16((B, Hq, L, d), seed, 1 << 48, 1 << 16)
     k = mkv.synth_fp16((B, Hkv, L, d), seed, 2 << 48, 1 << 16)
@@ -351,7 +372,7 @@ def run_prefill_bench(args):
     flops = Hq * 6 * d * P
     acs = float(r.a_cumul.double().sum().item())
     _, bf16_peak, _, _ = load_peaks()
-    out = {"workload": "Mistral-7B layer, 128K causal prefill (32q/8kv, d=128)", "ms": ms,
+    out = {"workload": pw["name"], "ms": ms,
            "tflops": flops / (ms / 1e3) / 1e12, "frac_of_bf16_peak": flops / (ms / 1e3) / 1e12 / bf16_peak,
            "flop_count": "3 GEMM-eq = 6*d*L(L+1)/2 per q-head", "a_cumul_sum_over_G_lq": acs / (Hq * L)}
     # K2 + K3 on the same layer at the 20% budget (10% HH + 10% RW): selection + gather/pack
@@ -485,16 +506,17 @@ def main():
         # ranks share one GPU (the 1-GPU validation of the N > 1 path)
         dist.init_process_group(os.environ.get("MKV_DIST_BACKEND", "nccl"))
     hbm_peak, bf16_peak, bf16_sust, peak_kind = load_peaks()
-    cfg_desc = {"workload": "Llama-3-8B GQA decode, 32 layers, 32q/8kv heads, d=128, 32K context, "
-                            "20% pyramid budget (10% HH depth-7 + 10% RW), n_r=128, group=16",
-                "batch_per_gpu": args.batch, "global_batch": args.batch * world, "context": CFG["context"],
+    W = WORKLOADS[args.workload]
+    metric = W["metric"]
+    cfg_desc = {"workload": W["desc"],
+                "batch_per_gpu": args.batch, "global_batch": args.batch * world, "context": W["cfg"]["context"],
                 "parallelism": f"dp{world} (sequence-batch shards, no collective)",
-                "l2": "inputs larger than L2 (3.4 GB of 2-bit pages per step vs 126 MB L2)"}
+                "l2": "inputs larger than L2 (GBs of 2-bit pages per step vs 126 MB L2)"}
     if args.impl == "reference":
         if rank != 0:
             return
-        ref = cpu_reference_decode(args.steps, args.warmup)
-        line = {"metric": METRIC, "value": ref["value"], "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+        ref = cpu_reference_decode(args.steps, args.warmup, cfg=dict(W["cfg"], batch=args.batch))
+        line = {"metric": metric, "value": ref["value"], "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * args.batch / ref["value"],
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
                 "data": "synthetic (integer-exact N(0,1) fp16 K/V, uniform A_cumul)", "config": cfg_desc,
@@ -514,7 +536,7 @@ def main():
         try:
             import oracle
             if oracle.ref_available():
-                cpu = cpu_reference_decode(steps=3, warmup=1)
+                cpu = cpu_reference_decode(steps=3, warmup=1, cfg=dict(W["cfg"], batch=args.batch))
             else:
                 cpu = {"unavailable": "oracle/_ref not built"}
         except Exception as e:
@@ -523,14 +545,15 @@ def main():
         return
     kern = res["kernel"]
     line = {
-        "metric": METRIC, "value": res["tokens_per_s"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "metric": metric, "value": res["tokens_per_s"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": res["ms_per_step"], "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "fp16 (2-bit codes, fp16 params, fp32 accumulate)",
         "data": "synthetic (integer-exact N(0,1) fp16 K/V/q, uniform A_cumul), random-init shapes",
         "config": cfg_desc,
         "hbm_gbs": res["hbm_gbs"],
         "roofline": {"bound": "hbm", "achieved": kern["gbs"], "peak": hbm_peak, "unit": "GB/s",
-                     "frac": kern["gbs"] / hbm_peak, "traffic": load_traffic(kern["name"]),
+                     "frac": kern["gbs"] / hbm_peak,
+                     "traffic": load_traffic(kern["name"]) if args.workload == "llama3-8b" else None,
                      "traffic_source": "profiles/r1_pages_traffic.json (ncu dram__bytes_read+write, mean of "
                                        "the 32 per-layer launches of one step)", "kernel": kern["name"],
                      "avg_launch_ms": kern["avg_launch_ms"], "bytes_per_launch": kern["bytes_per_launch"],

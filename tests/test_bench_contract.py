@@ -45,3 +45,11 @@ def test_b200_arm_line():
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] > 0
     assert "workload" in d["config"]
+
+
+@pytest.mark.gpu
+def test_b200_arm_lwm_shard_line():
+    """configs[4]'s per-GPU shard (one LWM-Text-7B sequence, 32 MHA heads, 256K context)."""
+    d = _line(["--workload", "lwm-7b", "--steps", "3", "--warmup", "3", "--no-prefill", "--no-cpu-baseline"])
+    assert "LWM-Text-7B" in d["metric"] and d["config"]["context"] == 262144 and d["config"]["batch_per_gpu"] == 1
+    assert d["value"] > 0 and 0.2 < d["roofline"]["frac"] < 1.05
