@@ -531,10 +531,10 @@ cudaError_t launch_append(const ResidualParams& p, cudaStream_t s) {
 // finish kernel: (append) + residual attention on tensor cores + split-K merge
 // ---------------------------------------------------------------------------
 // Finish kernel (one CTA per unit, launched with PDL): decode_append and the exact fp16
-// residual attention first, then -- after griddepcontrol.wait -- a single-round split-K
-// merge of the residual and page partials (online max, no extra barriers).
+// residual attention first, then -- after griddepcontrol.wait -- the split-K merge of the
+// residual and page partials (online max over kMergeBatch partials at a time, no extra barriers).
 // 4 warps at <= 96 registers and 33 KB of shared memory: a finish CTA fits on an SM beside a
-// page-kernel CTA (208 x 256 registers, 141 KB), so layer l's finish runs its residual
+// page-kernel CTA (<= 208 x 256 registers, 150 KB), so layer l's finish runs its residual
 // attention while layer l's pages are still in flight and layer l + 1's pages overlap its merge.
 constexpr int kFinishWarps = 4;
 constexpr int kMergeBatch = 8;  // page partials folded per online-max round
