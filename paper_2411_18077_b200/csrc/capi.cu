@@ -83,6 +83,8 @@ struct Plan {
     int32_t* d_pref = nullptr;    // [n_units + 1] local page prefix, then [warps] first unit per warp
     int32_t* d_wstart = nullptr;
     UnitRec* d_rec = nullptr;     // [n_units]
+    float* d_part_ml = nullptr;   // this range's page partials (slot = warp + unit), private to the plan
+    float* d_part_o = nullptr;
 };
 
 struct mkv_cache {
@@ -99,18 +101,20 @@ struct mkv_cache {
     __half* d_res_k = nullptr;
     __half* d_res_v = nullptr;
     uint32_t* d_status = nullptr;
-    float* d_part_ml = nullptr;
-    float* d_part_o = nullptr;
     uint64_t* d_trace = nullptr;  // diagnostics only (MKV_DECODE_TRACE)
     uint64_t trace_seq = 0;
-    int part_slots = 0;
+    int part_slots = 0;  // upper bound of page-partial slots per plan (each plan owns its buffers)
     std::unordered_map<uint64_t, Plan> plans;  // key: (unit_begin, n_units)
 
     ~mkv_cache() {
-        for (auto& kv : plans) cudaFree(kv.second.d_pref);
+        for (auto& kv : plans) {
+            cudaFree(kv.second.d_pref);
+            cudaFree(kv.second.d_part_ml);
+            cudaFree(kv.second.d_part_o);
+        }
         cudaFree(d_meta); cudaFree(d_pool); cudaFree(d_shadow); cudaFree(d_res_k); cudaFree(d_res_v);
         cudaFree(d_status);
-        cudaFree(d_part_ml); cudaFree(d_part_o); cudaFree(d_trace);
+        cudaFree(d_trace);
     }
 
     UnitMeta meta_of(int u) const {
@@ -368,8 +372,6 @@ int mkv_cache_create(const mkv_cache_config* cfg, mkv_cache** out) {
     if (e == cudaSuccess) e = al((void**)&c->d_res_k, (size_t)n * c->n_r * c->d * sizeof(__half));
     if (e == cudaSuccess) e = al((void**)&c->d_res_v, (size_t)n * c->n_r * c->d * sizeof(__half));
     if (e == cudaSuccess) e = al((void**)&c->d_status, sizeof(uint32_t));
-    if (e == cudaSuccess) e = al((void**)&c->d_part_ml, sizeof(float) * 2 * kMaxG * c->part_slots);
-    if (e == cudaSuccess) e = al((void**)&c->d_part_o, sizeof(float) * kMaxG * kHeadDim * c->part_slots);
     if (e == cudaSuccess) e = cudaMemset(c->d_status, 0, sizeof(uint32_t));
     if (e == cudaSuccess) e = cudaMemset(c->d_pool, 0, (size_t)acc * kPageBytes);
     if (e == cudaSuccess) e = c->upload_meta(0, n, 0);
@@ -397,7 +399,7 @@ int mkv_cache_bytes(const mkv_cache* c, uint64_t* page_bytes, uint64_t* residual
     if (page_bytes) *page_bytes = pb;
     if (residual_bytes) *residual_bytes = rb;
     if (total) *total = pb + rb + (c->shadow ? (uint64_t)c->total_pages * kShadowBytes : 0) +
-                        (uint64_t)c->part_slots * kMaxG * (kHeadDim + 2) * 4;
+                        (uint64_t)c->plans.size() * c->part_slots * kMaxG * (kHeadDim + 2) * 4;
     return MKV_OK;
 }
 
@@ -543,7 +545,12 @@ static int get_plan(mkv_cache* c, int ub, int n, cudaStream_t s, Plan** out) {
         rec[i].rend = pref[i] + c->n_pages[u];
         rec[i].n_prefill = c->n_prefill[u];
     }
-    if (!pl.d_pref) CK(cudaMalloc(&pl.d_pref, sizeof(int32_t) * ints + sizeof(UnitRec) * c->n_units));
+    if (!pl.d_pref) {
+        CK(cudaMalloc(&pl.d_pref, sizeof(int32_t) * ints + sizeof(UnitRec) * c->n_units));
+        const size_t slots = (size_t)num_sms() * kMaxPagesWarps + n;  // slot = warp + local unit
+        CK(cudaMalloc(&pl.d_part_ml, sizeof(float) * 2 * kMaxG * slots));
+        CK(cudaMalloc(&pl.d_part_o, sizeof(float) * kMaxG * kHeadDim * slots));
+    }
     CK(cudaMemcpyAsync(pl.d_pref, buf.data(), sizeof(int32_t) * buf.size(), cudaMemcpyHostToDevice, s));
     pl.d_rec = reinterpret_cast<UnitRec*>(pl.d_pref + ints);
     CK(cudaMemcpyAsync(pl.d_rec, rec.data(), sizeof(UnitRec) * n, cudaMemcpyHostToDevice, s));
@@ -574,7 +581,7 @@ static void fill_pages_params(mkv_cache* c, const Plan* pl, const mkv_decode_arg
     pp.group = a->group; pp.q = static_cast<const __half*>(a->q);
     pp.pref = pl->d_pref; pp.wstart = pl->d_wstart; pp.rec = pl->d_rec; pp.chunk = pl->chunk; pp.total_pages = pl->total;
     pp.n_warps = pl->grid * pages_config().warps;
-    pp.part_ml = c->d_part_ml; pp.part_o = c->d_part_o;
+    pp.part_ml = pl->d_part_ml; pp.part_o = pl->d_part_o;
     pp.scale_log2 = a->scale * 1.4426950408889634f;
     pp.trace = trace_slot(c);
     pp.early = 0;
@@ -622,7 +629,7 @@ static int decode_impl(mkv_cache* c, const mkv_decode_args* a, bool attend, cuda
     rp.k_new = static_cast<const __half*>(a->k_new);
     rp.v_new = static_cast<const __half*>(a->v_new);
     rp.res_k = c->d_res_k; rp.res_v = c->d_res_v; rp.pool = c->d_pool; rp.shadow = c->d_shadow;
-    rp.part_ml = c->d_part_ml; rp.part_o = c->d_part_o; rp.out = static_cast<__half*>(a->out);
+    rp.out = static_cast<__half*>(a->out);
     rp.scale_log2 = a->scale * 1.4426950408889634f;
     rp.status = c->d_status;
     rp.trace = nullptr;
@@ -641,6 +648,7 @@ static int decode_impl(mkv_cache* c, const mkv_decode_args* a, bool attend, cuda
         pp.early = early && !any_flush ? 1 : 0;
         CK(launch_pages(pp, pl->grid, s));
     }
+    rp.part_ml = pl->d_part_ml; rp.part_o = pl->d_part_o;
     rp.trace = trace_slot(c);
     if (rp.trace) rp.trace += 4 * (size_t)num_sms() * kMaxPagesWarps;
     CK(launch_finish(rp, pl->d_pref, std::max(pl->chunk, 1), pl->total > 0, s));
@@ -679,8 +687,16 @@ int mkv_decode_pages_only(mkv_cache* c, const mkv_decode_args* a, void* stream) 
 
 int mkv_decode_step_layers(mkv_cache* c, int n_layers, const mkv_decode_args* a, void* stream) {
     if (!a || n_layers < 0) return fail(MKV_ERR_INVALID_ARGUMENT, "decode_step: bad layer list");
-    for (int l = 0; l < n_layers; ++l)
-        if (int r = decode_impl(c, a + l, true, static_cast<cudaStream_t>(stream), l > 0)) return r;
+    // a layer skips the early wait only if no earlier layer of this call used its unit range
+    // (plan, and so partial buffers); otherwise it waits for the previous finish kernel
+    thread_local std::vector<std::pair<int, int>> seen;
+    seen.clear();
+    for (int l = 0; l < n_layers; ++l) {
+        const std::pair<int, int> key(a[l].unit_begin, a[l].n_units);
+        const bool repeat = std::find(seen.begin(), seen.end(), key) != seen.end();
+        seen.push_back(key);
+        if (int r = decode_impl(c, a + l, true, static_cast<cudaStream_t>(stream), l > 0 && !repeat)) return r;
+    }
     return MKV_OK;
 }
 

@@ -199,12 +199,13 @@ __global__ void __maxnreg__(208) pages_kernel(const PagesParams P) {
     // writes these pages (the append kernel of a flush step is a full-dependency launch)
     // or the plan/meta fields read here; q is read and partials are written after the wait.
     for (int s = 0; s < kStages; ++s) issue(s);
-    // P.early (every layer of a multi-layer call but the first): q is an input of the call,
-    // so the whole page pass may run while the previous layer's finish kernel is still
-    // merging; the only conflict is the partial buffers that kernel reads, so the wait
-    // moves to the first partial write.  Otherwise wait here, before touching q.
-    bool waited = !P.early;
-    if (waited) asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    // P.early (every layer of a multi-layer call but the first): q is an input of the call and
+    // the partial buffers belong to this layer's plan, so the whole page pass may run while the
+    // previous layer's finish kernel is still merging; the wait moves to the kernel's end (it
+    // orders this grid's completion after that kernel's, which keeps the launch chain from
+    // running ahead and makes the next call's first kernel wait for every merge).  Otherwise
+    // wait here, before touching q.
+    if (!P.early) asm volatile("griddepcontrol.wait;\n" ::: "memory");
     if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     stamp(1);
     prefetch_q(ci);
@@ -397,10 +398,6 @@ __global__ void __maxnreg__(208) pages_kernel(const PagesParams P) {
             l0 += __shfl_xor_sync(0xffffffffu, l0, o);
             l1 += __shfl_xor_sync(0xffffffffu, l1, o);
         }
-        if (!waited) {  // the previous layer's finish kernel has read the partial buffers
-            asm volatile("griddepcontrol.wait;\n" ::: "memory");
-            waited = true;
-        }
         const int slot = wg + unit;
         float* pml = P.part_ml + (size_t)slot * 2 * kMaxG;
         float* po = P.part_o + (size_t)slot * kMaxG * kHeadDim;
@@ -426,6 +423,7 @@ __global__ void __maxnreg__(208) pages_kernel(const PagesParams P) {
         }
     }
     stamp(2);
+    if (P.early) asm volatile("griddepcontrol.wait;\n" ::: "memory");
 }
 
 template <int W, int S>
