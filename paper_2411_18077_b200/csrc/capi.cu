@@ -589,6 +589,30 @@ static void fill_pages_params(mkv_cache* c, const Plan* pl, const mkv_decode_arg
 
 // early: a later layer of one mkv_decode_step_layers call -- its q was written before the
 // call, so the page kernel may read it while the previous layer's finish kernel still runs
+// argument / capacity checks of one decode call (no state change)
+static int decode_validate(mkv_cache* c, const mkv_decode_args* a, bool attend) {
+    const int ub = a->unit_begin, n = a->n_units;
+    if (int r = check_range(c, ub, n)) return r;
+    if (n == 0) return MKV_OK;
+    const bool append = a->k_new != nullptr;
+    if (append && !a->v_new) return fail(MKV_ERR_INVALID_ARGUMENT, "decode_append: null v");
+    if (attend) {
+        if (a->group < 1 || a->group > kMaxG) return fail(MKV_ERR_UNSUPPORTED, "decode: group %d outside 1..8", a->group);
+        if (!a->q || !a->out) return fail(MKV_ERR_INVALID_ARGUMENT, "decode: null q/out");
+        if (!aligned16(a->q) || !aligned16(a->out)) return fail(MKV_ERR_INVALID_ARGUMENT, "decode: q/out must be 16-byte aligned");
+    }
+    if (append && (!aligned16(a->k_new) || !aligned16(a->v_new)))
+        return fail(MKV_ERR_INVALID_ARGUMENT, "decode_append: k/v must be 16-byte aligned");
+    for (int i = 0; i < n; ++i) {
+        const int u = ub + i;
+        const int64_t total = (int64_t)c->n_pages[u] + c->n_res[u];
+        if (attend && total == 0) return fail(MKV_ERR_RUNTIME, "decode_step: empty cache (unit %d)", u);
+        if (append && c->n_res[u] + 1 == c->n_r && c->n_pages[u] + c->n_r / kGroup > c->cap_pages[u])
+            return fail(MKV_ERR_OUT_OF_RANGE, "decode: unit %d exceeds max_decode_tokens", u);
+    }
+    return MKV_OK;
+}
+
 static int decode_impl(mkv_cache* c, const mkv_decode_args* a, bool attend, cudaStream_t s, bool early = false) {
     const int ub = a->unit_begin, n = a->n_units;
     if (int r = check_range(c, ub, n)) return r;
@@ -687,15 +711,68 @@ int mkv_decode_pages_only(mkv_cache* c, const mkv_decode_args* a, void* stream) 
 
 int mkv_decode_step_layers(mkv_cache* c, int n_layers, const mkv_decode_args* a, void* stream) {
     if (!a || n_layers < 0) return fail(MKV_ERR_INVALID_ARGUMENT, "decode_step: bad layer list");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
     // a layer skips the early wait only if no earlier layer of this call used its unit range
     // (plan, and so partial buffers); otherwise it waits for the previous finish kernel
     thread_local std::vector<std::pair<int, int>> seen;
     seen.clear();
+    bool unique = true, all_append = n_layers > 1 && n_layers <= kMaxAppendSegs, flush = false;
     for (int l = 0; l < n_layers; ++l) {
         const std::pair<int, int> key(a[l].unit_begin, a[l].n_units);
-        const bool repeat = std::find(seen.begin(), seen.end(), key) != seen.end();
+        unique = unique && std::find(seen.begin(), seen.end(), key) == seen.end();
         seen.push_back(key);
-        if (int r = decode_impl(c, a + l, true, static_cast<cudaStream_t>(stream), l > 0 && !repeat)) return r;
+        all_append = all_append && a[l].k_new != nullptr && a[l].n_units > 0;
+    }
+    // A flush step with every layer appending: validate everything, update the mirror, upload the
+    // changed plans, then append + flush every layer's units in ONE launch, so the per-layer
+    // kernels that follow carry no append launches or copies between them.
+    if (unique && all_append) {
+        for (int l = 0; l < n_layers && !flush; ++l)
+            for (int i = 0; i < a[l].n_units && !flush; ++i) {
+                const int u = a[l].unit_begin + i;
+                if (u >= 0 && u < c->n_units && c->n_res[u] + 1 == c->n_r) flush = true;
+            }
+    }
+    if (unique && all_append && flush) {
+        for (int l = 0; l < n_layers; ++l)
+            if (int r = decode_validate(c, a + l, true)) return r;
+        if (int r = require_device()) return r;
+        AppendSegs segs{};
+        segs.n_seg = n_layers;
+        for (int l = 0; l < n_layers; ++l) {
+            for (int i = 0; i < a[l].n_units; ++i) {
+                const int u = a[l].unit_begin + i;
+                if (++c->n_res[u] == c->n_r) {
+                    c->n_res[u] = 0;
+                    c->n_pages[u] += c->n_r / kGroup;
+                    c->n_blocks[u] += 1;
+                }
+            }
+            segs.block_begin[l + 1] = segs.block_begin[l] + a[l].n_units;
+            segs.unit_begin[l] = a[l].unit_begin;
+            segs.k_new[l] = static_cast<const __half*>(a[l].k_new);
+            segs.v_new[l] = static_cast<const __half*>(a[l].v_new);
+        }
+        for (int l = 0; l < n_layers; ++l) {
+            Plan* pl = nullptr;
+            if (int r = get_plan(c, a[l].unit_begin, a[l].n_units, s, &pl)) return r;
+        }
+        ResidualParams rp{};
+        rp.meta = c->d_meta; rp.n_r = c->n_r; rp.res_k = c->d_res_k; rp.res_v = c->d_res_v;
+        rp.pool = c->d_pool; rp.shadow = c->d_shadow; rp.status = c->d_status;
+        CK(launch_append_segments(rp, segs, s));
+        for (int l = 0; l < n_layers; ++l) {
+            mkv_decode_args al = a[l];
+            al.k_new = nullptr;  // appended above
+            al.v_new = nullptr;
+            if (int r = decode_impl(c, &al, true, s, l > 0)) return r;
+        }
+        return MKV_OK;
+    }
+    for (int l = 0; l < n_layers; ++l) {
+        const std::pair<int, int> key(a[l].unit_begin, a[l].n_units);
+        const bool repeat = std::find(seen.begin(), seen.begin() + l, key) != seen.begin() + l;
+        if (int r = decode_impl(c, a + l, true, s, l > 0 && !repeat)) return r;
     }
     return MKV_OK;
 }

@@ -467,22 +467,34 @@ cudaError_t launch_pages(const PagesParams& p, int grid, cudaStream_t s) {
 // ---------------------------------------------------------------------------
 constexpr int kAppendThreads = 256;
 
-__global__ void __launch_bounds__(kAppendThreads) append_kernel(const ResidualParams P) {
+// One CTA per unit.  S.n_seg == 0: the units of P (unit_begin + block, tokens P.k_new /
+// P.v_new); otherwise segment s covers blocks [S.block_begin[s], S.block_begin[s + 1]) with its
+// own unit range and token arrays (every layer of a multi-layer call in one launch).
+__global__ void __launch_bounds__(kAppendThreads) append_kernel(const ResidualParams P, const AppendSegs S) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
     PageScratch* scratch = reinterpret_cast<PageScratch*>(smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = lane_id();
-    const int i = blockIdx.x;
-    const int u = P.unit_begin + i;
+    int i = blockIdx.x, u = P.unit_begin + i;
+    const __half* k_new = P.k_new;
+    const __half* v_new = P.v_new;
+    if (S.n_seg > 0) {
+        int sg = 0;
+        while (sg + 1 < S.n_seg && S.block_begin[sg + 1] <= (int)blockIdx.x) ++sg;
+        i = blockIdx.x - S.block_begin[sg];
+        u = S.unit_begin[sg] + i;
+        k_new = S.k_new[sg];
+        v_new = S.v_new[sg];
+    }
     const int d = kHeadDim;
     const UnitMeta meta = P.meta[u];
     __half* rk = P.res_k + (size_t)u * P.n_r * d;
     __half* rv = P.res_v + (size_t)u * P.n_r * d;
     const int n = meta.n_res + 1;
     if (tid < 16) {
-        reinterpret_cast<uint4*>(rk + (size_t)meta.n_res * d)[tid] = reinterpret_cast<const uint4*>(P.k_new + (size_t)i * d)[tid];
+        reinterpret_cast<uint4*>(rk + (size_t)meta.n_res * d)[tid] = reinterpret_cast<const uint4*>(k_new + (size_t)i * d)[tid];
     } else if (tid < 32) {
         reinterpret_cast<uint4*>(rv + (size_t)meta.n_res * d)[tid - 16] =
-            reinterpret_cast<const uint4*>(P.v_new + (size_t)i * d)[tid - 16];
+            reinterpret_cast<const uint4*>(v_new + (size_t)i * d)[tid - 16];
     }
     __threadfence_block();
     __syncthreads();
@@ -513,15 +525,30 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(const ResidualPa
     }
 }
 
-cudaError_t launch_append(const ResidualParams& p, cudaStream_t s) {
-    const size_t smem = sizeof(PageScratch) * (kAppendThreads / 32);
+static cudaError_t append_configure(size_t smem) {
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(append_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    append_kernel<<<p.n_units, kAppendThreads, smem, s>>>(p);
+    return cudaSuccess;
+}
+
+cudaError_t launch_append(const ResidualParams& p, cudaStream_t s) {
+    const size_t smem = sizeof(PageScratch) * (kAppendThreads / 32);
+    if (cudaError_t e = append_configure(smem)) return e;
+    AppendSegs none{};
+    append_kernel<<<p.n_units, kAppendThreads, smem, s>>>(p, none);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_append_segments(const ResidualParams& p, const AppendSegs& segs, cudaStream_t s) {
+    const size_t smem = sizeof(PageScratch) * (kAppendThreads / 32);
+    if (cudaError_t e = append_configure(smem)) return e;
+    const int blocks = segs.block_begin[segs.n_seg];
+    if (blocks == 0) return cudaSuccess;
+    append_kernel<<<blocks, kAppendThreads, smem, s>>>(p, segs);
     return cudaGetLastError();
 }
 

@@ -63,6 +63,16 @@ struct ResidualParams {
 };
 constexpr int kTraceFinishCtas = 8192;  // finish-kernel CTAs recorded per trace slot
 cudaError_t launch_append(const ResidualParams& p, cudaStream_t s);
+// every layer of one multi-layer decode call appended (and flushed) by one launch
+constexpr int kMaxAppendSegs = 32;
+struct AppendSegs {
+    int n_seg;
+    int block_begin[kMaxAppendSegs + 1];
+    int unit_begin[kMaxAppendSegs];
+    const __half* k_new[kMaxAppendSegs];
+    const __half* v_new[kMaxAppendSegs];
+};
+cudaError_t launch_append_segments(const ResidualParams& p, const AppendSegs& segs, cudaStream_t s);
 cudaError_t launch_finish(const ResidualParams& p, const int32_t* pref, int chunk, bool after_pages, cudaStream_t s);
 
 // Per-unit page-run record of a K4 plan (host-computed from the cache mirror).
