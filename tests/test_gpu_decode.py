@@ -207,3 +207,40 @@ def test_decode_step_layers_matches_per_layer_calls(mkv):
     for c in caches:
         c.check()
     assert caches[0].unit_info(0) == caches[1].unit_info(0)
+
+
+def test_decode_step_layers_partial_flush_matches_per_layer_calls(mkv):
+    """The fused flush path of mkv_decode_step_layers (one append launch for every layer) with
+    only some layers' units reaching n_r in a step: bit-identical to per-layer calls."""
+    d, n, G, L, layers, n_r = 128, 8, 4, 700, 4, 16
+    rng = np.random.default_rng(33)
+    budgets = [300, 30, 200, 90]
+    caps = [budgets[l] + 32 for l in range(layers) for _ in range(n)]
+    k = torch.from_numpy(rng.standard_normal((layers * n, L, d)).astype(np.float16)).cuda()
+    v = torch.from_numpy(rng.standard_normal((layers * n, L, d)).astype(np.float16)).cuda()
+    a = torch.from_numpy(rng.random((layers * n, L)).astype(np.float32)).cuda()
+    caches = []
+    for _ in range(2):
+        c = mkv.KVCache(layers * n, caps, max_decode_tokens=96, n_r=n_r)
+        for l in range(layers):
+            c.prefill(k[l * n:(l + 1) * n], v[l * n:(l + 1) * n], a[l * n:(l + 1) * n], budgets[l], 32,
+                      unit_begin=l * n)
+        # stagger the residual counts: layer l starts with 3 l extra tokens
+        for l in range(layers):
+            for t in range(3 * l):
+                c.append(*(2 * [torch.full((n, d), 0.01 * (t + 1), dtype=torch.float16, device="cuda")]),
+                         unit_begin=l * n)
+        caches.append(c)
+    scale = 1.0 / np.sqrt(d)
+    for s in range(40):  # flushes hit different layers at different steps
+        q = torch.from_numpy(rng.standard_normal((layers, n, G, d)).astype(np.float16)).cuda()
+        tk = torch.from_numpy(rng.standard_normal((layers, n, d)).astype(np.float16)).cuda()
+        tv = torch.from_numpy(rng.standard_normal((layers, n, d)).astype(np.float16)).cuda()
+        fused = caches[0].decode_step_layers(q, tk, tv, scale)
+        ref = torch.stack([caches[1].decode_step(q[l], tk[l], tv[l], scale, unit_begin=l * n)
+                           for l in range(layers)])
+        assert torch.equal(fused, ref), f"step {s}: max diff {(fused.float() - ref.float()).abs().max()}"
+    for c in caches:
+        c.check()
+    for u in range(0, layers * n, n):
+        assert caches[0].unit_info(u) == caches[1].unit_info(u)
