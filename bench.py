@@ -374,9 +374,16 @@ def run_prefill_bench(args):
     flops = Hq * 6 * d * P
     acs = float(r.a_cumul.double().sum().item())
     _, bf16_peak, _, _ = load_peaks()
+    # exponentials: 2 per visible (query, key) pair (pass 1 and the A_cumul pass); the SFU
+    # (MUFU.EX2) bound is 16 per clock per SM on B200 -- part of them run as FMA polynomials
+    exps = 2.0 * Hq * P
+    mufu_peak = 16.0 * torch.cuda.get_device_properties(0).multi_processor_count * 1.965e9
     out = {"workload": pw["name"], "ms": ms,
            "tflops": flops / (ms / 1e3) / 1e12, "frac_of_bf16_peak": flops / (ms / 1e3) / 1e12 / bf16_peak,
-           "flop_count": "3 GEMM-eq = 6*d*L(L+1)/2 per q-head", "a_cumul_sum_over_G_lq": acs / (Hq * L)}
+           "flop_count": "3 GEMM-eq = 6*d*L(L+1)/2 per q-head", "a_cumul_sum_over_G_lq": acs / (Hq * L),
+           "exp_per_s": exps / (ms / 1e3), "exp_frac_of_mufu_peak": exps / (ms / 1e3) / mufu_peak,
+           "exp_count": "2 per visible pair (pass 1 + A_cumul pass); MUFU peak 16/clk/SM at 1965 MHz, "
+                        "a share of them evaluated on the FMA pipe (MKV_PREFILL_POLY)"}
     # K2 + K3 on the same layer at the 20% budget (10% HH + 10% RW): selection + gather/pack
     hh = rw = int(math.floor(0.10 * L))
     ac = r.a_cumul.view(Hkv, L)
