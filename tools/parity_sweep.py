@@ -3,7 +3,7 @@ decode (random unit counts, GQA groups, n_r, budgets, step counts), K2 selection
 and tie-heavy scores, K3 codes/params through the reference-format export, all against the
 oracle.  Prints one line per family with the case count and the worst deviation.
 
-usage: python tools/parity_sweep.py [n_decode] [n_select] [n_pack]
+usage: python tools/parity_sweep.py [n_decode] [n_select] [n_pack] [n_prefill]
 """
 import os
 import sys
@@ -15,10 +15,13 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import oracle  # noqa: E402
 import paper_2411_18077_b200 as mkv  # noqa: E402
 from tests.test_gpu_decode import TOL, run_decode  # noqa: E402
+from tests.test_gpu_prefill import TOL_A_ABS, TOL_A_REL, TOL_LSE, TOL_O, make_inputs  # noqa: E402
+from tests.gpu_util import f32  # noqa: E402
 
 nd = int(sys.argv[1]) if len(sys.argv) > 1 else 60
 ns = int(sys.argv[2]) if len(sys.argv) > 2 else 300
 npk = int(sys.argv[3]) if len(sys.argv) > 3 else 100
+npf = int(sys.argv[4]) if len(sys.argv) > 4 else 40
 P = oracle.port()
 
 # ---- K4 decode ----
@@ -78,3 +81,38 @@ for seed in range(npk):
         fails += not (np.array_equal(w, ow) and np.array_equal(par, opar) and np.array_equal(br, obr))
     cache.close()
 print(f"K3 pack: {npk} random prefills (scales 1e-3..1e2), K and V streams compared, mismatches {fails}")
+
+# ---- K1 prefill (X_O, LSE, A_cumul within the suite's tolerances) ----
+import math  # noqa: E402
+worst = {"o": 0.0, "lse": 0.0, "a_excess": 0.0}
+fails = 0
+for seed in range(npf):
+    rng = np.random.default_rng(70000 + seed)
+    B, Hkv, G = int(rng.integers(1, 3)), int(rng.integers(1, 3)), int(rng.choice([1, 2, 4]))
+    causal = bool(rng.integers(0, 2))
+    lq = int(rng.integers(1, 700))
+    lk = lq + int(rng.integers(0, 300)) if causal else int(rng.integers(1, 1000))
+    q, k, v = make_inputs(B, Hkv * G, Hkv, lq, lk, seed=7 + seed)
+    scale = 1.0 / math.sqrt(128)
+    r = mkv.selective_flash_attn(torch.from_numpy(q).cuda(), torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda(),
+                                 scale, causal)
+    out, lse, ac = r.output.float().cpu().numpy(), r.lse.cpu().numpy(), r.a_cumul.cpu().numpy()
+    ok = True
+    for b in range(B):
+        for hk in range(Hkv):
+            acc = None
+            for g in range(G):
+                h = hk * G + g
+                ref = P.selective_flash_attn(f32(q[b, h]), f32(k[b, hk]), f32(v[b, hk]), scale, causal, 64, 64)
+                eo = float(np.max(np.abs(out[b, h] - ref.output)))
+                el = float(np.max(np.abs(lse[b, h] - ref.lse)))
+                worst["o"], worst["lse"] = max(worst["o"], eo), max(worst["lse"], el)
+                ok &= eo <= TOL_O and el <= TOL_LSE
+                acc = ref.a_cumul.copy() if acc is None else acc + ref.a_cumul
+            ex = float(np.max(np.abs(ac[b, hk] - acc) - (TOL_A_ABS + TOL_A_REL * np.abs(acc))))
+            worst["a_excess"] = max(worst["a_excess"], ex) if worst["a_excess"] else ex
+            ok &= ex <= 0
+    fails += not ok
+print(f"K1 prefill: {npf} random shapes (B, GQA group, causal / not, lq <= lk), worst |X_O| {worst['o']:.2e} "
+      f"(tol {TOL_O}), |LSE| {worst['lse']:.2e} (tol {TOL_LSE}), A_cumul max(err - tol) {worst['a_excess']:.2e} "
+      f"(<= 0 passes), failures {fails}")
