@@ -254,9 +254,9 @@ def run_mkv(args, rank, world):
     res = dict(ms_per_step=ms_per_step, tokens_per_s=tokens_per_s,
                hbm_gbs=bytes_timed / (ms / 1e3) / 1e9 * world, clocks=clk.summary(), setup_s=setup_s,
                # per step: a page kernel + a finish kernel per layer; a flush step adds ONE append
-               # launch for every layer (mkv_decode_step_layers' fused flush)
-               gpu_launches=args.steps * NL * 2 + sum(1 for s in range(args.warmup, steps_total)
-                                                      if (preroll + s + 1) % n_r == 0),
+               # launch for every layer and one plan-build launch (mkv_decode_step_layers)
+               gpu_launches=args.steps * NL * 2 + 2 * sum(1 for s in range(args.warmup, steps_total)
+                                                          if (preroll + s + 1) % n_r == 0),
                preroll=preroll,
                flushes_in_timed=sum(1 for s in range(args.warmup, steps_total) if (preroll + s + 1) % n_r == 0))
     # ---- dominant kernel alone (K4 page kernel), CUDA events on its stream ----

@@ -507,7 +507,9 @@ static void range_signature(const mkv_cache* c, int ub, int n, std::vector<int32
     }
 }
 
-static int get_plan(mkv_cache* c, int ub, int n, cudaStream_t s, Plan** out) {
+// jobs != nullptr: a changed plan is not uploaded but queued for plan_build_kernel (the
+// caller launches it once the device meta holds the new page counts)
+static int get_plan(mkv_cache* c, int ub, int n, cudaStream_t s, Plan** out, PlanBuildJobs* jobs = nullptr) {
     const uint64_t key = ((uint64_t)(uint32_t)ub << 32) | (uint32_t)n;
     Plan& pl = c->plans[key];
     thread_local std::vector<int32_t> sig;
@@ -551,10 +553,16 @@ static int get_plan(mkv_cache* c, int ub, int n, cudaStream_t s, Plan** out) {
         CK(cudaMalloc(&pl.d_part_ml, sizeof(float) * 2 * kMaxG * slots));
         CK(cudaMalloc(&pl.d_part_o, sizeof(float) * kMaxG * kHeadDim * slots));
     }
-    CK(cudaMemcpyAsync(pl.d_pref, buf.data(), sizeof(int32_t) * buf.size(), cudaMemcpyHostToDevice, s));
     pl.d_rec = reinterpret_cast<UnitRec*>(pl.d_pref + ints);
-    CK(cudaMemcpyAsync(pl.d_rec, rec.data(), sizeof(UnitRec) * n, cudaMemcpyHostToDevice, s));
     pl.d_wstart = pl.d_pref + n + 1;
+    if (jobs && jobs->n_jobs < kMaxPlanJobs && n > 0) {
+        PlanBuildJob& jb = jobs->job[jobs->n_jobs++];
+        jb.unit_begin = ub; jb.n = n; jb.chunk = chunk; jb.warps = warps;
+        jb.pref = pl.d_pref; jb.wstart = pl.d_wstart; jb.rec = pl.d_rec;
+    } else {
+        CK(cudaMemcpyAsync(pl.d_pref, buf.data(), sizeof(int32_t) * buf.size(), cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(pl.d_rec, rec.data(), sizeof(UnitRec) * n, cudaMemcpyHostToDevice, s));
+    }
     pl.sig = sig;
     pl.total = total;
     pl.chunk = chunk;
@@ -753,14 +761,17 @@ int mkv_decode_step_layers(mkv_cache* c, int n_layers, const mkv_decode_args* a,
             segs.k_new[l] = static_cast<const __half*>(a[l].k_new);
             segs.v_new[l] = static_cast<const __half*>(a[l].v_new);
         }
+        // changed plans are built on the device from the meta the append kernel updates
+        PlanBuildJobs jobs{};
         for (int l = 0; l < n_layers; ++l) {
             Plan* pl = nullptr;
-            if (int r = get_plan(c, a[l].unit_begin, a[l].n_units, s, &pl)) return r;
+            if (int r = get_plan(c, a[l].unit_begin, a[l].n_units, s, &pl, &jobs)) return r;
         }
         ResidualParams rp{};
         rp.meta = c->d_meta; rp.n_r = c->n_r; rp.res_k = c->d_res_k; rp.res_v = c->d_res_v;
         rp.pool = c->d_pool; rp.shadow = c->d_shadow; rp.status = c->d_status;
         CK(launch_append_segments(rp, segs, s));
+        CK(launch_plan_build(c->d_meta, jobs, s));
         for (int l = 0; l < n_layers; ++l) {
             mkv_decode_args al = a[l];
             al.k_new = nullptr;  // appended above

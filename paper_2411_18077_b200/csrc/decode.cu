@@ -553,6 +553,70 @@ cudaError_t launch_append_segments(const ResidualParams& p, const AppendSegs& se
 }
 
 // ---------------------------------------------------------------------------
+// plan build: a layer's page plan (prefix, per-warp first unit, unit records) from the device
+// meta, one CTA per plan, so a flush step uploads nothing between its kernels.  Same
+// arithmetic as the host (capi.cu get_plan): units padded to whole 4-page batches.
+// ---------------------------------------------------------------------------
+constexpr int kPlanThreads = 256;
+
+__global__ void __launch_bounds__(kPlanThreads) plan_build_kernel(const UnitMeta* __restrict__ meta,
+                                                                  const PlanBuildJobs J) {
+    __shared__ int part[kPlanThreads + 1];
+    const PlanBuildJob& jb = J.job[blockIdx.x];
+    const int n = jb.n, tid = threadIdx.x;
+    const int per = (n + kPlanThreads - 1) / kPlanThreads;
+    const int i0 = min(n, tid * per), i1 = min(n, i0 + per);
+    int local = 0;
+    for (int i = i0; i < i1; ++i) local += (meta[jb.unit_begin + i].n_pages + 3) & ~3;
+    part[tid] = local;
+    __syncthreads();
+    if (tid == 0) {  // exclusive scan of the per-thread sums
+        int acc = 0;
+        for (int t = 0; t < kPlanThreads; ++t) {
+            const int v = part[t];
+            part[t] = acc;
+            acc += v;
+        }
+        part[kPlanThreads] = acc;
+    }
+    __syncthreads();
+    int pf = part[tid];
+    for (int i = i0; i < i1; ++i) {
+        const UnitMeta m = meta[jb.unit_begin + i];
+        const int next = pf + ((m.n_pages + 3) & ~3);
+        jb.pref[i] = pf;
+        UnitRec r;
+        r.base = m.page_base - pf;
+        r.pbeg = pf;
+        r.pend = next;
+        r.rend = pf + m.n_pages;
+        r.n_prefill = m.n_prefill;
+        r.pad[0] = r.pad[1] = 0;
+        jb.rec[i] = r;
+        pf = next;
+    }
+    if (tid == 0) jb.pref[n] = part[kPlanThreads];
+    __syncthreads();
+    // first unit of warp w's range: the smallest i with pref[i + 1] > w * chunk (n - 1 at most)
+    for (int w = tid; w < jb.warps; w += kPlanThreads) {
+        const int p = w * jb.chunk;
+        int lo = 0, hi = n - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (jb.pref[mid + 1] > p) hi = mid;
+            else lo = mid + 1;
+        }
+        jb.wstart[w] = lo;
+    }
+}
+
+cudaError_t launch_plan_build(const UnitMeta* meta, const PlanBuildJobs& jobs, cudaStream_t s) {
+    if (jobs.n_jobs == 0) return cudaSuccess;
+    plan_build_kernel<<<jobs.n_jobs, kPlanThreads, 0, s>>>(meta, jobs);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
 // finish kernel: (append) + residual attention on tensor cores + split-K merge
 // ---------------------------------------------------------------------------
 // Finish kernel (one CTA per unit, launched with PDL): decode_append and the exact fp16

@@ -83,6 +83,20 @@ struct UnitRec {
     int32_t n_prefill;  // tokens of the prefill block (its last page may be partial)
     int32_t pad[2];
 };
+// device-side plan construction (flush steps of a multi-layer call)
+struct PlanBuildJob {
+    int unit_begin, n, chunk, warps;
+    int32_t* pref;    // [n + 1]
+    int32_t* wstart;  // [warps]
+    UnitRec* rec;     // [n]
+};
+constexpr int kMaxPlanJobs = 32;
+struct PlanBuildJobs {
+    int n_jobs;
+    PlanBuildJob job[kMaxPlanJobs];
+};
+cudaError_t launch_plan_build(const UnitMeta* meta, const PlanBuildJobs& jobs, cudaStream_t s);
+
 struct PagesParams {
     const uint8_t* pool;
     const UnitMeta* meta;
