@@ -731,9 +731,14 @@ int mkv_decode_step_layers(mkv_cache* c, int n_layers, const mkv_decode_args* a,
         seen.push_back(key);
         all_append = all_append && a[l].k_new != nullptr && a[l].n_units > 0;
     }
-    // A flush step with every layer appending: validate everything, update the mirror, upload the
-    // changed plans, then append + flush every layer's units in ONE launch, so the per-layer
-    // kernels that follow carry no append launches or copies between them.
+    // A flush step with every layer appending: validate everything, update the mirror, then append
+    // + flush every layer's units in ONE launch and build the changed plans on the device, so the
+    // per-layer kernels that follow carry no append launches or copies between them.
+    // the fused path appends every layer's units in one launch: the ranges must not overlap
+    for (int l = 0; l < n_layers && all_append; ++l)
+        for (int m = 0; m < l && all_append; ++m)
+            all_append = a[l].unit_begin + a[l].n_units <= a[m].unit_begin ||
+                         a[m].unit_begin + a[m].n_units <= a[l].unit_begin;
     if (unique && all_append) {
         for (int l = 0; l < n_layers && !flush; ++l)
             for (int i = 0; i < a[l].n_units && !flush; ++i) {
