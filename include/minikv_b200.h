@@ -216,7 +216,14 @@ int mkv_decode_pages_only(mkv_cache* cache, const mkv_decode_args* args, void* s
  * runs with MKV_DECODE_TRACE set): 4 globaltimer stamps per warp {start, after
  * griddepcontrol.wait, pages done, 0}.  Returns words written. */
 int mkv_debug_decode_trace(const mkv_cache* cache, uint64_t* out, int max_words);
-/* Multi-layer decode step: n_layers consecutive calls in one FFI crossing. */
+/* Multi-layer decode step: n_layers consecutive mkv_decode_step calls in one FFI crossing
+ * (same results, bit for bit, for any unit ranges, overlapping or not).
+ * Precondition -- every layer's q / k_new / v_new is already written when the call is made
+ * (stream-ordered before it), and none of them aliases an earlier layer's `out`: a layer whose
+ * unit range is disjoint from every earlier layer's starts its page pass (reading its q) while
+ * the previous layer's finish kernel is still merging.  This is the "all q known" form (a
+ * benchmark/driver that has every layer's q up front); a model whose q of layer l+1 depends on
+ * layer l's output calls mkv_decode_step once per layer (bench.py reports both). */
 int mkv_decode_step_layers(mkv_cache* cache, int n_layers, const mkv_decode_args* args,
                            void* stream);
 

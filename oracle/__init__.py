@@ -365,6 +365,10 @@ class RefOracle(_Lib):
                                             np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS"),
                                             C.c_int, C.POINTER(C.c_void_p)]
         L.mkr_decode_set_destroy.argtypes = [C.c_void_p]
+        L.mkr_decode_set_append.argtypes = [C.c_void_p, _f32p, _f32p, C.c_int]
+        L.mkr_pipeline_run.argtypes = [_sz, _sz, _sz, _sz, _sz, _sz, _sz, _sz, _sz, C.c_uint64, C.c_int,
+                                       C.c_void_p, C.c_void_p, _sz, C.c_void_p, C.c_void_p,
+                                       C.POINTER(C.c_double)]
         L.mkr_decode_set_step.argtypes = [C.c_void_p, _f32p, _f32p, _f32p, C.c_float, _f32p, C.c_int,
                                           C.POINTER(C.c_double)]
         L.mkr_prefill_heads.argtypes = [_sz, _sz, _sz, _sz, C.c_uint64, C.c_int,
@@ -389,6 +393,21 @@ class RefOracle(_Lib):
         _check(self.lib.mkr_quant_dequant_matrix(m, m.shape[0], m.shape[1], axis, group_size, out),
                "quantize/dequantize")
         return out
+
+    def pipeline_run(self, n_kv, g, l, d, hh, rw, steps, seed, threads, n_r=128, gs=16, want_xo=False):
+        """The reference's single-layer chain per kv-head unit (ref_capi.cpp mkr_pipeline_run):
+        selective_flash_attn -> prefill -> `steps` decode steps, on `threads` host threads."""
+        out = np.zeros((max(steps, 1), n_kv * g, d), np.float32)
+        ks = max(min(hh + rw, l), 1)
+        kept = np.zeros((n_kv, ks), np.int64)
+        nk = np.zeros(n_kv, np.int64)
+        xo = np.zeros((n_kv * g, l, d), np.float32) if want_xo else None
+        secs = (C.c_double * 4)()
+        _check(self.lib.mkr_pipeline_run(n_kv, g, l, d, hh, rw, n_r, gs, steps, seed, threads,
+                                          out.ctypes.data, kept.ctypes.data, ks, nk.ctypes.data,
+                                          xo.ctypes.data if xo is not None else None, secs), "pipeline_run")
+        return {"out": out[:steps], "kept": kept, "n_kept": nk, "x_o": xo, "wall_s": secs[0],
+                "attn_thread_s": secs[1], "prefill_thread_s": secs[2], "decode_thread_s": secs[3]}
 
     def cache_prefill(self, k, v, a_cumul, hh, rw, n_r=128, gs=16) -> "RefCache":
         k, v, a = _f32(k), _f32(v), _f32(a_cumul)

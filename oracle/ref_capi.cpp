@@ -329,6 +329,28 @@ int mkr_decode_set_create(size_t n_units, size_t l, size_t d, size_t g, const in
 
 void mkr_decode_set_destroy(mkr_decode_set* s) { delete s; }
 
+// decode_append (cache_engine.cpp:79-90) of one token per unit: k/v[u][d].
+int mkr_decode_set_append(mkr_decode_set* s, const float* k, const float* v, int threads) {
+    GUARD({
+        const std::size_t n = s->units.size(), d = s->d;
+        std::atomic<std::size_t> next{0};
+        std::atomic<int> err{0};
+        auto worker = [&]() {
+            for (std::size_t u; (u = next.fetch_add(1)) < n;) {
+                try {
+                    decode_append(s->units[u], Vector(k + u * d, k + (u + 1) * d), Vector(v + u * d, v + (u + 1) * d));
+                } catch (...) {
+                    err = status_of(std::current_exception());
+                }
+            }
+        };
+        std::vector<std::thread> pool;
+        for (int t = 0; t < (threads > 0 ? threads : 1); ++t) pool.emplace_back(worker);
+        for (auto& t : pool) t.join();
+        if (err) return err.load();
+    })
+}
+
 // One decode step for every unit: q[u][g][d], k/v[u][d] inputs, out[u][g][d].
 // Returns wall seconds in *secs.
 int mkr_decode_set_step(mkr_decode_set* s, const float* q, const float* k, const float* v,
@@ -407,6 +429,102 @@ int mkr_prefill_heads(size_t n_heads, size_t g, size_t l, size_t d, uint64_t see
             double tot = 0.0;
             for (double s : sums) tot += s;
             *a_cumul_sum = tot;
+        }
+        if (err) return err.load();
+    })
+}
+
+// The whole single-layer chain the reference CLI runs (minikv_cli.cpp:180-201), per kv-head
+// unit h of n_kv (G = g q-heads each), every unit independent on a thread pool:
+//   selective_flash_attn (tiles 64x64) per q-head -> a_cumul (GQA: fp32 sum over the unit's
+//   q-heads in head order) -> prefill(k, v, a_cumul, hh, rw, n_r, gs) -> `steps` decode
+//   iterations: g == 1 -> decode_step (cache_engine.cpp:100-138) itself; g > 1 ->
+//   decode_append once + decode_attention per q-head over [stored ; residual].
+// Inputs: Q stream (1, hq), K/V (2|3, h), decode q (4, h, s+1) [g*d], k/v (5|6, h, s+1) [d].
+// Outputs (any may be null): out[steps][n_kv*g][d], kept[n_kv][kept_stride] + n_kept[n_kv],
+// x_o[n_kv*g][l][d].  secs[0..3] = wall seconds of the whole pool, and per-phase thread-time
+// sums: attention, prefill (select + gather + quantize), decode.
+int mkr_pipeline_run(size_t n_kv, size_t g, size_t l, size_t d, size_t hh, size_t rw, size_t n_r, size_t gs,
+                     size_t steps, uint64_t seed, int threads, float* out, int64_t* kept, size_t kept_stride,
+                     int64_t* n_kept, float* x_o, double* secs) {
+    GUARD({
+        std::atomic<std::size_t> next{0};
+        std::atomic<int> err{0};
+        std::vector<double> t_attn(n_kv, 0.0), t_pre(n_kv, 0.0), t_dec(n_kv, 0.0);
+        const float scale = 1.0f / std::sqrt(static_cast<float>(d));
+        auto now = [] { return std::chrono::steady_clock::now(); };
+        auto dt = [](auto a, auto b) { return std::chrono::duration<double>(b - a).count(); };
+        auto worker = [&]() {
+            for (std::size_t h; (h = next.fetch_add(1)) < n_kv;) {
+                try {
+                    Matrix km(l, d), vm(l, d);
+                    synth_floats(seed, (2ull << 48) | (static_cast<uint64_t>(h) << 16), l * d, km.data.data());
+                    synth_floats(seed, (3ull << 48) | (static_cast<uint64_t>(h) << 16), l * d, vm.data.data());
+                    Vector acc(l, 0.0f);
+                    auto t0 = now();
+                    double attn_s = 0.0;
+                    for (std::size_t j = 0; j < g; ++j) {
+                        const std::size_t hq = h * g + j;
+                        Matrix qm(l, d);
+                        synth_floats(seed, (1ull << 48) | (static_cast<uint64_t>(hq) << 16), l * d, qm.data.data());
+                        auto ta = now();
+                        AttentionResult r = selective_flash_attn(qm, km, vm, scale, true, TileConfig{64, 64});
+                        attn_s += dt(ta, now());
+                        for (std::size_t c = 0; c < l; ++c) acc[c] += r.a_cumul[c];
+                        if (x_o) std::memcpy(x_o + hq * l * d, r.output.data.data(), sizeof(float) * l * d);
+                    }
+                    (void)t0;
+                    t_attn[h] = attn_s;
+                    auto tp = now();
+                    auto [cache, rep] = prefill(km, vm, acc, hh, rw, n_r, gs);
+                    t_pre[h] = dt(tp, now());
+                    if (kept) {
+                        for (std::size_t i = 0; i < rep.kept.kept.size() && i < kept_stride; ++i)
+                            kept[h * kept_stride + i] = static_cast<int64_t>(rep.kept.kept[i]);
+                    }
+                    if (n_kept) n_kept[h] = static_cast<int64_t>(rep.kept.kept.size());
+                    Vector tq(g * d), tk(d), tv(d);
+                    double dec_s = 0.0;
+                    for (std::size_t st = 0; st < steps; ++st) {
+                        const uint64_t id = (static_cast<uint64_t>(h) << 16) | (st + 1);
+                        synth_floats(seed, (4ull << 48) | id, g * d, tq.data());
+                        synth_floats(seed, (5ull << 48) | id, d, tk.data());
+                        synth_floats(seed, (6ull << 48) | id, d, tv.data());
+                        auto td = now();
+                        if (g == 1) {
+                            Vector o = decode_step(cache, tq, tk, tv, scale);
+                            dec_s += dt(td, now());
+                            if (out) std::memcpy(out + (st * n_kv + h) * d, o.data(), sizeof(float) * d);
+                        } else {
+                            decode_append(cache, tk, tv);
+                            Matrix keys = stored_keys(cache), vals = stored_values(cache);
+                            keys.data.insert(keys.data.end(), cache.r_key.data.begin(), cache.r_key.data.end());
+                            keys.rows += cache.r_key.rows;
+                            vals.data.insert(vals.data.end(), cache.r_value.data.begin(), cache.r_value.data.end());
+                            vals.rows += cache.r_value.rows;
+                            keys.cols = vals.cols = d;
+                            for (std::size_t j = 0; j < g; ++j) {
+                                auto [o, a] = decode_attention(Vector(tq.begin() + j * d, tq.begin() + (j + 1) * d),
+                                                               keys, vals, scale);
+                                if (out) std::memcpy(out + ((st * n_kv + h) * g + j) * d, o.data(), sizeof(float) * d);
+                            }
+                            dec_s += dt(td, now());
+                        }
+                    }
+                    t_dec[h] = dec_s;
+                } catch (...) {
+                    err = status_of(std::current_exception());
+                }
+            }
+        };
+        auto t0 = now();
+        std::vector<std::thread> pool;
+        for (int t = 0; t < (threads > 0 ? threads : 1); ++t) pool.emplace_back(worker);
+        for (auto& t : pool) t.join();
+        if (secs) {
+            secs[0] = dt(t0, now());
+            secs[1] = secs[2] = secs[3] = 0.0;
+            for (std::size_t h = 0; h < n_kv; ++h) { secs[1] += t_attn[h]; secs[2] += t_pre[h]; secs[3] += t_dec[h]; }
         }
         if (err) return err.load();
     })

@@ -316,8 +316,13 @@ int mkv_select(const mkv_select_args* a, void* stream) {
         if (a->hh_count[u] < 0) return fail(MKV_ERR_INVALID_ARGUMENT, "select_tokens: negative budget");
     if (a->n_units == 0) return MKV_OK;
     if (!a->a_cumul || !a->kept) return fail(MKV_ERR_INVALID_ARGUMENT, "select: null tensor");
-    if (a->kept_stride < std::min<int64_t>(a->length, 1))
-        return fail(MKV_ERR_INVALID_ARGUMENT, "select: kept_stride < length");
+    // every unit writes min(hh[u] + rw, L) indices at kept + u * kept_stride
+    int64_t need = 0;
+    for (int u = 0; u < a->n_units; ++u)
+        need = std::max<int64_t>(need, std::min<int64_t>((int64_t)a->hh_count[u] + a->rw_count, a->length));
+    if (a->kept_stride < std::max<int64_t>(need, 1))
+        return fail(MKV_ERR_INVALID_ARGUMENT, "select: kept_stride %lld < max kept %lld", (long long)a->kept_stride,
+                    (long long)need);
     if (int r = require_device()) return r;
     return do_select(a->a_cumul, a->a_stride, a->n_units, a->length, a->hh_count, a->rw_count, a->kept,
                      a->kept_stride, a->n_kept, static_cast<cudaStream_t>(stream));
@@ -621,7 +626,11 @@ static int decode_validate(mkv_cache* c, const mkv_decode_args* a, bool attend) 
     return MKV_OK;
 }
 
-static int decode_impl(mkv_cache* c, const mkv_decode_args* a, bool attend, cudaStream_t s, bool early = false) {
+// after_plan_build: the plan this call's page kernel reads was just written by plan_build_kernel
+// (fused flush step, first layer): launch that page kernel with a full dependency, since it
+// reads its plan before griddepcontrol.wait.
+static int decode_impl(mkv_cache* c, const mkv_decode_args* a, bool attend, cudaStream_t s, bool early = false,
+                       bool after_plan_build = false) {
     const int ub = a->unit_begin, n = a->n_units;
     if (int r = check_range(c, ub, n)) return r;
     if (n == 0) return MKV_OK;
@@ -678,7 +687,7 @@ static int decode_impl(mkv_cache* c, const mkv_decode_args* a, bool attend, cuda
         PagesParams pp;
         fill_pages_params(c, pl, a, pp);
         pp.early = early && !any_flush ? 1 : 0;
-        CK(launch_pages(pp, pl->grid, s));
+        CK(launch_pages(pp, pl->grid, s, !after_plan_build));
     }
     rp.part_ml = pl->d_part_ml; rp.part_o = pl->d_part_o;
     rp.trace = trace_slot(c);
@@ -720,36 +729,57 @@ int mkv_decode_pages_only(mkv_cache* c, const mkv_decode_args* a, void* stream) 
 int mkv_decode_step_layers(mkv_cache* c, int n_layers, const mkv_decode_args* a, void* stream) {
     if (!a || n_layers < 0) return fail(MKV_ERR_INVALID_ARGUMENT, "decode_step: bad layer list");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    // a layer skips the early wait only if no earlier layer of this call used its unit range
-    // (plan, and so partial buffers); otherwise it waits for the previous finish kernel
-    thread_local std::vector<std::pair<int, int>> seen;
-    seen.clear();
-    bool unique = true, all_append = n_layers > 1 && n_layers <= kMaxAppendSegs, flush = false;
+    // A layer's page kernel may skip its early griddepcontrol.wait (P.early) only if its unit
+    // range is disjoint from every earlier layer's range in this call: the early kernel reads
+    // meta/plan and triggers its dependents before the previous finish kernel (which appends
+    // to, and merges into, the units it owns) has completed.
+    auto disjoint = [&](int l, int m) {
+        return a[l].unit_begin + a[l].n_units <= a[m].unit_begin || a[m].unit_begin + a[m].n_units <= a[l].unit_begin;
+    };
+    std::vector<char> early(n_layers, 0);
+    bool all_disjoint = true;
     for (int l = 0; l < n_layers; ++l) {
-        const std::pair<int, int> key(a[l].unit_begin, a[l].n_units);
-        unique = unique && std::find(seen.begin(), seen.end(), key) == seen.end();
-        seen.push_back(key);
-        all_append = all_append && a[l].k_new != nullptr && a[l].n_units > 0;
+        bool ok = l > 0;
+        for (int m = 0; m < l && ok; ++m) ok = disjoint(l, m);
+        early[l] = ok ? 1 : 0;
+        if (l > 0 && !ok) all_disjoint = false;
     }
+    bool all_append = n_layers > 1 && n_layers <= kMaxAppendSegs, flush = false;
+    for (int l = 0; l < n_layers; ++l) all_append = all_append && a[l].k_new != nullptr && a[l].n_units > 0;
     // A flush step with every layer appending: validate everything, update the mirror, then append
     // + flush every layer's units in ONE launch and build the changed plans on the device, so the
-    // per-layer kernels that follow carry no append launches or copies between them.
-    // the fused path appends every layer's units in one launch: the ranges must not overlap
-    for (int l = 0; l < n_layers && all_append; ++l)
-        for (int m = 0; m < l && all_append; ++m)
-            all_append = a[l].unit_begin + a[l].n_units <= a[m].unit_begin ||
-                         a[m].unit_begin + a[m].n_units <= a[l].unit_begin;
-    if (unique && all_append) {
+    // per-layer kernels that follow carry no append launches or copies between them.  The fused
+    // append needs pairwise-disjoint ranges (one launch appends every layer's units).
+    if (all_disjoint && all_append) {
         for (int l = 0; l < n_layers && !flush; ++l)
             for (int i = 0; i < a[l].n_units && !flush; ++i) {
                 const int u = a[l].unit_begin + i;
                 if (u >= 0 && u < c->n_units && c->n_res[u] + 1 == c->n_r) flush = true;
             }
     }
-    if (unique && all_append && flush) {
+    if (all_disjoint && all_append && flush) {
         for (int l = 0; l < n_layers; ++l)
             if (int r = decode_validate(c, a + l, true)) return r;
         if (int r = require_device()) return r;
+        // the mirror of every unit of the call, restored (and the affected plans invalidated)
+        // if anything below fails before the device work is queued
+        struct Saved { int u, n_res, n_pages, n_blocks; };
+        std::vector<Saved> saved;
+        for (int l = 0; l < n_layers; ++l)
+            for (int i = 0; i < a[l].n_units; ++i) {
+                const int u = a[l].unit_begin + i;
+                saved.push_back({u, c->n_res[u], c->n_pages[u], c->n_blocks[u]});
+            }
+        auto rollback = [&](int r) {
+            for (const Saved& sv : saved) {
+                c->n_res[sv.u] = sv.n_res; c->n_pages[sv.u] = sv.n_pages; c->n_blocks[sv.u] = sv.n_blocks;
+            }
+            for (int l = 0; l < n_layers; ++l) {
+                auto it = c->plans.find(((uint64_t)(uint32_t)a[l].unit_begin << 32) | (uint32_t)a[l].n_units);
+                if (it != c->plans.end()) it->second.sig.clear();
+            }
+            return r;
+        };
         AppendSegs segs{};
         segs.n_seg = n_layers;
         for (int l = 0; l < n_layers; ++l) {
@@ -770,26 +800,24 @@ int mkv_decode_step_layers(mkv_cache* c, int n_layers, const mkv_decode_args* a,
         PlanBuildJobs jobs{};
         for (int l = 0; l < n_layers; ++l) {
             Plan* pl = nullptr;
-            if (int r = get_plan(c, a[l].unit_begin, a[l].n_units, s, &pl, &jobs)) return r;
+            if (int r = get_plan(c, a[l].unit_begin, a[l].n_units, s, &pl, &jobs)) return rollback(r);
         }
         ResidualParams rp{};
         rp.meta = c->d_meta; rp.n_r = c->n_r; rp.res_k = c->d_res_k; rp.res_v = c->d_res_v;
         rp.pool = c->d_pool; rp.shadow = c->d_shadow; rp.status = c->d_status;
-        CK(launch_append_segments(rp, segs, s));
-        CK(launch_plan_build(c->d_meta, jobs, s));
+        if (cudaError_t e = launch_append_segments(rp, segs, s)) return rollback(cuda_fail(e, "append kernel"));
+        if (cudaError_t e = launch_plan_build(c->d_meta, jobs, s)) return rollback(cuda_fail(e, "plan build kernel"));
         for (int l = 0; l < n_layers; ++l) {
             mkv_decode_args al = a[l];
             al.k_new = nullptr;  // appended above
             al.v_new = nullptr;
-            if (int r = decode_impl(c, &al, true, s, l > 0)) return r;
+            // layer 0's page kernel reads a plan plan_build_kernel just wrote: no PDL for it
+            if (int r = decode_impl(c, &al, true, s, early[l] != 0, l == 0 && jobs.n_jobs > 0)) return r;
         }
         return MKV_OK;
     }
-    for (int l = 0; l < n_layers; ++l) {
-        const std::pair<int, int> key(a[l].unit_begin, a[l].n_units);
-        const bool repeat = std::find(seen.begin(), seen.begin() + l, key) != seen.begin() + l;
-        if (int r = decode_impl(c, a + l, true, s, l > 0 && !repeat)) return r;
-    }
+    for (int l = 0; l < n_layers; ++l)
+        if (int r = decode_impl(c, a + l, true, s, early[l] != 0)) return r;
     return MKV_OK;
 }
 

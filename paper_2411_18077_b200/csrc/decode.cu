@@ -196,8 +196,10 @@ __global__ void __maxnreg__(208) pages_kernel(const PagesParams P) {
     };
     // The first kStages batches are requested before griddepcontrol.wait: under PDL they
     // overlap the previous kernel's tail.  Safe because no kernel that may still be running
-    // writes these pages (the append kernel of a flush step is a full-dependency launch)
-    // or the plan/meta fields read here; q is read and partials are written after the wait.
+    // writes these pages or the plan read above (the append kernel of a flush step is a
+    // full-dependency launch, and a page kernel whose plan was just written by
+    // plan_build_kernel is launched without PDL -- capi.cu decode_impl `after_plan_build`);
+    // q is read and partials are written after the wait.
     for (int s = 0; s < kStages; ++s) issue(s);
     // P.early (every layer of a multi-layer call but the first): q is an input of the call and
     // the partial buffers belong to this layer's plan, so the whole page pass may run while the
@@ -427,13 +429,17 @@ __global__ void __maxnreg__(208) pages_kernel(const PagesParams P) {
 }
 
 template <int W, int S>
-static cudaError_t launch_pages_t(const PagesParams& p, int grid, cudaStream_t s) {
+static cudaError_t launch_pages_t(const PagesParams& p, int grid, cudaStream_t s, bool pdl) {
     const size_t smem = (size_t)W * warp_smem<S>() + (size_t)W * S * sizeof(uint64_t);
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(pages_kernel<W, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         configured = true;
+    }
+    if (!pdl) {
+        pages_kernel<W, S><<<grid, W * 32, smem, s>>>(p);
+        return cudaGetLastError();
     }
     return launch_pdl(pages_kernel<W, S>, dim3(grid), dim3(W * 32), smem, s, p);
 }
@@ -456,10 +462,10 @@ PagesConfig pages_config() {
     return cfg;
 }
 
-cudaError_t launch_pages(const PagesParams& p, int grid, cudaStream_t s) {
+cudaError_t launch_pages(const PagesParams& p, int grid, cudaStream_t s, bool pdl) {
     const PagesConfig c = pages_config();
-    if (c.warps == 8 && c.stages == 3) return launch_pages_t<8, 3>(p, grid, s);
-    return launch_pages_t<8, 2>(p, grid, s);
+    if (c.warps == 8 && c.stages == 3) return launch_pages_t<8, 3>(p, grid, s, pdl);
+    return launch_pages_t<8, 2>(p, grid, s, pdl);
 }
 
 // ---------------------------------------------------------------------------

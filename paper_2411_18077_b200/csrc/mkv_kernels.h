@@ -117,7 +117,9 @@ struct PagesConfig {
     int warps, stages;
 };
 PagesConfig pages_config();
-cudaError_t launch_pages(const PagesParams& p, int grid, cudaStream_t s);
+// pdl = false: a full stream dependency (the previous kernel wrote the plan this kernel reads
+// before its griddepcontrol.wait, e.g. plan_build_kernel on a fused flush step)
+cudaError_t launch_pages(const PagesParams& p, int grid, cudaStream_t s, bool pdl = true);
 
 // ---- H2O baseline (h2o.cu) ----
 struct H2OParams {
@@ -162,5 +164,61 @@ struct PrefillAttnParams {
     int causal;
 };
 cudaError_t launch_prefill_attn(const PrefillAttnParams& p, cudaStream_t s);
+
+// ---- reference-format fp32 kernels (refmt.cu): the value-type reference signatures ----
+struct AttnF32Params {
+    const float* q;
+    const float* k;
+    const float* v;
+    int64_t ld_q, ld_k, ld_v, ld_o;
+    float* out;      // [lq][dv]
+    float* lse;      // [lq]
+    float* a_cumul;  // [lk] or null (pass 1 only)
+    int lq, lk, d, dv;
+    float scale;
+    int causal;
+};
+cudaError_t launch_attn_f32(const AttnF32Params& p, cudaStream_t s);
+int attn_f32_max_dv();
+struct DecodeF32Params {
+    const float* q;       // [d]
+    const float* keys;    // [n][ld_k]
+    const float* values;  // [n][ld_v]
+    int64_t ld_k, ld_v;
+    int n, d, dv;
+    float scale;
+    float* out;           // [dv]
+    float* attn;          // [n]
+};
+cudaError_t launch_decode_attn_f32(const DecodeF32Params& p, cudaStream_t s);
+struct QuantBlockParams {
+    const float* src;       // block rows (optionally gathered through row_idx) x cols, row stride ld
+    int64_t ld;
+    const int32_t* row_idx; // null: rows 0 .. rows - 1
+    int rows, cols, gs;
+    int axis;               // 0 = PerChannel, 1 = PerToken
+    uint8_t* codes;         // [rows * cols] in the block's stream order
+    float* params;          // [n_groups][2] (scale, zero)
+    uint32_t* status;       // |= 1: non-finite input
+};
+cudaError_t launch_quantize_block(const QuantBlockParams& p, cudaStream_t s);
+cudaError_t launch_pack_codes(const uint8_t* codes, int64_t n, int64_t code_off, uint32_t init, uint32_t* words,
+                              uint32_t* status, cudaStream_t s);
+struct DequantBlock {
+    int64_t code_off, group_off, row0;
+    int rows;
+    int pad;
+};
+struct DequantParams {
+    const uint32_t* words;
+    const float* params;
+    const DequantBlock* blk;
+    int n_blocks;
+    int64_t total_codes;
+    int cols, gs, axis;
+    float* out;
+    int64_t ld_out;
+};
+cudaError_t launch_dequantize(const DequantParams& p, cudaStream_t s);
 
 }  // namespace mkv

@@ -50,13 +50,32 @@ def plan(batch: int, n_kv_heads: int, world: int, rank: int) -> Shard:
     return Shard(rank, world, (b,), tuple(range(j * hp, (j + 1) * hp)), group)
 
 
+_SEQ_GROUPS = {}
+
+
+def seq_groups(shard: Shard):
+    """The process groups of ranks sharing a sequence ([b*group, (b+1)*group) for each b).
+    dist.new_group is collective over the whole world, so every rank creates every group
+    (once, cached) and uses its own."""
+    import torch.distributed as dist
+    key = (shard.world, shard.group)
+    if key not in _SEQ_GROUPS:
+        _SEQ_GROUPS[key] = [dist.new_group(list(range(b * shard.group, (b + 1) * shard.group)))
+                            for b in range(shard.world // shard.group)]
+    return _SEQ_GROUPS[key]
+
+
 def gather_heads(local_out, shard: Shard, group_ranks=None):
     """All-gather per-head outputs [B_local, Hq_local, d] into [B_local, Hq, d] across the
-    ranks sharing a sequence (only needed when batch < world)."""
+    ranks sharing a sequence (only needed when batch < world).  group_ranks: the process
+    group of this rank's sequence; None builds the sequence groups (collective: every rank
+    of the world must call it the same number of times)."""
     import torch
     import torch.distributed as dist
     if shard.group == 1:
         return local_out
+    if group_ranks is None:
+        group_ranks = seq_groups(shard)[shard.rank // shard.group]
     parts = [torch.empty_like(local_out) for _ in range(shard.group)]
     dist.all_gather(parts, local_out.contiguous(), group=group_ranks)
     return torch.cat(parts, dim=1)

@@ -244,3 +244,92 @@ def test_decode_step_layers_partial_flush_matches_per_layer_calls(mkv):
         c.check()
     for u in range(0, layers * n, n):
         assert caches[0].unit_info(u) == caches[1].unit_info(u)
+
+
+def test_decode_step_layers_overlapping_ranges_match_per_layer_calls(mkv):
+    """mkv_decode_step_layers is n_layers consecutive decode_step calls: with overlapping but
+    non-identical unit ranges (units appended twice in one call) a layer may not start its page
+    pass early, and the result must equal the consecutive per-range calls bit for bit, through
+    flushes (early flag only for ranges disjoint from every earlier one)."""
+    from paper_2411_18077_b200 import _capi
+    d, G, L, n_r = 128, 4, 600, 16
+    ranges = [(0, 8), (4, 8), (10, 6), (2, 3)]  # overlapping, none identical
+    n_units = 16
+    rng = np.random.default_rng(44)
+    caps = [200 + 40 for _ in range(n_units)]
+    k = torch.from_numpy(rng.standard_normal((n_units, L, d)).astype(np.float16)).cuda()
+    v = torch.from_numpy(rng.standard_normal((n_units, L, d)).astype(np.float16)).cuda()
+    a = torch.from_numpy(rng.random((n_units, L)).astype(np.float32)).cuda()
+    caches = []
+    for _ in range(2):
+        c = mkv.KVCache(n_units, caps, max_decode_tokens=160, n_r=n_r)
+        c.prefill(k, v, a, [150 + 3 * u for u in range(n_units)], 40)
+        caches.append(c)
+    scale = 1.0 / np.sqrt(d)
+    for s in range(24):
+        qs = [torch.from_numpy(rng.standard_normal((n, G, d)).astype(np.float16)).cuda() for _, n in ranges]
+        tks = [torch.from_numpy(rng.standard_normal((n, d)).astype(np.float16)).cuda() for _, n in ranges]
+        tvs = [torch.from_numpy(rng.standard_normal((n, d)).astype(np.float16)).cuda() for _, n in ranges]
+        outs = [torch.empty_like(q) for q in qs]
+        args = (_capi.DecodeArgs * len(ranges))()
+        for l, (ub, n) in enumerate(ranges):
+            args[l] = _capi.DecodeArgs(ub, n, G, qs[l].data_ptr(), tks[l].data_ptr(), tvs[l].data_ptr(),
+                                       outs[l].data_ptr(), float(scale))
+        _capi.check(_capi.lib().mkv_decode_step_layers(caches[0].h, len(ranges), args,
+                                                       int(torch.cuda.current_stream().cuda_stream)), "layers")
+        refs = [caches[1].decode_step(qs[l], tks[l], tvs[l], scale, unit_begin=ub) for l, (ub, n) in enumerate(ranges)]
+        for l in range(len(ranges)):
+            assert torch.equal(outs[l], refs[l]), f"step {s} range {l}"
+    for c in caches:
+        c.check()
+    for u in range(n_units):
+        assert caches[0].unit_info(u) == caches[1].unit_info(u)
+
+
+def test_decode_headline_shape_parity(mkv):
+    """configs[1]'s real per-unit shape through the headline API: 32K context, the pyramid budgets
+    hh 6084 -> 468 (+ rw 3276), 32 layers x 4 units, G = 4, every step through
+    mkv_decode_step_layers (cross-layer overlap, device-built plans on the fused flush step),
+    131 steps so the n_r = 128 flush happens inside; outputs checked against the oracle per
+    q-head (GQA composition, fp16-rounded params) before, at and after the flush."""
+    from tests.gpu_util import f32
+    d, G, L, NL, U, n_r = 128, 4, 32768, 32, 4, 128
+    P = oracle.port()
+    x, rw = int(0.10 * L), int(0.10 * L)
+    hh = [int(h) for h in P.allocate_pyramid(x, NL, 7, True)]
+    assert hh[0] == 6084 and hh[-1] == 468 and rw == 3276
+    n_units = NL * U
+    caps = [hh[u // U] + rw for u in range(n_units)]
+    cache = mkv.KVCache(n_units, caps, max_decode_tokens=256, n_r=n_r)
+    ocs = []
+    for l in range(NL):
+        k = mkv.synth_fp16((U, L * d), SEED, (2 << 48) | ((l * U) << 16), 1 << 16).view(U, L, d)
+        v = mkv.synth_fp16((U, L * d), SEED, (3 << 48) | ((l * U) << 16), 1 << 16).view(U, L, d)
+        a = mkv.synth_uniform((U, L), SEED, (7 << 48) | ((l * U) << 16), 1 << 16)
+        cache.prefill(k, v, a, [hh[l]] * U, rw, unit_begin=l * U)
+        kh, vh, ah = k.cpu().numpy(), v.cpu().numpy(), a.cpu().numpy()
+        for j in range(U):
+            oc = P.cache(d=d, n_r=n_r)
+            oc.prefill(f32(kh[j]), f32(vh[j]), ah[j], hh[l], rw)
+            ocs.append(oc)
+    scale = 1.0 / np.sqrt(d)
+    steps = 131
+    check = {0, 64, 126, 127, 128, 130}
+    worst = 0.0
+    for s in range(steps):
+        q = mkv.synth_fp16((n_units, G * d), SEED, (4 << 48) | (s + 1), 1 << 16).view(NL, U, G, d)
+        tk = mkv.synth_fp16((n_units, d), SEED, (5 << 48) | (s + 1), 1 << 16).view(NL, U, d)
+        tv = mkv.synth_fp16((n_units, d), SEED, (6 << 48) | (s + 1), 1 << 16).view(NL, U, d)
+        out = cache.decode_step_layers(q, tk, tv, scale).float().cpu().numpy().reshape(n_units, G, d)
+        qh = q.cpu().numpy().reshape(n_units, G, d)
+        tkh, tvh = tk.cpu().numpy().reshape(n_units, d), tv.cpu().numpy().reshape(n_units, d)
+        for u in range(n_units):
+            ocs[u].append(f32(tkh[u]), f32(tvh[u]))
+            if s in check:
+                for h in range(G):
+                    exp = ocs[u].attend(f32(qh[u, h]), scale, param_fp16=True)
+                    worst = max(worst, max_abs(out[u, h], exp))
+    cache.check()
+    info = cache.unit_info(0)
+    assert info["tokens_residual"] == (steps % n_r) and info["n_blocks"] == 2
+    assert worst <= TOL, worst

@@ -110,3 +110,28 @@ def test_prefill_errors(mkv):
         mkv.selective_flash_attn(x, y, y, 0.1, True)
     with pytest.raises(mkv.InvalidArgument):
         mkv.selective_flash_attn(x[:, :, :0], y, y, 0.1, False)
+
+
+def test_prefill_128k_sampled_rows_and_columns(mkv):
+    """configs[3] shape (Mistral-7B layer, 32 q / 8 kv heads, 128K causal): sampled X_O / LSE rows
+    against the reference's single-query attention over the row's visible keys
+    (attention.cpp:119-143 = row i of selective_flash_attn), and sampled A_cumul COLUMNS against an
+    fp64 host recomputation of pass 2 (attention.cpp:101-115) from Q, k_j and the device LSE
+    (itself checked on the sampled rows) -- the A_cumul that drives selection at this shape,
+    column by column.  Also the global invariant sum A_cumul = G * lq."""
+    import bench
+    Hq, Hkv, L, d = 32, 8, 131072, 128
+    q = mkv.synth_fp16((1, Hq, L, d), SEED, 1 << 48, 1 << 16)
+    k = mkv.synth_fp16((1, Hkv, L, d), SEED, 2 << 48, 1 << 16)
+    v = mkv.synth_fp16((1, Hkv, L, d), SEED, 3 << 48, 1 << 16)
+    scale = 1.0 / math.sqrt(d)
+    r = mkv.selective_flash_attn(q, k, v, scale, True)
+    torch.cuda.synchronize()
+    ac_sum = float(r.a_cumul.double().sum().item())
+    assert abs(ac_sum - Hq * L) <= 1e-3 * Hq * L
+    res = bench.prefill_parity(q, k, v, r, Hq, Hkv, L, d, scale,
+                               rows=(0, 1, 127, 128, 65537, L - 129, L - 1),
+                               cols=[0, 1, 2, 63, 64, 4097, L // 3, L // 2 + 1, L - 200, L - 128, L - 2, L - 1])
+    assert res["x_o_max_abs"] <= TOL_O, res
+    assert res["lse_max_abs"] <= TOL_LSE, res
+    assert res["a_cumul_excess_over_rel_tol"] <= TOL_A_ABS, res

@@ -55,7 +55,7 @@ def _worker(rank, world, port, batch, hkv, G, d, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("batch,hkv,world", [(4, 8, 2), (1, 8, 2)])
+@pytest.mark.parametrize("batch,hkv,world", [(4, 8, 2), (1, 8, 2), (2, 8, 4)])
 def test_gloo_world2(batch, hkv, world):
     G, d = 2, 4
     ctx = mp.get_context("spawn")
@@ -64,7 +64,7 @@ def test_gloo_world2(batch, hkv, world):
     procs = [ctx.Process(target=_worker, args=(r, world, port, batch, hkv, G, d, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = [q.get(timeout=120) for _ in procs]
+    res = [q.get(timeout=180) for _ in procs]
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
