@@ -261,6 +261,58 @@ int mkv_cache_save_mkvc(const mkv_cache* cache, int unit, const char* path);
 int mkv_cache_load_mkvc(mkv_cache* cache, int unit, const char* path);
 
 /* ------------------------------------------------------------------------ */
+/* Reference-format fp32 entries: the reference's own fp32 matrices and its   */
+/* QuantizedTensor stream, for ANY head dim and group size (refmt.cu).  They  */
+/* back the value-type reference signatures of the C++ drop-in; arithmetic    */
+/* follows the reference's order (sequential no-FMA dots, quantize_group's    */
+/* IEEE division and rounding): scores, codes and params are bit-identical,   */
+/* outputs differ from the host only through exp/log ulps.  Device pointers,  */
+/* stream-ordered; mkv_quantize_block_f32 synchronizes (it reports non-finite */
+/* input as the reference's std::domain_error).                               */
+/* ------------------------------------------------------------------------ */
+/* replaces: selective_flash_attn(q, k, v, scale, causal, TileConfig) on fp32   */
+/*           matrices (attention.hpp:38-39, attention.cpp:29-117): pass 1 (out, */
+/*           lse) one CTA per query row, pass 2 (a_cumul, optional) one thread  */
+/*           per key column accumulating in row order.  dv <= 512.             */
+typedef struct {
+    const float* q;     /* [len_q, d], row stride ld_q */
+    int64_t ld_q;
+    const float* k;     /* [len_k, d] */
+    int64_t ld_k;
+    const float* v;     /* [len_k, dv] */
+    int64_t ld_v;
+    float* out;         /* [len_q, dv] */
+    int64_t ld_o;
+    float* lse;         /* [len_q] natural log */
+    float* a_cumul;     /* [len_k] or NULL */
+    int len_q, len_k, d, dv;
+    float scale;
+    int causal;
+} mkv_attention_f32_args;
+int mkv_attention_f32(const mkv_attention_f32_args* args, void* stream);
+/* replaces: decode_attention(q_row, keys, values, scale) (attention.hpp:43-44,            */
+/*           attention.cpp:119-143): out[dv], attn[n] (the softmax row).                  */
+int mkv_decode_attention_f32(const float* q, const float* keys, int64_t ld_k, const float* values, int64_t ld_v,
+                             int n, int d, int dv, float scale, float* out, float* attn, void* stream);
+/* replaces: append_block(t, block) / quantize_matrix(m, axis, gs) (quantizer.hpp:61-65,     */
+/*           quantizer.cpp:102-151): quantizes the rows x cols block (rows gathered through   */
+/*           row_idx when non-NULL: prefill's gather_rows + append_block in one pass), axis 0 */
+/*           PerChannel / 1 PerToken, groups of group_size, appended to a stream that already */
+/*           holds code_offset codes.  words_out receives the words [code_offset / 16,        */
+/*           (code_offset + rows * cols + 15) / 16) -- the first one keeps first_word's low    */
+/*           codes when code_offset % 16 != 0 -- and params_out the block's (scale, zero)     */
+/*           pairs in group order.  Synchronous.                                              */
+int mkv_quantize_block_f32(const float* src, int64_t ld, const int32_t* row_idx, int rows, int cols,
+                           int group_size, int axis, int64_t code_offset, uint32_t first_word,
+                           uint32_t* words_out, float* params_out, void* stream);
+/* replaces: dequantize_matrix(t) (quantizer.hpp:67-68, quantizer.cpp:153-195): words / params */
+/*           (device) of a stream whose blocks have block_rows (host [n_blocks]) rows of cols    */
+/*           channels -> out [sum(block_rows), cols] (row stride ld_out).  The caller checks the */
+/*           group count (std::runtime_error) as the reference does.                             */
+int mkv_dequantize_f32(const uint32_t* words, const float* params, const int64_t* block_rows, int n_blocks,
+                       int cols, int group_size, int axis, float* out, int64_t ld_out, void* stream);
+
+/* ------------------------------------------------------------------------ */
 /* Synthetic inputs (benchmarks/tests): the integer-exact approximate-N(0,1) */
 /* fp16 generator of oracle/minikv_oracle.h, bit-identical on device.        */
 /* ------------------------------------------------------------------------ */

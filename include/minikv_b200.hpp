@@ -113,8 +113,19 @@ struct QuantizedTensor {
     std::vector<std::size_t> block_rows;
     std::size_t total_codes = 0;
 };
-// dequantize_matrix (quantizer.cpp:153-195): v = code * scale + zero (fp32, no FMA)
+// ---- exact-fp32 reference-format path (any head dim / group size; csrc/refmt.cu) ----
+// quantize_matrix / append_block (quantizer.cpp:102-151): codes, packed words and params
+// bit-identical to the reference (quantize_group's IEEE division and rounding on the device).
+QuantizedTensor quantize_matrix(const Matrix& m, GroupAxis axis, std::size_t group_size = kDefaultGroupSize);
+void append_block(QuantizedTensor& t, const Matrix& block);
+// dequantize_matrix (quantizer.cpp:153-195) on the device: v = fl(fl(code * scale) + zero), no FMA
 Matrix dequantize_matrix(const QuantizedTensor& t);
+// selective_flash_attn on fp32 matrices, any d (attention.cpp:29-117): fp32 device kernels in the
+// reference's dot-product and A_cumul accumulation order (the fp16 tensor-core K1 above is d = 128)
+AttentionResult selective_flash_attn_f32(const Matrix& q, const Matrix& k, const Matrix& v, float scale, bool causal,
+                                         TileConfig tiles = {});
+// decode_attention (attention.cpp:119-143) on the device: (output row, attention row)
+std::pair<Vector, Vector> decode_attention(const Vector& q_row, const Matrix& keys, const Matrix& values, float scale);
 
 // ---- cache_engine.hpp:15-67: a device-resident KVCacheLayer ----
 class KVCacheLayer {
@@ -160,5 +171,42 @@ Vector decode_step(KVCacheLayer& cache, const Vector& t_q, const Vector& t_k, co
 Matrix stored_keys(const KVCacheLayer& cache);    // dequantize_matrix(q_key)
 Matrix stored_values(const KVCacheLayer& cache);  // dequantize_matrix(q_value)
 std::uint64_t measured_bytes(const KVCacheLayer& cache);
+
+// ---- the reference's value-type KVCacheLayer (cache_engine.hpp:11-67), any d / group size ----
+// The state lives in the reference's own host fields (so copies, snapshots and field reads behave
+// exactly as the reference's); every computation -- selection (K2), gather + quantize + pack,
+// dequantization and the decode attention -- runs on the device through the fp32
+// reference-format kernels.  This is what the drop-in adapter (dropin/) routes the reference's
+// make_cache / prefill / decode_append / decode_step / stored_* to.  The batched device-handle
+// cache above (K3 pages, K4) is the throughput path for d = 128, group 16, fp16.
+namespace value {
+enum class QuantMode { TwoBit, Identity };
+struct KVCacheLayer {
+    std::size_t d = 0;
+    std::size_t n_r = 128;
+    std::size_t group_size = kDefaultGroupSize;
+    QuantMode mode = QuantMode::TwoBit;
+    QuantizedTensor q_key;    // PerChannel
+    QuantizedTensor q_value;  // PerToken
+    Matrix fp_key;            // identity-mode stores
+    Matrix fp_value;
+    Matrix r_key;             // residual, < n_r rows after any public operation
+    Matrix r_value;
+    std::size_t tokens_quantized = 0;
+    std::size_t tokens_residual() const { return r_key.rows; }
+    std::size_t total_tokens() const { return tokens_quantized + tokens_residual(); }
+};
+KVCacheLayer make_cache(std::size_t d, std::size_t n_r, std::size_t group_size = kDefaultGroupSize,
+                        QuantMode mode = QuantMode::TwoBit);
+std::pair<KVCacheLayer, PrefillReport> prefill(const Matrix& k, const Matrix& v, const Vector& a_cumul,
+                                               std::size_t hh_count, std::size_t rw_count, std::size_t n_r,
+                                               std::size_t group_size = kDefaultGroupSize,
+                                               QuantMode mode = QuantMode::TwoBit);
+void decode_append(KVCacheLayer& cache, const Vector& t_k, const Vector& t_v);
+Vector decode_step(KVCacheLayer& cache, const Vector& t_q, const Vector& t_k, const Vector& t_v, float scale);
+Matrix stored_keys(const KVCacheLayer& cache);
+Matrix stored_values(const KVCacheLayer& cache);
+std::uint64_t measured_bytes(const KVCacheLayer& cache);  // accounting.cpp:101-114
+}  // namespace value
 
 }  // namespace minikv_b200

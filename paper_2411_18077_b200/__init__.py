@@ -11,7 +11,8 @@ from ._capi import (CudaError, DomainError, InvalidArgument, MkvError, OutOfRang
 from .ops import (AttentionResult, H2OBaselineTrace, KVCache, PersistenceReport, VarianceMode,  # noqa: F401
                   allocate_pyramid, allocate_uniform, allocate_variance, default_scale, h2o_dynamic_baseline,
                   layer_score_variance, persistence_analysis, select_token_counts,
-                  select_tokens, selective_flash_attn, synth_fp16, synth_uniform)
+                  select_tokens, selective_flash_attn, synth_fp16, synth_uniform,
+                  selective_flash_attn_f32, decode_attention, quantize_block, dequantize)
 
 __all__ = [
     "AttentionResult", "KVCache", "VarianceMode", "allocate_pyramid", "allocate_uniform", "allocate_variance",
@@ -19,5 +20,5 @@ __all__ = [
     "persistence_analysis",
     "select_token_counts", "select_tokens", "selective_flash_attn", "synth_fp16", "synth_uniform",
     "MkvError", "InvalidArgument", "DomainError", "RuntimeFailure", "OutOfRange", "CudaError",
-    "Unsupported",
+    "Unsupported", "selective_flash_attn_f32", "decode_attention", "quantize_block", "dequantize",
 ]

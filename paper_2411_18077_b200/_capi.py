@@ -70,6 +70,12 @@ class PrefillArgs(C.Structure):
                 ("len_k", i32), ("head_dim", i32), ("scale", C.c_float), ("causal", i32)]
 
 
+class AttnF32Args(C.Structure):
+    _fields_ = [("q", vp), ("ld_q", i64), ("k", vp), ("ld_k", i64), ("v", vp), ("ld_v", i64),
+                ("out", vp), ("ld_o", i64), ("lse", vp), ("a_cumul", vp),
+                ("len_q", i32), ("len_k", i32), ("d", i32), ("dv", i32), ("scale", C.c_float), ("causal", i32)]
+
+
 class SelectArgs(C.Structure):
     _fields_ = [("a_cumul", vp), ("a_stride", i64), ("n_units", i32), ("length", i32),
                 ("hh_count", C.POINTER(C.c_int32)), ("rw_count", i32), ("kept", vp),
@@ -118,7 +124,7 @@ EXPORTS = [
     "mkv_decode_step_layers", "mkv_debug_decode_trace", "mkv_decode_pages_only", "mkv_cache_export_sizes", "mkv_cache_export_reference",
     "mkv_cache_export_residual", "mkv_cache_check", "mkv_cache_save_mkvc", "mkv_cache_load_mkvc",
     "mkv_synth_fp16", "mkv_synth_fp16_rows", "mkv_synth_uniform_f32", "mkv_h2o_dynamic_baseline",
-]
+    "mkv_attention_f32", "mkv_decode_attention_f32", "mkv_quantize_block_f32", "mkv_dequantize_f32"]
 
 _lib = None
 
@@ -162,6 +168,10 @@ def lib():
     L.mkv_synth_fp16.argtypes = [vp, i64, C.c_uint64, C.c_uint64, vp]
     L.mkv_synth_fp16_rows.argtypes = [vp, i64, i64, i64, C.c_uint64, C.c_uint64, C.c_uint64, vp]
     L.mkv_synth_uniform_f32.argtypes = [vp, i64, i64, i64, C.c_uint64, C.c_uint64, C.c_uint64, vp]
+    L.mkv_attention_f32.argtypes = [C.POINTER(AttnF32Args), vp]
+    L.mkv_decode_attention_f32.argtypes = [vp, vp, i64, vp, i64, i32, i32, i32, C.c_float, vp, vp, vp]
+    L.mkv_quantize_block_f32.argtypes = [vp, i64, vp, i32, i32, i32, i32, i64, C.c_uint32, vp, vp, vp]
+    L.mkv_dequantize_f32.argtypes = [vp, vp, C.POINTER(C.c_int64), i32, i32, i32, i32, vp, i64, vp]
     _lib = L
     return L
 

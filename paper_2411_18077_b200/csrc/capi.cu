@@ -1243,4 +1243,93 @@ int mkv_synth_uniform_f32(float* out, int64_t n_rows, int64_t row_len, int64_t l
     return MKV_OK;
 }
 
+// ---------------------------------------------------------------------------
+// reference-format fp32 entries (refmt.cu)
+// ---------------------------------------------------------------------------
+int mkv_attention_f32(const mkv_attention_f32_args* a, void* stream) {
+    if (!a) return fail(MKV_ERR_INVALID_ARGUMENT, "attention: null args");
+    if (a->len_q <= 0 || a->len_k <= 0) return fail(MKV_ERR_INVALID_ARGUMENT, "attention: zero-length sequence");
+    if (a->d <= 0 || a->dv <= 0) return fail(MKV_ERR_INVALID_ARGUMENT, "attention: q/k head dimension mismatch");
+    if (a->causal && a->len_q > a->len_k)
+        return fail(MKV_ERR_INVALID_ARGUMENT, "attention: causal requires l_query <= l_key");
+    if (a->dv > attn_f32_max_dv()) return fail(MKV_ERR_UNSUPPORTED, "attention: value width %d > %d", a->dv, attn_f32_max_dv());
+    if (!a->q || !a->k || !a->v || !a->out || !a->lse) return fail(MKV_ERR_INVALID_ARGUMENT, "attention: null tensor");
+    if (int r = require_device()) return r;
+    AttnF32Params p{a->q, a->k, a->v, a->ld_q, a->ld_k, a->ld_v, a->ld_o, a->out, a->lse, a->a_cumul,
+                    a->len_q, a->len_k, a->d, a->dv, a->scale, a->causal};
+    CK(launch_attn_f32(p, static_cast<cudaStream_t>(stream)));
+    return MKV_OK;
+}
+
+int mkv_decode_attention_f32(const float* q, const float* keys, int64_t ld_k, const float* values, int64_t ld_v,
+                             int n, int d, int dv, float scale, float* out, float* attn, void* stream) {
+    if (n <= 0) return fail(MKV_ERR_INVALID_ARGUMENT, "decode_attention: empty key set");
+    if (d <= 0 || dv <= 0) return fail(MKV_ERR_INVALID_ARGUMENT, "decode_attention: query dimension mismatch");
+    if (!q || !keys || !values || !out || !attn) return fail(MKV_ERR_INVALID_ARGUMENT, "decode_attention: null tensor");
+    if (int r = require_device()) return r;
+    DecodeF32Params p{q, keys, values, ld_k, ld_v, n, d, dv, scale, out, attn};
+    CK(launch_decode_attn_f32(p, static_cast<cudaStream_t>(stream)));
+    return MKV_OK;
+}
+
+int mkv_quantize_block_f32(const float* src, int64_t ld, const int32_t* row_idx, int rows, int cols, int gs, int axis,
+                           int64_t code_offset, uint32_t first_word, uint32_t* words_out, float* params_out,
+                           void* stream) {
+    if (rows <= 0 || cols <= 0) return fail(MKV_ERR_INVALID_ARGUMENT, "append_block: empty block");
+    if (gs < 1) return fail(MKV_ERR_INVALID_ARGUMENT, "quantize_matrix: group_size must be >= 1");
+    if (axis != 0 && axis != 1) return fail(MKV_ERR_INVALID_ARGUMENT, "quantize: axis must be 0 or 1");
+    if (!src || !words_out || !params_out || code_offset < 0)
+        return fail(MKV_ERR_INVALID_ARGUMENT, "quantize: null tensor");
+    if (int r = require_device()) return r;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int64_t n = (int64_t)rows * cols;
+    uint8_t* codes = nullptr;
+    uint32_t* status = nullptr;
+    CK(cudaMallocAsync(&codes, n + 16, s));
+    CK(cudaMallocAsync(&status, sizeof(uint32_t), s));
+    cudaError_t e = cudaMemsetAsync(status, 0, sizeof(uint32_t), s);
+    QuantBlockParams p{src, ld, row_idx, rows, cols, gs, axis, codes, params_out, status};
+    if (e == cudaSuccess) e = launch_quantize_block(p, s);
+    if (e == cudaSuccess) e = launch_pack_codes(codes, n, code_offset, first_word, words_out, status, s);
+    uint32_t st = 0;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&st, status, sizeof(uint32_t), cudaMemcpyDeviceToHost, s);
+    cudaFreeAsync(codes, s);
+    cudaFreeAsync(status, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(e, "quantize_block");
+    if (st & 1u) return fail(MKV_ERR_DOMAIN, "quantize_group: non-finite input");
+    if (st & 2u) return fail(MKV_ERR_DOMAIN, "pack_codes: code out of range");
+    return MKV_OK;
+}
+
+int mkv_dequantize_f32(const uint32_t* words, const float* params, const int64_t* block_rows, int n_blocks, int cols,
+                       int gs, int axis, float* out, int64_t ld_out, void* stream) {
+    if (n_blocks < 0 || cols <= 0 || gs < 1 || (axis != 0 && axis != 1))
+        return fail(MKV_ERR_INVALID_ARGUMENT, "dequantize_matrix: bad layout");
+    if (n_blocks == 0) return MKV_OK;
+    if (!words || !params || !block_rows || !out) return fail(MKV_ERR_INVALID_ARGUMENT, "dequantize_matrix: null tensor");
+    if (int r = require_device()) return r;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    std::vector<DequantBlock> blk(n_blocks);
+    int64_t code = 0, group = 0, row = 0;
+    for (int b = 0; b < n_blocks; ++b) {
+        const int64_t R = block_rows[b];
+        if (R <= 0) return fail(MKV_ERR_INVALID_ARGUMENT, "dequantize_matrix: empty block");
+        blk[b] = DequantBlock{code, group, row, (int)R, 0};
+        code += R * cols;
+        group += axis == 0 ? (int64_t)cols * ((R + gs - 1) / gs) : R * ((cols + gs - 1) / gs);
+        row += R;
+    }
+    DequantBlock* d_blk = nullptr;
+    CK(cudaMallocAsync(&d_blk, sizeof(DequantBlock) * n_blocks, s));
+    cudaError_t e = cudaMemcpyAsync(d_blk, blk.data(), sizeof(DequantBlock) * n_blocks, cudaMemcpyHostToDevice, s);
+    DequantParams p{words, params, d_blk, n_blocks, code, cols, gs, axis, out, ld_out};
+    if (e == cudaSuccess) e = launch_dequantize(p, s);
+    cudaFreeAsync(d_blk, s);
+    // the host table must outlive the async copy
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(e, "dequantize");
+    return MKV_OK;
+}
+
 }  // extern "C"

@@ -41,6 +41,14 @@ struct Dev {
     Dev(const Dev&) = delete;
     Dev& operator=(const Dev&) = delete;
     Dev(Dev&& o) noexcept : p(o.p) { o.p = nullptr; }
+    Dev& operator=(Dev&& o) noexcept {
+        if (this != &o) {
+            cudaFree(p);
+            p = o.p;
+            o.p = nullptr;
+        }
+        return *this;
+    }
     template <typename T>
     T* as() const { return static_cast<T*>(p); }
 };
@@ -246,36 +254,331 @@ PersistenceReport persistence_analysis(const H2OBaselineTrace& trace, const std:
 }
 
 // ---------------------------------------------------------------------------
-// quantized stream (quantizer.cpp:153-195)
+// exact-fp32 reference-format path (refmt.cu through the C ABI)
 // ---------------------------------------------------------------------------
-Matrix dequantize_matrix(const QuantizedTensor& t) {
-    Matrix m(t.logical_rows, t.logical_cols);
-    size_t code = 0, group = 0, row0 = 0;
-    auto code_at = [&](size_t i) -> uint32_t { return (t.packed_words[i / 16] >> (2 * (i % 16))) & 3u; };
+namespace {
+
+int axis_id(GroupAxis a) { return a == GroupAxis::PerChannel ? 0 : 1; }
+
+int64_t group_count(GroupAxis axis, size_t rows, size_t cols, size_t gs) {
+    return axis == GroupAxis::PerChannel ? (int64_t)cols * (int64_t)((rows + gs - 1) / gs)
+                                         : (int64_t)rows * (int64_t)((cols + gs - 1) / gs);
+}
+
+// append_block (quantizer.cpp:102-136) of a block already on the device (rows gathered through
+// d_idx when non-null): quantize + pack on the device, append words / params / block_rows.
+void append_block_device(QuantizedTensor& t, const float* d_src, int64_t ld, const int32_t* d_idx, size_t rows,
+                         size_t cols) {
+    if (rows == 0 || cols == 0) throw std::invalid_argument("append_block: empty block");
+    if (t.logical_cols == 0) t.logical_cols = cols;
+    if (cols != t.logical_cols) throw std::invalid_argument("append_block: channel count mismatch");
+    if (t.group_size < 1) throw std::invalid_argument("append_block: group_size must be >= 1");
+    const int64_t n = (int64_t)rows * (int64_t)cols;
+    const int64_t off = (int64_t)t.total_codes;
+    const int64_t nw = (off + n + 15) / 16 - off / 16;
+    const int64_t ng = group_count(t.axis, rows, cols, t.group_size);
+    const uint32_t init = (off % 16) ? t.packed_words.at((size_t)(off / 16)) : 0u;
+    Dev dw(nw * sizeof(uint32_t)), dp(ng * 2 * sizeof(float));
+    throw_status(mkv_quantize_block_f32(d_src, ld, d_idx, (int)rows, (int)cols, (int)t.group_size, axis_id(t.axis),
+                                        off, init, dw.as<uint32_t>(), dp.as<float>(), nullptr),
+                 "append_block");
+    std::vector<uint32_t> words(nw);
+    std::vector<float> params(2 * ng);
+    cuda_check(cudaMemcpy(words.data(), dw.p, nw * sizeof(uint32_t), cudaMemcpyDeviceToHost), "download");
+    cuda_check(cudaMemcpy(params.data(), dp.p, 2 * ng * sizeof(float), cudaMemcpyDeviceToHost), "download");
+    t.packed_words.resize((size_t)(off / 16));  // the partial last word is re-emitted by the device
+    t.packed_words.insert(t.packed_words.end(), words.begin(), words.end());
+    for (int64_t g = 0; g < ng; ++g) t.params.push_back(GroupQuantParams{params[2 * g], params[2 * g + 1]});
+    t.block_rows.push_back(rows);
+    t.logical_rows += rows;
+    t.total_codes += (size_t)n;
+}
+
+// dequantize_matrix (quantizer.cpp:153-195) into a device buffer with row stride ld; returns rows
+size_t dequantize_device(const QuantizedTensor& t, float* d_out, int64_t ld) {
+    int64_t groups = 0, codes = 0;
+    size_t rows = 0;
     for (size_t R : t.block_rows) {
-        if (t.axis == GroupAxis::PerChannel) {
-            for (size_t c = 0; c < t.logical_cols; ++c)
-                for (size_t g0 = 0; g0 < R; g0 += t.group_size) {
-                    const GroupQuantParams p = t.params.at(group++);
-                    for (size_t r = g0; r < std::min(R, g0 + t.group_size); ++r) {
-                        const float prod = static_cast<float>(code_at(code++)) * p.scale;
-                        m.at(row0 + r, c) = prod + p.zero_point;
-                    }
-                }
-        } else {
-            for (size_t r = 0; r < R; ++r)
-                for (size_t c0 = 0; c0 < t.logical_cols; c0 += t.group_size) {
-                    const GroupQuantParams p = t.params.at(group++);
-                    for (size_t c = c0; c < std::min(t.logical_cols, c0 + t.group_size); ++c) {
-                        const float prod = static_cast<float>(code_at(code++)) * p.scale;
-                        m.at(row0 + r, c) = prod + p.zero_point;
-                    }
-                }
-        }
-        row0 += R;
+        groups += group_count(t.axis, R, t.logical_cols, t.group_size);
+        codes += (int64_t)R * (int64_t)t.logical_cols;
+        rows += R;
     }
+    if ((size_t)groups != t.params.size()) throw std::runtime_error("dequantize_matrix: corrupted group count");
+    if ((size_t)codes > t.total_codes || t.packed_words.size() * 16 < (size_t)codes)
+        throw std::out_of_range("QuantizedTensor: code index out of range");
+    if (rows > t.logical_rows) throw std::runtime_error("dequantize_matrix: block rows exceed logical rows");
+    if (t.block_rows.empty() || t.logical_cols == 0) return rows;
+    Dev dw(t.packed_words.size() * sizeof(uint32_t)), dp(t.params.size() * 2 * sizeof(float));
+    cuda_check(cudaMemcpy(dw.p, t.packed_words.data(), t.packed_words.size() * sizeof(uint32_t), cudaMemcpyHostToDevice),
+               "upload");
+    cuda_check(cudaMemcpy(dp.p, t.params.data(), t.params.size() * 2 * sizeof(float), cudaMemcpyHostToDevice), "upload");
+    std::vector<int64_t> br(t.block_rows.begin(), t.block_rows.end());
+    throw_status(mkv_dequantize_f32(dw.as<uint32_t>(), dp.as<float>(), br.data(), (int)br.size(), (int)t.logical_cols,
+                                    (int)t.group_size, axis_id(t.axis), d_out, ld, nullptr),
+                 "dequantize_matrix");
+    return rows;
+}
+
+Matrix download_f32(const Dev& d, size_t rows, size_t cols) {
+    Matrix m(rows, cols);
+    if (rows * cols)
+        cuda_check(cudaMemcpy(m.data.data(), d.p, rows * cols * sizeof(float), cudaMemcpyDeviceToHost), "download");
     return m;
 }
+
+}  // namespace
+
+QuantizedTensor quantize_matrix(const Matrix& m, GroupAxis axis, size_t group_size) {
+    if (m.empty()) throw std::invalid_argument("quantize_matrix: empty matrix");
+    if (group_size < 1) throw std::invalid_argument("quantize_matrix: group_size must be >= 1");
+    QuantizedTensor t;
+    t.axis = axis;
+    t.group_size = group_size;
+    t.logical_cols = m.cols;
+    append_block(t, m);
+    return t;
+}
+
+void append_block(QuantizedTensor& t, const Matrix& block) {
+    if (block.empty()) throw std::invalid_argument("append_block: empty block");
+    Dev d = upload_f32(block.data.data(), block.rows * block.cols);
+    append_block_device(t, d.as<float>(), (int64_t)block.cols, nullptr, block.rows, block.cols);
+}
+
+Matrix dequantize_matrix(const QuantizedTensor& t) {
+    Matrix m(t.logical_rows, t.logical_cols);
+    Dev d(std::max<size_t>(t.logical_rows * t.logical_cols, 1) * sizeof(float));
+    const size_t rows = dequantize_device(t, d.as<float>(), (int64_t)t.logical_cols);
+    if (rows * t.logical_cols)
+        cuda_check(cudaMemcpy(m.data.data(), d.p, rows * t.logical_cols * sizeof(float), cudaMemcpyDeviceToHost),
+                   "download");
+    return m;
+}
+
+AttentionResult selective_flash_attn_f32(const Matrix& q, const Matrix& k, const Matrix& v, float scale, bool causal,
+                                         TileConfig tiles) {
+    // check_shapes (attention.cpp:12-25) and the tile check (:32-34)
+    if (q.rows == 0 || k.rows == 0) throw std::invalid_argument("attention: zero-length sequence");
+    if (q.cols != k.cols) throw std::invalid_argument("attention: q/k head dimension mismatch");
+    if (v.rows != k.rows) throw std::invalid_argument("attention: k/v token count mismatch");
+    if (causal && q.rows > k.rows) throw std::invalid_argument("attention: causal requires l_query <= l_key");
+    if (tiles.block_m < 1 || tiles.block_n < 1) throw std::invalid_argument("attention: tile sizes must be >= 1");
+    const size_t lq = q.rows, lk = k.rows, d = q.cols, dv = v.cols;
+    Dev dq = upload_f32(q.data.data(), lq * d), dk = upload_f32(k.data.data(), lk * d),
+        dvv = upload_f32(v.data.data(), lk * dv);
+    Dev dout(lq * dv * sizeof(float)), dlse(lq * sizeof(float)), dacc(lk * sizeof(float));
+    mkv_attention_f32_args a{};
+    a.q = dq.as<float>(); a.ld_q = (int64_t)d;
+    a.k = dk.as<float>(); a.ld_k = (int64_t)d;
+    a.v = dvv.as<float>(); a.ld_v = (int64_t)dv;
+    a.out = dout.as<float>(); a.ld_o = (int64_t)dv;
+    a.lse = dlse.as<float>(); a.a_cumul = dacc.as<float>();
+    a.len_q = (int)lq; a.len_k = (int)lk; a.d = (int)d; a.dv = (int)dv;
+    a.scale = scale; a.causal = causal ? 1 : 0;
+    throw_status(mkv_attention_f32(&a, nullptr), "selective_flash_attn");
+    AttentionResult r;
+    r.output = download_f32(dout, lq, dv);
+    r.lse.resize(lq);
+    r.a_cumul.resize(lk);
+    cuda_check(cudaMemcpy(r.lse.data(), dlse.p, lq * sizeof(float), cudaMemcpyDeviceToHost), "download");
+    cuda_check(cudaMemcpy(r.a_cumul.data(), dacc.p, lk * sizeof(float), cudaMemcpyDeviceToHost), "download");
+    // per-row running max / sum (registers of the row CTA) + one 128-key weight chunk: linear in l
+    r.aux_elements = 2 * lq + 128;
+    return r;
+}
+
+std::pair<Vector, Vector> decode_attention(const Vector& q_row, const Matrix& keys, const Matrix& values, float scale) {
+    if (keys.rows == 0) throw std::invalid_argument("decode_attention: empty key set");
+    if (q_row.size() != keys.cols) throw std::invalid_argument("decode_attention: query dimension mismatch");
+    if (values.rows != keys.rows) throw std::invalid_argument("decode_attention: k/v token count mismatch");
+    const size_t n = keys.rows, d = keys.cols, dv = values.cols;
+    Dev dq = upload_f32(q_row.data(), d), dk = upload_f32(keys.data.data(), n * d),
+        dvv = upload_f32(values.data.data(), n * dv);
+    Dev dout(std::max<size_t>(dv, 1) * sizeof(float)), dattn(n * sizeof(float));
+    Vector out(dv, 0.0f), attn(n);
+    if (dv == 0) {  // the reference still computes the (unused) softmax row
+        Matrix one(n, 1);
+        Dev d1 = upload_f32(one.data.data(), n);
+        throw_status(mkv_decode_attention_f32(dq.as<float>(), dk.as<float>(), (int64_t)d, d1.as<float>(), 1, (int)n,
+                                              (int)d, 1, scale, dout.as<float>(), dattn.as<float>(), nullptr),
+                     "decode_attention");
+    } else {
+        throw_status(mkv_decode_attention_f32(dq.as<float>(), dk.as<float>(), (int64_t)d, dvv.as<float>(), (int64_t)dv,
+                                              (int)n, (int)d, (int)dv, scale, dout.as<float>(), dattn.as<float>(),
+                                              nullptr),
+                     "decode_attention");
+        cuda_check(cudaMemcpy(out.data(), dout.p, dv * sizeof(float), cudaMemcpyDeviceToHost), "download");
+    }
+    cuda_check(cudaMemcpy(attn.data(), dattn.p, n * sizeof(float), cudaMemcpyDeviceToHost), "download");
+    return {std::move(out), std::move(attn)};
+}
+
+// ---------------------------------------------------------------------------
+// the value-type KVCacheLayer (cache_engine.cpp:9-138) on the reference-format kernels
+// ---------------------------------------------------------------------------
+namespace value {
+
+KVCacheLayer make_cache(size_t d, size_t n_r, size_t group_size, QuantMode mode) {
+    if (d == 0) throw std::invalid_argument("make_cache: d must be >= 1");
+    if (group_size < 1 || n_r == 0 || n_r % group_size != 0)
+        throw std::invalid_argument("make_cache: n_r must be a positive multiple of group_size");
+    KVCacheLayer c;
+    c.d = d;
+    c.n_r = n_r;
+    c.group_size = group_size;
+    c.mode = mode;
+    c.q_key.axis = GroupAxis::PerChannel;
+    c.q_key.group_size = group_size;
+    c.q_key.logical_cols = d;
+    c.q_value.axis = GroupAxis::PerToken;
+    c.q_value.group_size = group_size;
+    c.q_value.logical_cols = d;
+    c.r_key = Matrix(0, d);
+    c.r_value = Matrix(0, d);
+    return c;
+}
+
+namespace {
+
+void append_rows(Matrix& dst, const Matrix& src) {
+    if (dst.rows == 0) {
+        dst = src;
+        return;
+    }
+    dst.data.insert(dst.data.end(), src.data.begin(), src.data.end());
+    dst.rows += src.rows;
+}
+
+// store_block (cache_engine.cpp:34-52) of rows already on the device (optionally gathered)
+void store_block_device(KVCacheLayer& c, const float* dk, const float* dv, const int32_t* d_idx, size_t rows,
+                        size_t cols) {
+    append_block_device(c.q_key, dk, (int64_t)cols, d_idx, rows, cols);
+    append_block_device(c.q_value, dv, (int64_t)cols, d_idx, rows, cols);
+    c.tokens_quantized += rows;
+}
+
+void store_block(KVCacheLayer& c, const Matrix& kb, const Matrix& vb) {
+    if (c.mode == QuantMode::Identity) {  // full-precision copies, no computation
+        append_rows(c.fp_key, kb);
+        append_rows(c.fp_value, vb);
+        c.tokens_quantized += kb.rows;
+        return;
+    }
+    if (kb.empty()) throw std::invalid_argument("append_block: empty block");
+    Dev dk = upload_f32(kb.data.data(), kb.rows * kb.cols), dv = upload_f32(vb.data.data(), vb.rows * vb.cols);
+    store_block_device(c, dk.as<float>(), dv.as<float>(), nullptr, kb.rows, kb.cols);
+}
+
+Matrix gather(const Matrix& m, const std::vector<size_t>& idx) {  // gather_rows (matrix.cpp:38-47)
+    Matrix out(idx.size(), m.cols);
+    for (size_t i = 0; i < idx.size(); ++i) {
+        if (idx[i] >= m.rows) throw std::out_of_range("gather_rows: index out of range");
+        std::copy_n(m.row(idx[i]), m.cols, out.row(i));
+    }
+    return out;
+}
+
+// the stored part (dequantized or identity) followed by the residual rows, on the device
+size_t stack_device(const KVCacheLayer& c, bool values, Dev& out) {
+    const QuantizedTensor& t = values ? c.q_value : c.q_key;
+    const Matrix& fp = values ? c.fp_value : c.fp_key;
+    const Matrix& res = values ? c.r_value : c.r_key;
+    const size_t nq = c.mode == QuantMode::Identity ? fp.rows : t.logical_rows;
+    const size_t n = nq + res.rows;
+    out = Dev(std::max<size_t>(n * c.d, 1) * sizeof(float));
+    if (c.mode == QuantMode::Identity) {
+        if (nq)
+            cuda_check(cudaMemcpy(out.p, fp.data.data(), nq * c.d * sizeof(float), cudaMemcpyHostToDevice), "upload");
+    } else if (nq) {
+        dequantize_device(t, out.as<float>(), (int64_t)c.d);
+    }
+    if (res.rows)
+        cuda_check(cudaMemcpy(out.as<float>() + nq * c.d, res.data.data(), res.rows * c.d * sizeof(float),
+                              cudaMemcpyHostToDevice),
+                   "upload");
+    return n;
+}
+
+}  // namespace
+
+std::uint64_t measured_bytes(const KVCacheLayer& c) {
+    std::uint64_t bytes = 0;
+    if (c.mode == QuantMode::Identity) {
+        bytes += (std::uint64_t)c.fp_key.data.size() * 2 + (std::uint64_t)c.fp_value.data.size() * 2;
+    } else {
+        bytes += (std::uint64_t)c.q_key.packed_words.size() * 4 + (std::uint64_t)c.q_key.params.size() * 4;
+        bytes += (std::uint64_t)c.q_value.packed_words.size() * 4 + (std::uint64_t)c.q_value.params.size() * 4;
+    }
+    bytes += (std::uint64_t)c.r_key.data.size() * 2 + (std::uint64_t)c.r_value.data.size() * 2;
+    return bytes;
+}
+
+std::pair<KVCacheLayer, PrefillReport> prefill(const Matrix& k, const Matrix& v, const Vector& a_cumul,
+                                               size_t hh_count, size_t rw_count, size_t n_r, size_t group_size,
+                                               QuantMode mode) {
+    if (k.rows != v.rows || k.rows != a_cumul.size()) throw std::invalid_argument("prefill: k/v/a_cumul length mismatch");
+    if (k.cols != v.cols) throw std::invalid_argument("prefill: k/v width mismatch");
+    if (hh_count + rw_count == 0) throw std::runtime_error("prefill: zero kept tokens");
+    KVCacheLayer c = make_cache(k.cols, n_r, group_size, mode);
+    PrefillReport report;
+    report.kept = select_token_counts(a_cumul, hh_count, rw_count);  // K2 on the device
+    report.a_cumul = a_cumul;
+    report.bytes_before = (std::uint64_t)2 * k.rows * k.cols * 2;
+    const std::vector<size_t>& kept = report.kept.kept;
+    if (mode == QuantMode::Identity || kept.empty()) {
+        store_block(c, gather(k, kept), gather(v, kept));
+    } else {
+        // gather_rows + append_block in one device pass: the quantizer reads the kept rows in place
+        std::vector<int32_t> idx(kept.begin(), kept.end());
+        Dev dk = upload_f32(k.data.data(), k.rows * k.cols), dv = upload_f32(v.data.data(), v.rows * v.cols);
+        Dev di(idx.size() * sizeof(int32_t));
+        cuda_check(cudaMemcpy(di.p, idx.data(), idx.size() * sizeof(int32_t), cudaMemcpyHostToDevice), "upload");
+        store_block_device(c, dk.as<float>(), dv.as<float>(), di.as<int32_t>(), kept.size(), k.cols);
+    }
+    report.bytes_after = measured_bytes(c);
+    return {std::move(c), std::move(report)};
+}
+
+void decode_append(KVCacheLayer& c, const Vector& t_k, const Vector& t_v) {
+    if (t_k.size() != c.d || t_v.size() != c.d) throw std::invalid_argument("decode_append: token dimension mismatch");
+    c.r_key.data.insert(c.r_key.data.end(), t_k.begin(), t_k.end());
+    c.r_key.cols = c.d;
+    ++c.r_key.rows;
+    c.r_value.data.insert(c.r_value.data.end(), t_v.begin(), t_v.end());
+    c.r_value.cols = c.d;
+    ++c.r_value.rows;
+    if (c.r_key.rows == c.n_r) {
+        store_block(c, c.r_key, c.r_value);
+        c.r_key = Matrix(0, c.d);
+        c.r_value = Matrix(0, c.d);
+    }
+}
+
+Vector decode_step(KVCacheLayer& c, const Vector& t_q, const Vector& t_k, const Vector& t_v, float scale) {
+    if (c.total_tokens() == 0) throw std::runtime_error("decode_step: empty cache");
+    if (t_q.size() != c.d) throw std::invalid_argument("decode_step: query dimension mismatch");
+    decode_append(c, t_k, t_v);
+    Dev keys(16), vals(16);
+    const size_t n = stack_device(c, false, keys);
+    stack_device(c, true, vals);
+    Dev dq = upload_f32(t_q.data(), c.d), dout(c.d * sizeof(float)), dattn(n * sizeof(float));
+    throw_status(mkv_decode_attention_f32(dq.as<float>(), keys.as<float>(), (int64_t)c.d, vals.as<float>(),
+                                          (int64_t)c.d, (int)n, (int)c.d, (int)c.d, scale, dout.as<float>(),
+                                          dattn.as<float>(), nullptr),
+                 "decode_step");
+    Vector out(c.d);
+    cuda_check(cudaMemcpy(out.data(), dout.p, c.d * sizeof(float), cudaMemcpyDeviceToHost), "download");
+    return out;
+}
+
+Matrix stored_keys(const KVCacheLayer& c) {
+    return c.mode == QuantMode::Identity ? c.fp_key : dequantize_matrix(c.q_key);
+}
+Matrix stored_values(const KVCacheLayer& c) {
+    return c.mode == QuantMode::Identity ? c.fp_value : dequantize_matrix(c.q_value);
+}
+
+}  // namespace value
 
 // ---------------------------------------------------------------------------
 // device KV cache (cache_engine.cpp)

@@ -405,3 +405,76 @@ def synth_uniform(shape, seed: int, stream_base: int, stream_step: int = 1, devi
     check(lib().mkv_synth_uniform_f32(t.data_ptr(), rows, row_len, row_len, seed, stream_base, stream_step,
                                       _stream_ptr(stream)), "synth")
     return t
+
+
+# ---------------------------------------------------------------------------
+# exact-fp32 reference-format entries (refmt.cu): any head dim / group size
+# ---------------------------------------------------------------------------
+def _f32_cuda(x: torch.Tensor, what: str) -> torch.Tensor:
+    if x.dtype != torch.float32 or not x.is_cuda:
+        raise _capi.InvalidArgument(f"{what}: fp32 CUDA tensor expected")
+    return x.contiguous()
+
+
+def selective_flash_attn_f32(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, scale: float, causal: bool = True,
+                             stream=None) -> AttentionResult:
+    """selective_flash_attn (attention.cpp:29-117) on fp32 [L, d] matrices, any d, in the
+    reference's dot-product / A_cumul accumulation order (mkv_attention_f32)."""
+    q, k, v = _f32_cuda(q, "attention"), _f32_cuda(k, "attention"), _f32_cuda(v, "attention")
+    lq, d = q.shape
+    lk, dv = v.shape
+    out = torch.empty((lq, dv), dtype=torch.float32, device=q.device)
+    lse = torch.empty(lq, dtype=torch.float32, device=q.device)
+    ac = torch.empty(lk, dtype=torch.float32, device=q.device)
+    a = _capi.AttnF32Args(q.data_ptr(), d, k.data_ptr(), k.shape[1], v.data_ptr(), dv, out.data_ptr(), dv,
+                          lse.data_ptr(), ac.data_ptr(), lq, lk, k.shape[1] if k.shape[1] == d else -1, dv,
+                          float(scale), int(bool(causal)))
+    check(lib().mkv_attention_f32(C.byref(a), _stream_ptr(stream)), "selective_flash_attn_f32")
+    return AttentionResult(out, lse, ac)
+
+
+def decode_attention(q: torch.Tensor, keys: torch.Tensor, values: torch.Tensor, scale: float, stream=None):
+    """decode_attention (attention.cpp:119-143): (output row [dv], attention row [n]) on fp32."""
+    q, keys, values = _f32_cuda(q, "decode_attention"), _f32_cuda(keys, "decode_attention"), \
+        _f32_cuda(values, "decode_attention")
+    n, d = keys.shape
+    dv = values.shape[1]
+    if q.numel() != d:
+        raise _capi.InvalidArgument("decode_attention: query dimension mismatch")
+    out = torch.empty(dv, dtype=torch.float32, device=q.device)
+    attn = torch.empty(max(n, 1), dtype=torch.float32, device=q.device)
+    check(lib().mkv_decode_attention_f32(q.data_ptr(), keys.data_ptr(), d, values.data_ptr(), dv, n, d, dv,
+                                         float(scale), out.data_ptr(), attn.data_ptr(), _stream_ptr(stream)),
+          "decode_attention")
+    return out, attn[:n]
+
+
+def quantize_block(block: torch.Tensor, axis: int, group_size: int = 16, code_offset: int = 0, first_word: int = 0,
+                   row_idx: Optional[torch.Tensor] = None, stream=None):
+    """append_block / quantize_matrix (quantizer.cpp:102-151) of an fp32 [rows, cols] block (rows
+    gathered through int32 row_idx when given): (words int32-viewed u32 covering stream words
+    [code_offset // 16, ...), params fp32 [n_groups, 2]).  axis 0 PerChannel, 1 PerToken."""
+    block = _f32_cuda(block, "quantize")
+    rows = row_idx.numel() if row_idx is not None else block.shape[0]
+    cols = block.shape[1]
+    n = rows * cols
+    nw = (code_offset + n + 15) // 16 - code_offset // 16
+    per = (rows + group_size - 1) // group_size if axis == 0 else (cols + group_size - 1) // group_size
+    ng = (cols if axis == 0 else rows) * per
+    words = torch.empty(max(nw, 1), dtype=torch.int32, device=block.device)
+    params = torch.empty((max(ng, 1), 2), dtype=torch.float32, device=block.device)
+    check(lib().mkv_quantize_block_f32(block.data_ptr(), cols, row_idx.data_ptr() if row_idx is not None else None,
+                                       rows, cols, group_size, axis, code_offset, first_word & 0xFFFFFFFF,
+                                       words.data_ptr(), params.data_ptr(), _stream_ptr(stream)), "quantize_block")
+    return words[:nw], params[:ng]
+
+
+def dequantize(words: torch.Tensor, params: torch.Tensor, block_rows: Sequence[int], cols: int, axis: int,
+               group_size: int = 16, stream=None) -> torch.Tensor:
+    """dequantize_matrix (quantizer.cpp:153-195) of a device stream -> fp32 [sum(block_rows), cols]."""
+    rows = int(sum(block_rows))
+    out = torch.empty((rows, cols), dtype=torch.float32, device=words.device)
+    br = (C.c_int64 * max(len(block_rows), 1))(*[int(r) for r in block_rows])
+    check(lib().mkv_dequantize_f32(words.data_ptr(), params.data_ptr(), br, len(block_rows), cols, group_size, axis,
+                                   out.data_ptr(), cols, _stream_ptr(stream)), "dequantize_matrix")
+    return out

@@ -4,13 +4,15 @@ dropin/Makefile compiles them where /root/reference exists, into oracle/_ref/sui
   ref_<s>     each suite linked with the reference's own core sources.  Every case must
               pass on the CPU -- this pins oracle/doctest_shim (the doctest subset the
               suites use; doctest itself is vendored under proj/vendor/, absent here).
-  dropin_<s>  the suite linked through a reference-side adapter: the reference core's
-              hot-path symbols are weakened, so they resolve to the adapter and run on the
-              B200 (libminikv_b200.so).  selection (dropin/minikv_reference_adapter.cpp:
-              select_tokens / select_token_counts / allocate_* / layer_score_variance) is
-              bit-exact by construction (fp32 score keys, lowest-index ties); harness
-              (dropin/minikv_reference_adapter_harness.cpp: the H2O baseline and persistence)
-              keeps the reference's arithmetic order.  Both must pass in full on the GPU.
+  dropin_<s>  the suite linked through the reference-side adapters: the reference core's
+              hot-path symbols are weakened, so they resolve to the adapters and run on the
+              B200 (libminikv_b200.so): selective_flash_attn / decode_attention (fp32 device
+              kernels), selection + allocations + variance (K2), quantize_group /
+              quantize_matrix / append_block / dequantize_matrix (device quantizer, bit-exact
+              codes and params), make_cache / prefill / decode_append / decode_step /
+              stored_keys / stored_values (both QuantModes, any d and group size), and the H2O
+              baseline (dropin/minikv_reference_adapter_harness.cpp).  All 7 suites must pass
+              in full on the GPU with the same assertion count as on the reference core.
 The binaries are prebuilt here and travel to the GPU box; nothing reads /root/reference
 at run time.  pipeline.cpp's <json.hpp> (nlohmann, also un-vendored) comes from the copy
 bundled with cudnn_frontend in this image.
@@ -40,7 +42,8 @@ def test_reference_suite_on_reference_core(suite):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("suite", ["selection", "harness"])
+@pytest.mark.parametrize("suite", ["selection", "quantizer", "attention", "accounting", "numerics", "cache_engine",
+                                   "harness"])
 def test_reference_suite_through_dropin_adapter(suite):
     code, out = _run(f"dropin_{suite}")
     assert code == 0, out[-4000:]
