@@ -523,16 +523,17 @@ static int get_plan(mkv_cache* c, int ub, int n, cudaStream_t s, Plan** out, Pla
         *out = &pl;
         return MKV_OK;
     }
-    const int wpc = pages_config().warps;
+    const PagesConfig pc = pages_config();
+    const int wpc = pc.warps, bm = pc.batch - 1;
     const int max_warps = num_sms() * wpc;
     std::vector<int32_t> buf(n + 1 + max_warps, 0);
     int32_t* pref = buf.data();
-    // each unit's pages padded to whole 4-page batches, warp ranges whole batches: every
-    // warp gets the same number of batches (a batch costs the same however full it is)
-    for (int i = 0; i < n; ++i) pref[i + 1] = pref[i] + ((c->n_pages[ub + i] + 3) & ~3);
+    // each unit's pages padded to whole batches, worker ranges whole batches: every worker
+    // gets the same number of batches (a batch costs the same however full it is)
+    for (int i = 0; i < n; ++i) pref[i + 1] = pref[i] + ((c->n_pages[ub + i] + bm) & ~bm);
     const int total = pref[n];
-    const int min_chunk = 8;
-    const int chunk = (std::max(min_chunk, (total + max_warps - 1) / std::max(max_warps, 1)) + 3) & ~3;
+    const int min_chunk = std::max(8, pc.batch);
+    const int chunk = (std::max(min_chunk, (total + max_warps - 1) / std::max(max_warps, 1)) + bm) & ~bm;
     const int warps = total > 0 ? (total + chunk - 1) / chunk : 0;
     int32_t* wstart = pref + n + 1;
     for (int w = 0, i = 0; w < warps; ++w) {  // first unit with pages that contains page w*chunk
@@ -562,7 +563,7 @@ static int get_plan(mkv_cache* c, int ub, int n, cudaStream_t s, Plan** out, Pla
     pl.d_wstart = pl.d_pref + n + 1;
     if (jobs && jobs->n_jobs < kMaxPlanJobs && n > 0) {
         PlanBuildJob& jb = jobs->job[jobs->n_jobs++];
-        jb.unit_begin = ub; jb.n = n; jb.chunk = chunk; jb.warps = warps;
+        jb.unit_begin = ub; jb.n = n; jb.chunk = chunk; jb.warps = warps; jb.batch = pc.batch;
         jb.pref = pl.d_pref; jb.wstart = pl.d_wstart; jb.rec = pl.d_rec;
     } else {
         CK(cudaMemcpyAsync(pl.d_pref, buf.data(), sizeof(int32_t) * buf.size(), cudaMemcpyHostToDevice, s));
@@ -578,7 +579,12 @@ static int get_plan(mkv_cache* c, int ub, int n, cudaStream_t s, Plan** out, Pla
 
 // Diagnostics (MKV_DECODE_TRACE): two alternating slots (consecutive decode calls), each
 // [page-kernel warps x 4 stamps][finish CTAs x 4 stamps] of globaltimer values.
-static size_t trace_slot_words() { return 4 * ((size_t)num_sms() * kMaxPagesWarps + kTraceFinishCtas); }
+// page-kernel region: mma.sync 4 stamps per warp (<= kMaxPagesWarps per SM); tcgen05 kTcTraceWords
+// per worker (2 per SM)
+static size_t trace_page_words() {
+    return (size_t)num_sms() * std::max<size_t>(4 * kMaxPagesWarps, 2 * kTcTraceWords);
+}
+static size_t trace_slot_words() { return trace_page_words() + 4 * (size_t)kTraceFinishCtas; }
 static uint64_t* trace_slot(mkv_cache* c) {
     static const bool tracing = getenv("MKV_DECODE_TRACE") != nullptr;
     if (!tracing) return nullptr;
@@ -691,7 +697,7 @@ static int decode_impl(mkv_cache* c, const mkv_decode_args* a, bool attend, cuda
     }
     rp.part_ml = pl->d_part_ml; rp.part_o = pl->d_part_o;
     rp.trace = trace_slot(c);
-    if (rp.trace) rp.trace += 4 * (size_t)num_sms() * kMaxPagesWarps;
+    if (rp.trace) rp.trace += trace_page_words();
     CK(launch_finish(rp, pl->d_pref, std::max(pl->chunk, 1), pl->total > 0, s));
     ++c->trace_seq;
     return MKV_OK;

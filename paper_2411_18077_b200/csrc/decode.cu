@@ -444,19 +444,22 @@ static cudaError_t launch_pages_t(const PagesParams& p, int grid, cudaStream_t s
     return launch_pdl(pages_kernel<W, S>, dim3(grid), dim3(W * 32), smem, s, p);
 }
 
-// (warps per CTA, ring stages) of the page kernel; MKV_PAGES_CFG=WxS selects a variant
+// The page pass: the mma.sync pages_kernel above (8 warps x 2 stages, 4-page batches;
+// MKV_PAGES_CFG=8x3 for 3 stages) by default.  MKV_PAGES_IMPL=tc selects pages_tc_kernel
+// (decode_tc.cu: tcgen05 + TMEM, 2 workers per CTA, 8-page batches) -- parity-green, but measured
+// 2.4x slower on the bench shapes, so it stays an A/B
+// variant.
 PagesConfig pages_config() {
     static PagesConfig cfg = [] {
         // 8 warps: a 12-warp CTA ran the page pass ~2% faster (same SM sub-partition
-        // throughput) but needs the whole register file, so no finish CTA
-        // could share its SM; 8 warps also leave a third fewer partials to merge.
-        PagesConfig c{8, 2};
+        // throughput) but needs the whole register file, so no finish CTA could share its SM
+        PagesConfig c{8, 2, 4, 0};
         if (const char* e = getenv("MKV_PAGES_CFG")) {
-            int w = 0, s = 0;
-            if (sscanf(e, "%dx%d", &w, &s) == 2 &&
-                ((w == 8 && s == 3) || (w == 8 && s == 2)))
-                c = PagesConfig{w, s};
+            int w = 0, st = 0;
+            if (sscanf(e, "%dx%d", &w, &st) == 2 && w == 8 && (st == 2 || st == 3)) c.stages = st;
         }
+        const char* impl = getenv("MKV_PAGES_IMPL");
+        if (impl && impl[0] == 't') c = PagesConfig{2, 3, 8, 1};
         return c;
     }();
     return cfg;
@@ -464,7 +467,8 @@ PagesConfig pages_config() {
 
 cudaError_t launch_pages(const PagesParams& p, int grid, cudaStream_t s, bool pdl) {
     const PagesConfig c = pages_config();
-    if (c.warps == 8 && c.stages == 3) return launch_pages_t<8, 3>(p, grid, s, pdl);
+    if (c.tc) return launch_pages_tc(p, grid, s, pdl);
+    if (c.stages == 3) return launch_pages_t<8, 3>(p, grid, s, pdl);
     return launch_pages_t<8, 2>(p, grid, s, pdl);
 }
 
@@ -561,7 +565,7 @@ cudaError_t launch_append_segments(const ResidualParams& p, const AppendSegs& se
 // ---------------------------------------------------------------------------
 // plan build: a layer's page plan (prefix, per-warp first unit, unit records) from the device
 // meta, one CTA per plan, so a flush step uploads nothing between its kernels.  Same
-// arithmetic as the host (capi.cu get_plan): units padded to whole 4-page batches.
+// arithmetic as the host (capi.cu get_plan): units padded to whole batches.
 // ---------------------------------------------------------------------------
 constexpr int kPlanThreads = 256;
 
@@ -573,7 +577,8 @@ __global__ void __launch_bounds__(kPlanThreads) plan_build_kernel(const UnitMeta
     const int per = (n + kPlanThreads - 1) / kPlanThreads;
     const int i0 = min(n, tid * per), i1 = min(n, i0 + per);
     int local = 0;
-    for (int i = i0; i < i1; ++i) local += (meta[jb.unit_begin + i].n_pages + 3) & ~3;
+    const int bm = jb.batch - 1;  // units padded to whole batches
+    for (int i = i0; i < i1; ++i) local += (meta[jb.unit_begin + i].n_pages + bm) & ~bm;
     part[tid] = local;
     __syncthreads();
     if (tid == 0) {  // exclusive scan of the per-thread sums
@@ -589,7 +594,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_build_kernel(const UnitMeta
     int pf = part[tid];
     for (int i = i0; i < i1; ++i) {
         const UnitMeta m = meta[jb.unit_begin + i];
-        const int next = pf + ((m.n_pages + 3) & ~3);
+        const int next = pf + ((m.n_pages + bm) & ~bm);
         jb.pref[i] = pf;
         UnitRec r;
         r.base = m.page_base - pf;

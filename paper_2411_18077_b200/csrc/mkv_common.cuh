@@ -143,6 +143,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
         "r"(phase)
         : "memory");
 }
+// as mbar_wait, but each try suspends the warp up to ~1 us until the phase completes (fewer
+// spinning issue slots for waiters that are rarely on the critical path)
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "LAB_WAITS:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000;\n"
+        "@p bra.uni DONES;\n"
+        "bra.uni LAB_WAITS;\n"
+        "DONES:\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
 __device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gmem_src, uint32_t bytes,
                                          uint64_t* bar) {
     asm volatile(

@@ -85,7 +85,7 @@ struct UnitRec {
 };
 // device-side plan construction (flush steps of a multi-layer call)
 struct PlanBuildJob {
-    int unit_begin, n, chunk, warps;
+    int unit_begin, n, chunk, warps, batch;
     int32_t* pref;    // [n + 1]
     int32_t* wstart;  // [warps]
     UnitRec* rec;     // [n]
@@ -113,13 +113,19 @@ struct PagesParams {
     int early;              // q may be read before griddepcontrol.wait (see pages_kernel)
 };
 constexpr int kMaxPagesWarps = 12;  // partial-slot sizing
+// pages_tc_kernel trace (MKV_DECODE_TRACE): per worker, batches 4..7: 8 stamps of compute warp 0,
+// 8 of compute warp 1, 4 of the control warp
+constexpr int kTcTraceWords = 80;
 struct PagesConfig {
-    int warps, stages;
+    int warps, stages;  // workers (page-range owners) per CTA, ring stages
+    int batch;          // pages per batch: units are padded to whole batches in the plan
+    int tc;             // 1: pages_tc_kernel (tcgen05), 0: pages_kernel (mma.sync)
 };
 PagesConfig pages_config();
 // pdl = false: a full stream dependency (the previous kernel wrote the plan this kernel reads
 // before its griddepcontrol.wait, e.g. plan_build_kernel on a fused flush step)
 cudaError_t launch_pages(const PagesParams& p, int grid, cudaStream_t s, bool pdl = true);
+cudaError_t launch_pages_tc(const PagesParams& p, int grid, cudaStream_t s, bool pdl);
 
 // ---- H2O baseline (h2o.cu) ----
 struct H2OParams {

@@ -333,3 +333,17 @@ def test_decode_headline_shape_parity(mkv):
     info = cache.unit_info(0)
     assert info["tokens_residual"] == (steps % n_r) and info["n_blocks"] == 2
     assert worst <= TOL, worst
+
+
+def test_decode_tcgen05_page_variant_parity():
+    """The tcgen05 page pass (MKV_PAGES_IMPL=tc, decode_tc.cu: codes -> TMEM, tcgen05.mma with
+    per-page scaled B operands) -- an A/B variant of the mma.sync page kernel -- passes the same
+    oracle parity tests (G = 1 / 4 / 8, flushes, partial pages, split units, the headline shape)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, MKV_PAGES_IMPL="tc")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", os.path.join(root, "tests", "test_gpu_decode.py"),
+                        "-k", "not tcgen05"], cwd=root, env=env, capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
