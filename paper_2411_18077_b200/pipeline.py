@@ -6,8 +6,16 @@ per layer the q/k/v projections (cuBLAS fp32), K1 selective flash attention
 variance (device), the budget policy (uniform / pyramid / variance-proportional /
 variance-inverse, selection.cpp:48-128), K2 + K3 prefill compression; then `steps`
 decode iterations through K4 with each layer's output feeding the next, while a
-full-precision keep-all pipeline (fp32 torch attention over every K/V row) runs
-side by side from the same tokens -- the deviation trace of pipeline.cpp:166-230.
+full-precision keep-all pipeline runs side by side from the same tokens -- the
+deviation trace of pipeline.cpp:166-230.  The keep-all side is the reference's fp32
+decode_attention (pipeline.cpp:205) on the device (refmt.cu), per head.  mode =
+"identity" (QuantMode::Identity, cache_engine.hpp:13-15) keeps the selected rows in
+fp32 and decodes them with the same kernel: with a keep-all budget it reproduces the
+full-precision pipeline exactly (acceptance criterion 7's identity check).
+
+The reference's own pipeline driver (pipeline.cpp run_from_config, its seeded Rng stream)
+runs on these kernels through the drop-in adapter: tests/test_reference_suites.py
+(test_cache_engine's run_model cases and acceptance criterion 7).
 
 Differences from the reference pipeline, by design: the device head dimension is
 128 (d = 128 * n_heads), activations enter the kernels rounded to fp16, and the
@@ -43,6 +51,7 @@ class RunConfig:  # pipeline.hpp:16-35
     bottom_heavy: bool = True
     n_r: int = 128
     group_size: int = 16
+    mode: str = "two_bit"  # two_bit | identity (QuantMode, cache_engine.hpp:13-15)
 
     @property
     def d(self) -> int:
@@ -55,6 +64,8 @@ class RunConfig:  # pipeline.hpp:16-35
             raise ValueError("RunConfig: negative budget")
         if self.policy not in ("uniform", "pyramid", "var_prop", "var_inv"):
             raise ValueError(f"RunConfig: unknown policy {self.policy}")
+        if self.mode not in ("two_bit", "identity"):
+            raise ValueError(f"RunConfig: unknown mode {self.mode}")
 
 
 @dataclass
@@ -122,15 +133,22 @@ def run_model(weights, prompt: torch.Tensor, cfg: RunConfig) -> RunTrace:
         hh, _ = ops.allocate_variance(layer_vars, mean_hh * L, mode)
     trace.per_layer_hh = list(hh)
     caps = [min(hh[i] + rw, l) for i in range(L) for _ in range(H)]
+    identity = cfg.mode == "identity"
     cache = ops.KVCache(L * H, caps, max_decode_tokens=cfg.steps + cfg.n_r, n_r=cfg.n_r,
                         group_size=cfg.group_size, keep_fp32_params=True)
+    id_k, id_v = [], []  # identity mode: the selected rows in fp32 per layer [H][n, 128]
     for i in range(L):  # K2 + K3 per layer (cache_engine.cpp:56-77)
         cache.prefill(ks[i], vs[i], acs[i], hh[i], rw, unit_begin=i * H)
+        if identity:
+            kept_idx, nk = ops.select_token_counts(acs[i], [hh[i]] * H, rw)
+            id_k.append([ks[i][h, kept_idx[h, :nk[h]].long()].float() for h in range(H)])
+            id_v.append([vs[i][h, kept_idx[h, :nk[h]].long()].float() for h in range(H)])
     cache.check()
     for i in range(L):
         kept = min(hh[i] + rw, l)
         before = H * 4 * l * HEAD_DIM
-        after = sum(_measured_bytes(cache, i * H + h) for h in range(H))
+        after = (sum(2 * (t.numel() + u.numel()) for t, u in zip(id_k[i], id_v[i])) if identity
+                 else sum(_measured_bytes(cache, i * H + h) for h in range(H)))
         trace.layers.append({"layer": i, "kept_tokens": H * kept, "hh_tokens": H * (kept - min(rw, l)),
                              "rw_tokens": H * min(rw, l), "bytes_before": before, "bytes_after": after})
         trace.total_bytes_before += before
@@ -146,14 +164,22 @@ def run_model(weights, prompt: torch.Tensor, cfg: RunConfig) -> RunTrace:
         step_dev = 0.0
         for i, (wq, wk, wv) in enumerate(weights):
             qc, kc, vc = (xc @ wq).view(H, HEAD_DIM), (xc @ wk).view(H, HEAD_DIM), (xc @ wv).view(H, HEAD_DIM)
-            out_c = cache.decode_step(qc.half()[:, None, :], kc.half(), vc.half(), scale, unit_begin=i * H)
+            if identity:  # fp32 stores + the device decode_attention over [stored ; new token]
+                oc = torch.empty(H, HEAD_DIM, device="cuda")
+                for h in range(H):
+                    id_k[i][h] = torch.cat([id_k[i][h], kc[h][None]], 0)
+                    id_v[i][h] = torch.cat([id_v[i][h], vc[h][None]], 0)
+                    oc[h] = ops.decode_attention(qc[h].contiguous(), id_k[i][h], id_v[i][h], scale)[0]
+            else:
+                out_c = cache.decode_step(qc.half()[:, None, :], kc.half(), vc.half(), scale, unit_begin=i * H)
+                oc = out_c[:, 0, :].float()
             l1q[i] = torch.maximum(l1q[i], qc.abs().sum(-1))
             qr, kr, vr = (xr @ wq).view(H, HEAD_DIM), (xr @ wk).view(H, HEAD_DIM), (xr @ wv).view(H, HEAD_DIM)
             ref_k[i] = torch.cat([ref_k[i], kr[:, None, :]], 1)
             ref_v[i] = torch.cat([ref_v[i], vr[:, None, :]], 1)
-            att = torch.softmax(torch.einsum("hc,hlc->hl", qr, ref_k[i]) * scale, -1)
-            out_r = torch.einsum("hl,hlc->hc", att, ref_v[i])
-            oc = out_c[:, 0, :].float()
+            # the reference keep-all decode: decode_attention per head (pipeline.cpp:205), on the device
+            out_r = torch.stack([ops.decode_attention(qr[h].contiguous(), ref_k[i][h].contiguous(),
+                                                      ref_v[i][h].contiguous(), scale)[0] for h in range(H)])
             step_dev = max(step_dev, float((oc - out_r).abs().max()))
             xc, xr = oc.reshape(d), out_r.reshape(d)
         trace.decode.append({"step": s, "max_abs_dev": step_dev})
