@@ -632,16 +632,21 @@ def config0_gpu():
             cache.decode_step(qdd[s], kdd[s], vdd[s], scale, out=outs[s])
         return r, cache
 
-    r, cache = chain(q, k, v, qd, kd, vd)  # warm-up (module load, kernel attributes)
-    torch.cuda.synchronize()
-    cache.close()
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-    ev[0].record()
-    r, cache = chain(q, k, v, qd, kd, vd, ev)
-    ev[3].record()
-    torch.cuda.synchronize()
-    cache.close()
-    t_attn, t_pack, t_dec = ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3])
+    for _ in range(2):  # warm-up (module load, kernel attributes, clocks up after the CPU phases)
+        r, cache = chain(q, k, v, qd, kd, vd)
+        torch.cuda.synchronize()
+        cache.close()
+    times = []
+    for _ in range(5):  # median of 5 timed chains
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        ev[0].record()
+        r, cache = chain(q, k, v, qd, kd, vd, ev)
+        ev[3].record()
+        torch.cuda.synchronize()
+        cache.close()
+        times.append((ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3])))
+    times.sort(key=lambda x: sum(x))
+    t_attn, t_pack, t_dec = times[len(times) // 2]
     kept, nk = mkv.select_token_counts(r.a_cumul[0], hh, rw)
     gpu_out = outs.float().cpu().numpy()
     gpu_xo = r.output.float().cpu().numpy()[0]
@@ -651,15 +656,18 @@ def config0_gpu():
     hq, hk, hv = q.cpu().pin_memory(), k.cpu().pin_memory(), v.cpu().pin_memory()
     hqd, hkd, hvd = qd.cpu().pin_memory(), kd.cpu().pin_memory(), vd.cpu().pin_memory()
     hout = torch.empty_like(outs, device="cpu").pin_memory()
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    dq, dk, dv = hq.cuda(non_blocking=True), hk.cuda(non_blocking=True), hv.cuda(non_blocking=True)
-    dqd, dkd, dvd = hqd.cuda(non_blocking=True), hkd.cuda(non_blocking=True), hvd.cuda(non_blocking=True)
-    r2, cache = chain(dq, dk, dv, dqd, dkd, dvd)
-    hout.copy_(outs, non_blocking=True)
-    torch.cuda.synchronize()
-    e2e_ms = (time.perf_counter() - t0) * 1e3
-    cache.close()
+    e2es = []
+    for _ in range(3):  # median of 3
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        dq, dk, dv = hq.cuda(non_blocking=True), hk.cuda(non_blocking=True), hv.cuda(non_blocking=True)
+        dqd, dkd, dvd = hqd.cuda(non_blocking=True), hkd.cuda(non_blocking=True), hvd.cuda(non_blocking=True)
+        r2, cache = chain(dq, dk, dv, dqd, dkd, dvd)
+        hout.copy_(outs, non_blocking=True)
+        torch.cuda.synchronize()
+        e2es.append((time.perf_counter() - t0) * 1e3)
+        cache.close()
+    e2e_ms = sorted(e2es)[1]
     total_ms = t_attn + t_pack + t_dec
     P = L * (L + 1) / 2
     return {

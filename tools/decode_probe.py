@@ -18,7 +18,7 @@ import paper_2411_18077_b200 as mkv  # noqa: E402
 NL = int(sys.argv[1]) if len(sys.argv) > 1 else 4
 R = int(sys.argv[2]) if len(sys.argv) > 2 else 64
 REPS = int(sys.argv[3]) if len(sys.argv) > 3 else 20
-cfg = dict(bench.CFG)
+cfg = dict(bench.LLAMA, batch=16)
 B, Hq, Hkv, d, L = cfg["batch"], cfg["n_q_heads"], cfg["n_kv_heads"], cfg["head_dim"], cfg["context"]
 G = Hq // Hkv
 hh, rw = bench.budgets(cfg)

@@ -1,21 +1,23 @@
 #!/bin/bash
 # Round profiling pass (run on the GPU box from the repo root):
-#   1. the bench line (N=1),  2. the ncu launch list of a short bench run,
+#   1. the bench line (N=1) and the reference arm,  2. the ncu launch list of a short bench run,
 #   3. per-launch DRAM traffic of every K4 page kernel of one step (roofline "traffic"),
 #   4. one --set full capture each of pages_kernel, finish_kernel and the K1 prefill kernels.
 set -u
 out=${1:-gpurun_out}
 mkdir -p "$out"
 python bench.py > "$out/bench.json" 2> "$out/bench.err"
+python bench.py --impl reference > "$out/bench_ref.json" 2> "$out/bench_ref.err"
+SHORT="--steps 2 --warmup 3 --no-prefill --no-cpu-baseline --no-config0 --no-serving"
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file "$out/launches.csv" \
-    python bench.py --steps 2 --warmup 3 --no-prefill --no-cpu-baseline > /dev/null 2>&1
+    python bench.py $SHORT > /dev/null 2>&1
 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
     -k regex:pages_kernel -s 96 -c 32 --csv --log-file "$out/pages_traffic.csv" \
-    python bench.py --steps 2 --warmup 3 --no-prefill --no-cpu-baseline > /dev/null 2>&1
+    python bench.py $SHORT > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:pages_kernel -s 100 -c 1 -o "$out/prof_pages" -f \
-    python bench.py --steps 2 --warmup 3 --no-prefill --no-cpu-baseline > /dev/null 2>&1
+    python bench.py $SHORT > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:finish_kernel -s 100 -c 1 -o "$out/prof_finish" -f \
-    python bench.py --steps 2 --warmup 3 --no-prefill --no-cpu-baseline > /dev/null 2>&1
+    python bench.py $SHORT > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:attn_fwd_kernel -s 1 -c 1 -o "$out/prof_fwd" -f \
     python tools/prefill_one.py 16384 > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:acumul_kernel -s 1 -c 1 -o "$out/prof_acum" -f \
