@@ -713,6 +713,11 @@ def config0(threads):
     gout, gxo = g.pop("_out"), g.pop("_xo")
     dec_dev = [float(np.max(np.abs(gout[:, h] - ref["out"][:, h]))) for h in range(CFG0["heads"]) if same_sel[h]]
     xo_dev = float(np.max(np.abs(gxo - ref["x_o"])))
+    # the reference's prefill attention rate (3 GEMM-equivalents, 6 d P per head, P = L(L+1)/2),
+    # measured on the 8 x 4K heads: thread-seconds of selective_flash_attn on one thread
+    P0 = CFG0["L"] * (CFG0["L"] + 1) / 2
+    for t_, v_ in cpu.items():
+        v_["attn_gflops_per_thread"] = CFG0["heads"] * 6 * CFG0["d"] * P0 / v_["attn_thread_s"] / 1e9
     g["cpu_reference"] = {str(t): v for t, v in cpu.items()}
     g["cpu_reference"]["kind"] = "reference (oracle/_ref, unmodified sources; one thread per head)"
     g["speedup_vs_cpu_nproc"] = cpu[threads]["wall_s"] * 1e3 / g["gpu_ms"]["e2e_total_from_host"]
@@ -994,6 +999,19 @@ def main():
         if not args.no_prefill:
             try:
                 extras["prefill"] = run_prefill_bench(args)
+                c0 = extras.get("config0") or {}
+                one = (c0.get("cpu_reference") or {}).get("1")
+                if one and "ms" in extras["prefill"]:
+                    pw = W["prefill"]
+                    flops = pw["hq"] * 6 * 128 * pw["L"] * (pw["L"] + 1) / 2
+                    s1 = flops / (one["attn_gflops_per_thread"] * 1e9)
+                    extras["prefill"]["cpu_reference"] = {
+                        "kind": "reference", "extrapolated": True,
+                        "how": "the reference selective_flash_attn's measured rate on configs[0]'s 8 x 4K heads "
+                               "(config0.cpu_reference['1'].attn_gflops_per_thread; the work is 3 GEMM-eq "
+                               "6 d L(L+1)/2 per head, so time scales quadratically in L)",
+                        "seconds_1_thread": s1, "seconds_nproc": s1 / min(threads, pw["hq"]), "cores": threads,
+                        "speedup_vs_gpu_nproc": s1 / min(threads, pw["hq"]) / (extras["prefill"]["ms"] / 1e3)}
             except Exception as e:  # reported, never silently substituted
                 extras["prefill"] = {"error": repr(e)}
     if rank != 0:
