@@ -85,6 +85,17 @@ struct Plan {
     UnitRec* d_rec = nullptr;     // [n_units]
     float* d_part_ml = nullptr;   // this range's page partials (slot = warp + unit), private to the plan
     float* d_part_o = nullptr;
+    // Double buffer for plans prepared ahead (fused flush): after a step whose finish kernels
+    // flushed residual blocks, the next plan is computed on the host and uploaded on the copy
+    // stream into the other buffer; the next call that needs it waits on `ready` and swaps.
+    int32_t* d_buf[2] = {nullptr, nullptr};
+    int cur = 0;
+    bool pending = false;
+    std::vector<int32_t> pending_sig;
+    int p_total = 0, p_chunk = 0, p_grid = 0;
+    cudaEvent_t ready = nullptr;
+    void* h_stage = nullptr;      // pinned staging of the pending upload
+    size_t stage_bytes = 0;
 };
 
 struct mkv_cache {
@@ -106,12 +117,19 @@ struct mkv_cache {
     int part_slots = 0;  // upper bound of page-partial slots per plan (each plan owns its buffers)
     std::unordered_map<uint64_t, Plan> plans;  // key: (unit_begin, n_units)
 
+    cudaStream_t copy_stream = nullptr;  // async plan uploads (fused flush)
+    cudaEvent_t ev_compute = nullptr;
     ~mkv_cache() {
         for (auto& kv : plans) {
-            cudaFree(kv.second.d_pref);
+            cudaFree(kv.second.d_buf[0]);
+            cudaFree(kv.second.d_buf[1]);
             cudaFree(kv.second.d_part_ml);
             cudaFree(kv.second.d_part_o);
+            if (kv.second.ready) cudaEventDestroy(kv.second.ready);
+            if (kv.second.h_stage) cudaFreeHost(kv.second.h_stage);
         }
+        if (copy_stream) cudaStreamDestroy(copy_stream);
+        if (ev_compute) cudaEventDestroy(ev_compute);
         cudaFree(d_meta); cudaFree(d_pool); cudaFree(d_shadow); cudaFree(d_res_k); cudaFree(d_res_v);
         cudaFree(d_status);
         cudaFree(d_trace);
@@ -512,69 +530,153 @@ static void range_signature(const mkv_cache* c, int ub, int n, std::vector<int32
     }
 }
 
+// The host arithmetic of a plan for the current mirror counts of units [ub, ub + n): every
+// unit's pages padded to whole batches, worker ranges whole batches (every worker gets the
+// same number of batches: a batch costs the same however full it is).  buf = [pref (n + 1)]
+// [wstart (max workers)] (staged layout: ints), then the unit records.
+struct HostPlan {
+    std::vector<int32_t> buf;
+    std::vector<UnitRec> rec;
+    int total = 0, chunk = 0, warps = 0, grid = 0;
+};
+static size_t plan_ints(const mkv_cache* c) { return ((c->n_units + 1 + (size_t)num_sms() * kMaxPagesWarps + 3) / 4) * 4; }
+static void host_plan(const mkv_cache* c, int ub, int n, HostPlan& hp) {
+    const PagesConfig pc = pages_config();
+    const int wpc = pc.warps, bm = pc.batch - 1;
+    const int max_warps = num_sms() * wpc;
+    hp.buf.assign(plan_ints(c), 0);
+    int32_t* pref = hp.buf.data();
+    for (int i = 0; i < n; ++i) pref[i + 1] = pref[i] + ((c->n_pages[ub + i] + bm) & ~bm);
+    hp.total = pref[n];
+    const int min_chunk = std::max(8, pc.batch);
+    hp.chunk = (std::max(min_chunk, (hp.total + max_warps - 1) / std::max(max_warps, 1)) + bm) & ~bm;
+    hp.warps = hp.total > 0 ? (hp.total + hp.chunk - 1) / hp.chunk : 0;
+    int32_t* wstart = pref + n + 1;
+    for (int w = 0, i = 0; w < hp.warps; ++w) {  // first unit with pages that contains page w*chunk
+        const int p = w * hp.chunk;
+        while (i < n - 1 && pref[i + 1] <= p) ++i;
+        wstart[w] = i;
+    }
+    hp.rec.assign(n, UnitRec{});
+    for (int i = 0; i < n; ++i) {
+        const int u = ub + i;
+        hp.rec[i].base = c->page_base[u] - pref[i];
+        hp.rec[i].pbeg = pref[i];
+        hp.rec[i].pend = pref[i + 1];
+        hp.rec[i].rend = pref[i] + c->n_pages[u];
+        hp.rec[i].n_prefill = c->n_prefill[u];
+    }
+    hp.grid = (hp.warps + wpc - 1) / wpc;
+}
+static void plan_point(const mkv_cache* c, Plan& pl, int n) {
+    pl.d_pref = pl.d_buf[pl.cur];
+    pl.d_rec = reinterpret_cast<UnitRec*>(pl.d_pref + plan_ints(c));
+    pl.d_wstart = pl.d_pref + n + 1;
+}
+static int plan_alloc(mkv_cache* c, Plan& pl, int n) {
+    if (pl.d_buf[0]) return MKV_OK;
+    const size_t bytes = sizeof(int32_t) * plan_ints(c) + sizeof(UnitRec) * c->n_units;
+    CK(cudaMalloc(&pl.d_buf[0], bytes));
+    CK(cudaMalloc(&pl.d_buf[1], bytes));
+    const size_t slots = (size_t)num_sms() * kMaxPagesWarps + n;  // slot = worker + local unit
+    CK(cudaMalloc(&pl.d_part_ml, sizeof(float) * 2 * kMaxG * slots));
+    CK(cudaMalloc(&pl.d_part_o, sizeof(float) * kMaxG * kHeadDim * slots));
+    pl.cur = 0;
+    plan_point(c, pl, n);
+    return MKV_OK;
+}
+
 // jobs != nullptr: a changed plan is not uploaded but queued for plan_build_kernel (the
-// caller launches it once the device meta holds the new page counts)
-static int get_plan(mkv_cache* c, int ub, int n, cudaStream_t s, Plan** out, PlanBuildJobs* jobs = nullptr) {
+// caller launches it once the device meta holds the new page counts).  *swapped: the plan was
+// prepared ahead and uploaded on the copy stream (the stream now waits for it; the caller
+// launches its first reader with a full dependency).
+static int get_plan(mkv_cache* c, int ub, int n, cudaStream_t s, Plan** out, PlanBuildJobs* jobs = nullptr,
+                    bool* swapped = nullptr) {
     const uint64_t key = ((uint64_t)(uint32_t)ub << 32) | (uint32_t)n;
     Plan& pl = c->plans[key];
     thread_local std::vector<int32_t> sig;
     range_signature(c, ub, n, sig);
+    if (swapped) *swapped = false;
     if (pl.d_pref && pl.sig == sig) {
         *out = &pl;
         return MKV_OK;
     }
-    const PagesConfig pc = pages_config();
-    const int wpc = pc.warps, bm = pc.batch - 1;
-    const int max_warps = num_sms() * wpc;
-    std::vector<int32_t> buf(n + 1 + max_warps, 0);
-    int32_t* pref = buf.data();
-    // each unit's pages padded to whole batches, worker ranges whole batches: every worker
-    // gets the same number of batches (a batch costs the same however full it is)
-    for (int i = 0; i < n; ++i) pref[i + 1] = pref[i] + ((c->n_pages[ub + i] + bm) & ~bm);
-    const int total = pref[n];
-    const int min_chunk = std::max(8, pc.batch);
-    const int chunk = (std::max(min_chunk, (total + max_warps - 1) / std::max(max_warps, 1)) + bm) & ~bm;
-    const int warps = total > 0 ? (total + chunk - 1) / chunk : 0;
-    int32_t* wstart = pref + n + 1;
-    for (int w = 0, i = 0; w < warps; ++w) {  // first unit with pages that contains page w*chunk
-        const int p = w * chunk;
-        while (i < n - 1 && pref[i + 1] <= p) ++i;
-        wstart[w] = i;
+    if (pl.pending && pl.pending_sig == sig) {  // prepared ahead: wait for its upload, swap
+        CK(cudaStreamWaitEvent(s, pl.ready, 0));
+        pl.cur ^= 1;
+        plan_point(c, pl, n);
+        pl.sig = sig;
+        pl.total = pl.p_total; pl.chunk = pl.p_chunk; pl.grid = pl.p_grid;
+        pl.pending = false;
+        if (swapped) *swapped = true;
+        *out = &pl;
+        return MKV_OK;
     }
-    // records follow the int32 arrays (16-byte aligned)
-    const size_t ints = ((c->n_units + 1 + (size_t)num_sms() * kMaxPagesWarps + 3) / 4) * 4;
-    std::vector<UnitRec> rec(n);
-    for (int i = 0; i < n; ++i) {
-        const int u = ub + i;
-        memset(&rec[i], 0, sizeof(UnitRec));
-        rec[i].base = c->page_base[u] - pref[i];
-        rec[i].pbeg = pref[i];
-        rec[i].pend = pref[i + 1];
-        rec[i].rend = pref[i] + c->n_pages[u];
-        rec[i].n_prefill = c->n_prefill[u];
-    }
-    if (!pl.d_pref) {
-        CK(cudaMalloc(&pl.d_pref, sizeof(int32_t) * ints + sizeof(UnitRec) * c->n_units));
-        const size_t slots = (size_t)num_sms() * kMaxPagesWarps + n;  // slot = warp + local unit
-        CK(cudaMalloc(&pl.d_part_ml, sizeof(float) * 2 * kMaxG * slots));
-        CK(cudaMalloc(&pl.d_part_o, sizeof(float) * kMaxG * kHeadDim * slots));
-    }
-    pl.d_rec = reinterpret_cast<UnitRec*>(pl.d_pref + ints);
-    pl.d_wstart = pl.d_pref + n + 1;
+    pl.pending = false;
+    HostPlan hp;
+    host_plan(c, ub, n, hp);
+    if (int r = plan_alloc(c, pl, n)) return r;
     if (jobs && jobs->n_jobs < kMaxPlanJobs && n > 0) {
         PlanBuildJob& jb = jobs->job[jobs->n_jobs++];
-        jb.unit_begin = ub; jb.n = n; jb.chunk = chunk; jb.warps = warps; jb.batch = pc.batch;
+        jb.unit_begin = ub; jb.n = n; jb.chunk = hp.chunk; jb.warps = hp.warps; jb.batch = pages_config().batch;
         jb.pref = pl.d_pref; jb.wstart = pl.d_wstart; jb.rec = pl.d_rec;
     } else {
-        CK(cudaMemcpyAsync(pl.d_pref, buf.data(), sizeof(int32_t) * buf.size(), cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(pl.d_rec, rec.data(), sizeof(UnitRec) * n, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(pl.d_pref, hp.buf.data(), sizeof(int32_t) * (n + 1 + hp.warps), cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(pl.d_rec, hp.rec.data(), sizeof(UnitRec) * n, cudaMemcpyHostToDevice, s));
     }
     pl.sig = sig;
-    pl.total = total;
-    pl.chunk = chunk;
-    pl.grid = (warps + wpc - 1) / wpc;
+    pl.total = hp.total;
+    pl.chunk = hp.chunk;
+    pl.grid = hp.grid;
     *out = &pl;
     return MKV_OK;
+}
+
+// After a fused-flush step (the mirror already holds the new page counts): compute the plan
+// the next call will need and upload it into the plan's other buffer on the copy stream, after
+// everything queued on `s` so far (the other buffer's last readers included).
+static int prepare_next_plan(mkv_cache* c, int ub, int n, cudaStream_t s) {
+    const uint64_t key = ((uint64_t)(uint32_t)ub << 32) | (uint32_t)n;
+    Plan& pl = c->plans[key];
+    if (int r = plan_alloc(c, pl, n)) return r;
+    if (!c->copy_stream) {
+        CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&c->ev_compute, cudaEventDisableTiming));
+    }
+    if (!pl.ready) CK(cudaEventCreateWithFlags(&pl.ready, cudaEventDisableTiming));
+    CK(cudaEventSynchronize(pl.ready));  // the staging buffer's previous upload has completed
+    HostPlan hp;
+    host_plan(c, ub, n, hp);
+    const size_t ib = sizeof(int32_t) * plan_ints(c), rb = sizeof(UnitRec) * n;
+    if (pl.stage_bytes < ib + rb) {
+        if (pl.h_stage) cudaFreeHost(pl.h_stage);
+        pl.h_stage = nullptr;
+        CK(cudaMallocHost(&pl.h_stage, ib + rb));
+        pl.stage_bytes = ib + rb;
+    }
+    memcpy(pl.h_stage, hp.buf.data(), ib);
+    memcpy(static_cast<uint8_t*>(pl.h_stage) + ib, hp.rec.data(), rb);
+    CK(cudaEventRecord(c->ev_compute, s));
+    CK(cudaStreamWaitEvent(c->copy_stream, c->ev_compute, 0));
+    CK(cudaMemcpyAsync(pl.d_buf[pl.cur ^ 1], pl.h_stage, ib + rb, cudaMemcpyHostToDevice, c->copy_stream));
+    CK(cudaEventRecord(pl.ready, c->copy_stream));
+    range_signature(c, ub, n, pl.pending_sig);
+    pl.pending = true;
+    pl.p_total = hp.total; pl.p_chunk = hp.chunk; pl.p_grid = hp.grid;
+    return MKV_OK;
+}
+
+// MKV_FLUSH=fused: a residual block is flushed by the finish kernel of the step that fills it
+// (no append_kernel / plan_build_kernel launch; the next plan is uploaded off the critical
+// path).  Measured slower than the default: the flush then runs per layer
+// on 128 CTAs of 4 warps on the step's critical path, instead of one append launch for every
+// layer's units across the whole GPU.
+static bool fused_flush_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("MKV_FLUSH");
+        return e && e[0] == 'f';
+    }();
+    return on;
 }
 
 // Diagnostics (MKV_DECODE_TRACE): two alternating slots (consecutive decode calls), each
@@ -658,6 +760,14 @@ static int decode_impl(mkv_cache* c, const mkv_decode_args* a, bool attend, cuda
             return fail(MKV_ERR_OUT_OF_RANGE, "decode: unit %d exceeds max_decode_tokens", u);
     }
     if (int r = require_device()) return r;
+    // Fused flush (default): a unit whose residual this append fills is flushed by this step's
+    // finish kernel (quantize the block into pages, attend it dequantized); this step's page pass
+    // covers the pages that existed before, so its plan is taken before the mirror moves on.
+    const bool fused = attend && append && fused_flush_enabled();
+    Plan* pl = nullptr;
+    bool swapped = false;
+    if (fused)
+        if (int r = get_plan(c, ub, n, s, &pl, nullptr, &swapped)) return r;
     bool any_flush = false;
     if (append) {
         for (int i = 0; i < n; ++i) {
@@ -680,26 +790,33 @@ static int decode_impl(mkv_cache* c, const mkv_decode_args* a, bool attend, cuda
     rp.scale_log2 = a->scale * 1.4426950408889634f;
     rp.status = c->d_status;
     rp.trace = nullptr;
-    // flush steps (or append-only calls): append (+ quantize the full block) before the page pass
-    if (append && (any_flush || !attend)) {
+    rp.fused_flush = fused && any_flush ? 1 : 0;
+    // unfused flush steps (or append-only calls): append (+ quantize the full block) before the
+    // page pass
+    if (!fused && append && (any_flush || !attend)) {
         CK(launch_append(rp, s));
         rp.k_new = nullptr;
         rp.v_new = nullptr;
     }
     if (!attend) return MKV_OK;
-    Plan* pl = nullptr;
-    if (int r = get_plan(c, ub, n, s, &pl)) return r;
+    if (!fused)
+        if (int r = get_plan(c, ub, n, s, &pl, nullptr, &swapped)) return r;
     if (pl->total > 0) {
         PagesParams pp;
         fill_pages_params(c, pl, a, pp);
-        pp.early = early && !any_flush ? 1 : 0;
-        CK(launch_pages(pp, pl->grid, s, !after_plan_build));
+        pp.early = early && (fused || !any_flush) ? 1 : 0;
+        // full dependency when the plan was just written by a kernel or swapped in behind an
+        // event wait (the page kernel reads it before its griddepcontrol.wait)
+        CK(launch_pages(pp, pl->grid, s, !(after_plan_build || swapped)));
     }
     rp.part_ml = pl->d_part_ml; rp.part_o = pl->d_part_o;
     rp.trace = trace_slot(c);
     if (rp.trace) rp.trace += trace_page_words();
     CK(launch_finish(rp, pl->d_pref, std::max(pl->chunk, 1), pl->total > 0, s));
     ++c->trace_seq;
+    // the next call's plan (new page counts), prepared and uploaded off the critical path
+    if (fused && any_flush)
+        if (int r = prepare_next_plan(c, ub, n, s)) return r;
     return MKV_OK;
 }
 
@@ -724,11 +841,12 @@ int mkv_decode_pages_only(mkv_cache* c, const mkv_decode_args* a, void* stream) 
     if (int r = require_device()) return r;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     Plan* pl = nullptr;
-    if (int r = get_plan(c, a->unit_begin, a->n_units, s, &pl)) return r;
+    bool swapped = false;
+    if (int r = get_plan(c, a->unit_begin, a->n_units, s, &pl, nullptr, &swapped)) return r;
     if (pl->total == 0) return MKV_OK;
     PagesParams pp;
     fill_pages_params(c, pl, a, pp);
-    CK(launch_pages(pp, pl->grid, s));
+    CK(launch_pages(pp, pl->grid, s, !swapped));
     return MKV_OK;
 }
 
@@ -756,14 +874,14 @@ int mkv_decode_step_layers(mkv_cache* c, int n_layers, const mkv_decode_args* a,
     // + flush every layer's units in ONE launch and build the changed plans on the device, so the
     // per-layer kernels that follow carry no append launches or copies between them.  The fused
     // append needs pairwise-disjoint ranges (one launch appends every layer's units).
-    if (all_disjoint && all_append) {
+    if (all_disjoint && all_append && !fused_flush_enabled()) {
         for (int l = 0; l < n_layers && !flush; ++l)
             for (int i = 0; i < a[l].n_units && !flush; ++i) {
                 const int u = a[l].unit_begin + i;
                 if (u >= 0 && u < c->n_units && c->n_res[u] + 1 == c->n_r) flush = true;
             }
     }
-    if (all_disjoint && all_append && flush) {
+    if (all_disjoint && all_append && flush && !fused_flush_enabled()) {
         for (int l = 0; l < n_layers; ++l)
             if (int r = decode_validate(c, a + l, true)) return r;
         if (int r = require_device()) return r;

@@ -640,12 +640,15 @@ constexpr int kFinishWarps = 4;
 constexpr int kMergeBatch = 8;  // page partials folded per online-max round
 constexpr int kFinishThreads = kFinishWarps * 32;
 
-struct FinishSmem {
-    // per warp: 16 K rows + 16 V rows (swizzled 16-byte chunks); afterwards the warp's
-    // residual partial o[G][128] (fp32, <= 4 KB) reuses the same bytes
-    uint8_t tile[kFinishWarps][8192];
-    float wml[kFinishWarps][2][kMaxG];
-};
+// Shared memory: one slot per warp -- 16 K rows + 16 V rows (swizzled 16-byte chunks, 8 KB;
+// afterwards the warp's residual partial o[G][128] fp32 reuses the same bytes) -- then the warp
+// (m, l) partials.  A launch that may fuse a flush (ResidualParams::fused_flush) uses
+// PageScratch-sized slots (its k / v rows are the tile); the others stay at 8 KB per warp, so a
+// finish CTA keeps fitting beside a page-kernel CTA.
+constexpr int kFinishSlot = 8192;
+constexpr int kFinishSlotFlush = (int)sizeof(PageScratch);
+__host__ __device__ constexpr int finish_smem_bytes(int slot) { return kFinishWarps * slot + kFinishWarps * 2 * kMaxG * 4; }
+static_assert(offsetof(PageScratch, k) == 0 && offsetof(PageScratch, v) == 4096, "tile = PageScratch k, v");
 
 __device__ __forceinline__ void ldmatrix_x4_trans(uint32_t (&r)[4], const void* p) {
     asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
@@ -656,7 +659,8 @@ __device__ __forceinline__ void ldmatrix_x4_trans(uint32_t (&r)[4], const void* 
 __global__ void __launch_bounds__(kFinishThreads, 5) finish_kernel(const ResidualParams P, const int32_t* __restrict__ pref,
                                                                    int chunk) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
-    FinishSmem& S = *reinterpret_cast<FinishSmem*>(smem_raw);
+    const int slot = P.fused_flush ? kFinishSlotFlush : kFinishSlot;
+    float (*wml)[2][kMaxG] = reinterpret_cast<float (*)[2][kMaxG]>(smem_raw + kFinishWarps * slot);
     const int tid = threadIdx.x, warp = tid >> 5, lane = lane_id();
     const int gid = lane >> 2, tig = lane & 3;
     const int i = blockIdx.x;
@@ -667,6 +671,7 @@ __global__ void __launch_bounds__(kFinishThreads, 5) finish_kernel(const Residua
     const int n_old = P.meta[u].n_res;
     const bool app = P.k_new != nullptr;
     const int n = n_old + (app ? 1 : 0);
+    const bool flush = app && P.fused_flush && n == P.n_r;  // this append fills the residual block
     const int ntiles = (n + 15) >> 4;
     const int upre = pref[i], uend = pref[i + 1];
     const int w_first = upre / chunk, w_last = (uend > upre) ? (uend - 1) / chunk : w_first - 1;
@@ -700,31 +705,12 @@ __global__ void __launch_bounds__(kFinishThreads, 5) finish_kernel(const Residua
     float O[8][4];
 #pragma unroll
     for (int g = 0; g < 8; ++g) O[g][0] = O[g][1] = O[g][2] = O[g][3] = 0.0f;
-    uint8_t* tile = S.tile[warp];
+    uint8_t* tile = smem_raw + warp * slot;
     // rows past the residual count are multiplied by p = 0: they must hold finite values
     for (int e = lane; e < 8192 / 16; e += 32) reinterpret_cast<uint4*>(tile)[e] = make_uint4(0, 0, 0, 0);
     __syncwarp();
-    for (int t = warp; t < ntiles; t += kFinishWarps) {
-        const int row0 = 16 * t;
-        const int nrows = min(16, n_old - row0);  // rows already in the residual buffer
-        for (int e = lane; e < 256; e += 32) {
-            const int r = e >> 4, cc = e & 15;
-            if (r < nrows) {
-                const int off = r * 256 + ((cc ^ (r & 7)) << 4);
-                cp_async16(tile + off, rk + (size_t)(row0 + r) * d + cc * 8);
-                cp_async16(tile + 4096 + off, rv + (size_t)(row0 + r) * d + cc * 8);
-            }
-        }
-        cp_async_commit();
-        if (app && n_old >= row0 && n_old < row0 + 16) {  // decode_append (cache_engine.cpp:79-90)
-            const int r = n_old - row0, cc = lane & 15;
-            const bool is_v = lane >= 16;
-            const uint4 x = reinterpret_cast<const uint4*>((is_v ? P.v_new : P.k_new) + (size_t)i * d)[cc];
-            reinterpret_cast<uint4*>((is_v ? rv : rk) + (size_t)n_old * d)[cc] = x;
-            *reinterpret_cast<uint4*>(tile + (is_v ? 4096 : 0) + r * 256 + ((cc ^ (r & 7)) << 4)) = x;
-        }
-        cp_async_wait_all();
-        __syncwarp();
+    // scores, online softmax and P V of one 16-row tile (rows >= valid masked)
+    auto attend_tile = [&](int valid) {
         float Sx[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
         for (int kc = 0; kc < 8; ++kc) {
@@ -735,7 +721,6 @@ __global__ void __launch_bounds__(kFinishThreads, 5) finish_kernel(const Residua
             a[3] = *reinterpret_cast<const uint32_t*>(tile + (gid + 8) * 256 + (((2 * kc + 1) ^ gid) << 4) + 4 * tig);
             mma_16816(Sx, a, qb[kc][0], qb[kc][1]);
         }
-        const int valid = n - row0;
         float x0 = Sx[0] * sl2, x1 = Sx[1] * sl2, x2 = Sx[2] * sl2, x3 = Sx[3] * sl2;
         if (gid >= valid) { x0 = -INFINITY; x1 = -INFINITY; }
         if (gid + 8 >= valid) { x2 = -INFINITY; x3 = -INFINITY; }
@@ -768,6 +753,87 @@ __global__ void __launch_bounds__(kFinishThreads, 5) finish_kernel(const Residua
             mma_16816(O[g], a, pb0, pb1);
         }
         __syncwarp();
+    };
+    if (flush) {
+        // ---- fused flush (decode_append's store_block, cache_engine.cpp:34-52,79-90): the new
+        // token completes the n_r-row residual block; quantize it into n_r / 16 pages here (the
+        // K3 page builder, same pages as append_kernel) and attend the block in its DEQUANTIZED
+        // form, as decode_step does after a flush (cache_engine.cpp:108-136).  This step's page
+        // pass covers the older pages only. ----
+        if (tid < 16) {
+            reinterpret_cast<uint4*>(rk + (size_t)n_old * d)[tid] = reinterpret_cast<const uint4*>(P.k_new + (size_t)i * d)[tid];
+        } else if (tid < 32) {
+            reinterpret_cast<uint4*>(rv + (size_t)n_old * d)[tid - 16] =
+                reinterpret_cast<const uint4*>(P.v_new + (size_t)i * d)[tid - 16];
+        }
+        __threadfence_block();
+        __syncthreads();
+        const UnitMeta meta = P.meta[u];
+        PageScratch& ps = *reinterpret_cast<PageScratch*>(tile);
+        bool ok = true;
+        for (int t = warp; t < P.n_r / kGroup; t += kFinishWarps) {
+            for (int e = lane; e < 16 * 16; e += 32) {
+                const int r = e >> 4, c16 = e & 15;
+                reinterpret_cast<uint4*>(ps.k[r])[c16] = reinterpret_cast<const uint4*>(rk + (size_t)(16 * t + r) * d)[c16];
+                reinterpret_cast<uint4*>(ps.v[r])[c16] = reinterpret_cast<const uint4*>(rv + (size_t)(16 * t + r) * d)[c16];
+            }
+            __syncwarp();
+            const int64_t page = meta.page_base + meta.n_pages + t;
+            ok &= build_page(ps, 16, P.pool + (size_t)page * kPageBytes,
+                             P.shadow ? P.shadow + (size_t)page * (kShadowBytes / 4) : nullptr);
+            // dequantize the page into the tile: v = fl(code * scale) + zero with the page's fp16
+            // (scale, zero), rounded to fp16 (the page pass's values, up to that rounding)
+            const __half* ks = reinterpret_cast<const __half*>(ps.page + kKS);
+            const __half* kz = reinterpret_cast<const __half*>(ps.page + kKZ);
+            const __half* vs = reinterpret_cast<const __half*>(ps.page + kVS);
+            const __half* vz = reinterpret_cast<const __half*>(ps.page + kVZ);
+            for (int e = lane; e < 16 * 16; e += 32) {
+                const int r = e >> 4, cc = e & 15, g = cc >> 1;
+                uint32_t kq[4], vq[4];
+                const float vsc = __half2float(vs[vs_param_idx(r, g)]), vzp = __half2float(vz[vz_param_idx(r, g)]);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int c0 = 8 * cc + 2 * j, c1 = c0 + 1;
+                    const float k0 = __fadd_rn(__fmul_rn((float)ps.kc[r][c0], __half2float(ks[k_param_idx(c0)])),
+                                               __half2float(kz[k_param_idx(c0)]));
+                    const float k1 = __fadd_rn(__fmul_rn((float)ps.kc[r][c1], __half2float(ks[k_param_idx(c1)])),
+                                               __half2float(kz[k_param_idx(c1)]));
+                    kq[j] = pack_half2(k0, k1);
+                    vq[j] = pack_half2(__fadd_rn(__fmul_rn((float)ps.vc[r][c0], vsc), vzp),
+                                       __fadd_rn(__fmul_rn((float)ps.vc[r][c1], vsc), vzp));
+                }
+                __syncwarp();  // (ps.k / ps.v are overwritten: every lane has read its codes first)
+                *reinterpret_cast<uint4*>(tile + r * 256 + ((cc ^ (r & 7)) << 4)) = make_uint4(kq[0], kq[1], kq[2], kq[3]);
+                *reinterpret_cast<uint4*>(tile + 4096 + r * 256 + ((cc ^ (r & 7)) << 4)) =
+                    make_uint4(vq[0], vq[1], vq[2], vq[3]);
+            }
+            __syncwarp();
+            attend_tile(16);
+        }
+        if (!ok && lane == 0) atomicOr(P.status, kStatusNonFinite);
+    }
+    for (int t = warp; t < (flush ? 0 : ntiles); t += kFinishWarps) {
+        const int row0 = 16 * t;
+        const int nrows = min(16, n_old - row0);  // rows already in the residual buffer
+        for (int e = lane; e < 256; e += 32) {
+            const int r = e >> 4, cc = e & 15;
+            if (r < nrows) {
+                const int off = r * 256 + ((cc ^ (r & 7)) << 4);
+                cp_async16(tile + off, rk + (size_t)(row0 + r) * d + cc * 8);
+                cp_async16(tile + 4096 + off, rv + (size_t)(row0 + r) * d + cc * 8);
+            }
+        }
+        cp_async_commit();
+        if (app && n_old >= row0 && n_old < row0 + 16) {  // decode_append (cache_engine.cpp:79-90)
+            const int r = n_old - row0, cc = lane & 15;
+            const bool is_v = lane >= 16;
+            const uint4 x = reinterpret_cast<const uint4*>((is_v ? P.v_new : P.k_new) + (size_t)i * d)[cc];
+            reinterpret_cast<uint4*>((is_v ? rv : rk) + (size_t)n_old * d)[cc] = x;
+            *reinterpret_cast<uint4*>(tile + (is_v ? 4096 : 0) + r * 256 + ((cc ^ (r & 7)) << 4)) = x;
+        }
+        cp_async_wait_all();
+        __syncwarp();
+        attend_tile(n - row0);
     }
 #pragma unroll
     for (int o = 4; o < 32; o <<= 1) {
@@ -784,10 +850,17 @@ __global__ void __launch_bounds__(kFinishThreads, 5) finish_kernel(const Residua
         if (h1 < G) { wo[h1 * kHeadDim + c] = O[g][1]; wo[h1 * kHeadDim + c + 8] = O[g][3]; }
     }
     if (gid == 0) {
-        if (h0 < G) { S.wml[warp][0][h0] = m0; S.wml[warp][1][h0] = l0; }
-        if (h1 < G) { S.wml[warp][0][h1] = m1; S.wml[warp][1][h1] = l1; }
+        if (h0 < G) { wml[warp][0][h0] = m0; wml[warp][1][h0] = l0; }
+        if (h1 < G) { wml[warp][0][h1] = m1; wml[warp][1][h1] = l1; }
     }
-    if (app && tid == 0) P.meta[u].n_res = n;  // only this CTA reads this unit's n_res after the append
+    if (app && tid == 0) {  // only this CTA reads this unit's meta after the append
+        if (flush) {
+            P.meta[u].n_pages += P.n_r / kGroup;
+            P.meta[u].n_res = 0;
+        } else {
+            P.meta[u].n_res = n;
+        }
+    }
     // ---- the page partials are complete past this point ----
     fstamp(1);
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
@@ -799,12 +872,12 @@ __global__ void __launch_bounds__(kFinishThreads, 5) finish_kernel(const Residua
         const int h = e / (d / 2), c2 = e % (d / 2);
         float M = -INFINITY, L = 0.0f, ax = 0.0f, ay = 0.0f;
         for (int w = 0; w < kFinishWarps; ++w) {
-            const float lw = S.wml[w][1][h];
+            const float lw = wml[w][1][h];
             if (lw > 0.0f) {
-                const float mw = S.wml[w][0][h];
+                const float mw = wml[w][0][h];
                 const float nm = fmaxf(M, mw);
                 const float f = fast_exp2(M - nm), s = fast_exp2(mw - nm);
-                const float2 wv = reinterpret_cast<const float2*>(S.tile[w])[h * (kHeadDim / 2) + c2];
+                const float2 wv = reinterpret_cast<const float2*>(smem_raw + w * slot)[h * (kHeadDim / 2) + c2];
                 ax = fmaf(wv.x, s, ax * f);
                 ay = fmaf(wv.y, s, ay * f);
                 L = fmaf(lw, s, L * f);
@@ -846,10 +919,11 @@ __global__ void __launch_bounds__(kFinishThreads, 5) finish_kernel(const Residua
 }
 
 cudaError_t launch_finish(const ResidualParams& p, const int32_t* pref, int chunk, bool after_pages, cudaStream_t s) {
-    const size_t smem = sizeof(FinishSmem);
+    const size_t smem = finish_smem_bytes(p.fused_flush ? kFinishSlotFlush : kFinishSlot);
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e = cudaFuncSetAttribute(finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             finish_smem_bytes(kFinishSlotFlush));
         if (e != cudaSuccess) return e;
         configured = true;
     }

@@ -60,6 +60,7 @@ struct ResidualParams {
     float scale_log2;
     uint32_t* status;
     uint64_t* trace;      // diagnostics: per CTA {start, residual done, wait released, end}, or null
+    int fused_flush;      // finish_kernel quantizes a residual block this append fills (no append_kernel)
 };
 constexpr int kTraceFinishCtas = 8192;  // finish-kernel CTAs recorded per trace slot
 cudaError_t launch_append(const ResidualParams& p, cudaStream_t s);

@@ -335,15 +335,20 @@ def test_decode_headline_shape_parity(mkv):
     assert worst <= TOL, worst
 
 
-def test_decode_tcgen05_page_variant_parity():
-    """The tcgen05 page pass (MKV_PAGES_IMPL=tc, decode_tc.cu: codes -> TMEM, tcgen05.mma with
-    per-page scaled B operands) -- an A/B variant of the mma.sync page kernel -- passes the same
-    oracle parity tests (G = 1 / 4 / 8, flushes, partial pages, split units, the headline shape)."""
+@pytest.mark.parametrize("env", [{"MKV_PAGES_IMPL": "tc"}, {"MKV_FLUSH": "fused"}],
+                         ids=["tcgen05-page-pass", "fused-flush"])
+def test_decode_variant_parity(env):
+    """The decode variants kept as measured A/Bs pass the same oracle parity tests (G = 1 / 4 / 8,
+    flushes, partial pages, split units, the headline shape, bit-identity of the multi-layer
+    call): MKV_PAGES_IMPL=tc -- the tcgen05 page pass (decode_tc.cu: codes -> TMEM,
+    tcgen05.mma with per-page scaled B operands); MKV_FLUSH=fused -- the residual flush done by
+    the finish kernel of the step that fills the block (pages built there, the block attended
+    dequantized, the next plan uploaded off the critical path)."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, MKV_PAGES_IMPL="tc")
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", os.path.join(root, "tests", "test_gpu_decode.py"),
-                        "-k", "not tcgen05"], cwd=root, env=env, capture_output=True, text=True, timeout=1200)
+                        "-k", "not variant"], cwd=root, env=dict(os.environ, **env), capture_output=True, text=True,
+                       timeout=1200)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
