@@ -796,14 +796,15 @@ def run_prefill_bench(args):
     except mkv.MkvError as e:
         return {"unavailable": str(e)}
     torch.cuda.synchronize()
-    reps = 3
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(reps):
+    reps = []
+    for _ in range(5):  # median of 5 launches (each timed with CUDA events)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
         r = mkv.selective_flash_attn(q, k, v, scale, True)
-    e1.record()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / reps
+        e1.record()
+        torch.cuda.synchronize()
+        reps.append(e0.elapsed_time(e1))
+    ms = sorted(reps)[len(reps) // 2]
     P = L * (L + 1) / 2
     flops = Hq * 6 * d * P
     acs = float(r.a_cumul.double().sum().item())
