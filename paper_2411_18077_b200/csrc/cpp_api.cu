@@ -348,6 +348,8 @@ void append_block(QuantizedTensor& t, const Matrix& block) {
 Matrix dequantize_matrix(const QuantizedTensor& t) {
     Matrix m(t.logical_rows, t.logical_cols);
     Dev d(std::max<size_t>(t.logical_rows * t.logical_cols, 1) * sizeof(float));
+    // rows past the blocks (an inconsistent tensor) stay 0, as in the reference's Matrix
+    cuda_check(cudaMemset(d.p, 0, std::max<size_t>(t.logical_rows * t.logical_cols, 1) * sizeof(float)), "memset");
     const size_t rows = dequantize_device(t, d.as<float>(), (int64_t)t.logical_cols);
     if (rows * t.logical_cols)
         cuda_check(cudaMemcpy(m.data.data(), d.p, rows * t.logical_cols * sizeof(float), cudaMemcpyDeviceToHost),
@@ -486,6 +488,7 @@ size_t stack_device(const KVCacheLayer& c, bool values, Dev& out) {
     const size_t nq = c.mode == QuantMode::Identity ? fp.rows : t.logical_rows;
     const size_t n = nq + res.rows;
     out = Dev(std::max<size_t>(n * c.d, 1) * sizeof(float));
+    cuda_check(cudaMemset(out.p, 0, std::max<size_t>(n * c.d, 1) * sizeof(float)), "memset");
     if (c.mode == QuantMode::Identity) {
         if (nq)
             cuda_check(cudaMemcpy(out.p, fp.data.data(), nq * c.d * sizeof(float), cudaMemcpyHostToDevice), "upload");
