@@ -79,7 +79,7 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 // ---------------------------------------------------------------------------
 struct Plan {
     std::vector<int32_t> sig;  // per unit (pages, prefill rows) the plan was built for
-    int total = 0, chunk = 0, grid = 0;
+    int total = 0, warps = 0, grid = 0;  // padded pages, workers (balanced ranges), CTAs
     int32_t* d_pref = nullptr;    // [n_units + 1] local page prefix, then [warps] first unit per warp
     int32_t* d_wstart = nullptr;
     UnitRec* d_rec = nullptr;     // [n_units]
@@ -92,7 +92,7 @@ struct Plan {
     int cur = 0;
     bool pending = false;
     std::vector<int32_t> pending_sig;
-    int p_total = 0, p_chunk = 0, p_grid = 0;
+    int p_total = 0, p_warps = 0, p_grid = 0;
     cudaEvent_t ready = nullptr;
     void* h_stage = nullptr;      // pinned staging of the pending upload
     size_t stage_bytes = 0;
@@ -537,23 +537,35 @@ static void range_signature(const mkv_cache* c, int ub, int n, std::vector<int32
 struct HostPlan {
     std::vector<int32_t> buf;
     std::vector<UnitRec> rec;
-    int total = 0, chunk = 0, warps = 0, grid = 0;
+    int total = 0, warps = 0, grid = 0;
 };
 static size_t plan_ints(const mkv_cache* c) { return ((c->n_units + 1 + (size_t)num_sms() * kMaxPagesWarps + 3) / 4) * 4; }
+// CTAs of the page pass (one per SM at most): MKV_PAGE_CTAS overrides (A/B of leaving SMs to
+// the co-scheduled finish kernels)
+static int page_ctas() {
+    static const int n = [] {
+        const char* e = getenv("MKV_PAGE_CTAS");
+        const int v = e ? atoi(e) : 0;
+        return (v > 0 && v <= num_sms()) ? v : num_sms();
+    }();
+    return n;
+}
 static void host_plan(const mkv_cache* c, int ub, int n, HostPlan& hp) {
     const PagesConfig pc = pages_config();
     const int wpc = pc.warps, bm = pc.batch - 1;
-    const int max_warps = num_sms() * wpc;
+    const int max_warps = page_ctas() * wpc;
     hp.buf.assign(plan_ints(c), 0);
     int32_t* pref = hp.buf.data();
     for (int i = 0; i < n; ++i) pref[i + 1] = pref[i] + ((c->n_pages[ub + i] + bm) & ~bm);
     hp.total = pref[n];
-    const int min_chunk = std::max(8, pc.batch);
-    hp.chunk = (std::max(min_chunk, (hp.total + max_warps - 1) / std::max(max_warps, 1)) + bm) & ~bm;
-    hp.warps = hp.total > 0 ? (hp.total + hp.chunk - 1) / hp.chunk : 0;
+    // balanced worker ranges (range_begin): every worker >= 2 batches (>= 8 pages for the
+    // mma.sync pass), at most one worker per resident warp slot
+    const int T = hp.total / pc.batch;
+    const int min_batches = std::max(1, 8 / pc.batch);
+    hp.warps = T > 0 ? std::max(1, std::min(max_warps, T / min_batches)) : 0;
     int32_t* wstart = pref + n + 1;
-    for (int w = 0, i = 0; w < hp.warps; ++w) {  // first unit with pages that contains page w*chunk
-        const int p = w * hp.chunk;
+    for (int w = 0, i = 0; w < hp.warps; ++w) {  // first unit with pages that contains the range's first page
+        const int p = pc.batch * range_begin(w, T, hp.warps);
         while (i < n - 1 && pref[i + 1] <= p) ++i;
         wstart[w] = i;
     }
@@ -606,7 +618,7 @@ static int get_plan(mkv_cache* c, int ub, int n, cudaStream_t s, Plan** out, Pla
         pl.cur ^= 1;
         plan_point(c, pl, n);
         pl.sig = sig;
-        pl.total = pl.p_total; pl.chunk = pl.p_chunk; pl.grid = pl.p_grid;
+        pl.total = pl.p_total; pl.warps = pl.p_warps; pl.grid = pl.p_grid;
         pl.pending = false;
         if (swapped) *swapped = true;
         *out = &pl;
@@ -618,7 +630,7 @@ static int get_plan(mkv_cache* c, int ub, int n, cudaStream_t s, Plan** out, Pla
     if (int r = plan_alloc(c, pl, n)) return r;
     if (jobs && jobs->n_jobs < kMaxPlanJobs && n > 0) {
         PlanBuildJob& jb = jobs->job[jobs->n_jobs++];
-        jb.unit_begin = ub; jb.n = n; jb.chunk = hp.chunk; jb.warps = hp.warps; jb.batch = pages_config().batch;
+        jb.unit_begin = ub; jb.n = n; jb.warps = hp.warps; jb.batch = pages_config().batch;
         jb.pref = pl.d_pref; jb.wstart = pl.d_wstart; jb.rec = pl.d_rec;
     } else {
         CK(cudaMemcpyAsync(pl.d_pref, hp.buf.data(), sizeof(int32_t) * (n + 1 + hp.warps), cudaMemcpyHostToDevice, s));
@@ -626,7 +638,7 @@ static int get_plan(mkv_cache* c, int ub, int n, cudaStream_t s, Plan** out, Pla
     }
     pl.sig = sig;
     pl.total = hp.total;
-    pl.chunk = hp.chunk;
+    pl.warps = hp.warps;
     pl.grid = hp.grid;
     *out = &pl;
     return MKV_OK;
@@ -662,7 +674,7 @@ static int prepare_next_plan(mkv_cache* c, int ub, int n, cudaStream_t s) {
     CK(cudaEventRecord(pl.ready, c->copy_stream));
     range_signature(c, ub, n, pl.pending_sig);
     pl.pending = true;
-    pl.p_total = hp.total; pl.p_chunk = hp.chunk; pl.p_grid = hp.grid;
+    pl.p_total = hp.total; pl.p_warps = hp.warps; pl.p_grid = hp.grid;
     return MKV_OK;
 }
 
@@ -700,8 +712,8 @@ static uint64_t* trace_slot(mkv_cache* c) {
 static void fill_pages_params(mkv_cache* c, const Plan* pl, const mkv_decode_args* a, PagesParams& pp) {
     pp.pool = c->d_pool; pp.meta = c->d_meta; pp.unit_begin = a->unit_begin; pp.n_units = a->n_units;
     pp.group = a->group; pp.q = static_cast<const __half*>(a->q);
-    pp.pref = pl->d_pref; pp.wstart = pl->d_wstart; pp.rec = pl->d_rec; pp.chunk = pl->chunk; pp.total_pages = pl->total;
-    pp.n_warps = pl->grid * pages_config().warps;
+    pp.pref = pl->d_pref; pp.wstart = pl->d_wstart; pp.rec = pl->d_rec; pp.total_pages = pl->total;
+    pp.n_warps = pl->warps;
     pp.part_ml = pl->d_part_ml; pp.part_o = pl->d_part_o;
     pp.scale_log2 = a->scale * 1.4426950408889634f;
     pp.trace = trace_slot(c);
@@ -812,7 +824,8 @@ static int decode_impl(mkv_cache* c, const mkv_decode_args* a, bool attend, cuda
     rp.part_ml = pl->d_part_ml; rp.part_o = pl->d_part_o;
     rp.trace = trace_slot(c);
     if (rp.trace) rp.trace += trace_page_words();
-    CK(launch_finish(rp, pl->d_pref, std::max(pl->chunk, 1), pl->total > 0, s));
+    const WorkerRanges wr{std::max(pl->warps, 1), std::max(pl->total / pages_config().batch, 1), pages_config().batch};
+    CK(launch_finish(rp, pl->d_pref, wr, pl->total > 0, s));
     ++c->trace_seq;
     // the next call's plan (new page counts), prepared and uploaded off the critical path
     if (fused && any_flush)

@@ -127,8 +127,10 @@ __global__ void __maxnreg__(208) pages_kernel(const PagesParams P) {
         }
     };
     stamp(0);
-    const int start = wg * P.chunk;
-    const int end = min(start + P.chunk, P.total_pages);
+    const int T = P.total_pages / kBatch;
+    if (wg >= P.n_warps) return;
+    const int start = kBatch * range_begin(wg, T, P.n_warps);
+    const int end = kBatch * range_begin(wg + 1, T, P.n_warps);
     if (start >= end) return;
     const int G = P.group;
     const int qchunks = G * kHeadDim * 2 / 16;
@@ -609,8 +611,9 @@ __global__ void __launch_bounds__(kPlanThreads) plan_build_kernel(const UnitMeta
     if (tid == 0) jb.pref[n] = part[kPlanThreads];
     __syncthreads();
     // first unit of warp w's range: the smallest i with pref[i + 1] > w * chunk (n - 1 at most)
+    const int T = part[kPlanThreads] / jb.batch;
     for (int w = tid; w < jb.warps; w += kPlanThreads) {
-        const int p = w * jb.chunk;
+        const int p = jb.batch * range_begin(w, T, jb.warps);
         int lo = 0, hi = n - 1;
         while (lo < hi) {
             const int mid = (lo + hi) >> 1;
@@ -657,7 +660,7 @@ __device__ __forceinline__ void ldmatrix_x4_trans(uint32_t (&r)[4], const void* 
 }
 
 __global__ void __launch_bounds__(kFinishThreads, 5) finish_kernel(const ResidualParams P, const int32_t* __restrict__ pref,
-                                                                   int chunk) {
+                                                                   const WorkerRanges wr) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
     const int slot = P.fused_flush ? kFinishSlotFlush : kFinishSlot;
     float (*wml)[2][kMaxG] = reinterpret_cast<float (*)[2][kMaxG]>(smem_raw + kFinishWarps * slot);
@@ -674,7 +677,8 @@ __global__ void __launch_bounds__(kFinishThreads, 5) finish_kernel(const Residua
     const bool flush = app && P.fused_flush && n == P.n_r;  // this append fills the residual block
     const int ntiles = (n + 15) >> 4;
     const int upre = pref[i], uend = pref[i + 1];
-    const int w_first = upre / chunk, w_last = (uend > upre) ? (uend - 1) / chunk : w_first - 1;
+    const int w_first = uend > upre ? worker_of_batch(upre / wr.batch, wr.total_batches, wr.workers) : 0;
+    const int w_last = uend > upre ? worker_of_batch((uend - 1) / wr.batch, wr.total_batches, wr.workers) : -1;
     const int n_part = w_last - w_first + 1;
     __half* rk = P.res_k + (size_t)u * P.n_r * d;
     __half* rv = P.res_v + (size_t)u * P.n_r * d;
@@ -918,7 +922,8 @@ __global__ void __launch_bounds__(kFinishThreads, 5) finish_kernel(const Residua
     fstamp(3);
 }
 
-cudaError_t launch_finish(const ResidualParams& p, const int32_t* pref, int chunk, bool after_pages, cudaStream_t s) {
+cudaError_t launch_finish(const ResidualParams& p, const int32_t* pref, WorkerRanges wr, bool after_pages,
+                          cudaStream_t s) {
     const size_t smem = finish_smem_bytes(p.fused_flush ? kFinishSlotFlush : kFinishSlot);
     static bool configured = false;
     if (!configured) {
@@ -930,10 +935,10 @@ cudaError_t launch_finish(const ResidualParams& p, const int32_t* pref, int chun
     // PDL only behind a page kernel: a finish that follows another finish (no pages) reads
     // the n_res / residual rows that kernel writes, so it needs the full dependency
     if (!after_pages) {
-        finish_kernel<<<p.n_units, kFinishThreads, smem, s>>>(p, pref, chunk);
+        finish_kernel<<<p.n_units, kFinishThreads, smem, s>>>(p, pref, wr);
         return cudaGetLastError();
     }
-    return launch_pdl(finish_kernel, dim3(p.n_units), dim3(kFinishThreads), smem, s, p, pref, chunk);
+    return launch_pdl(finish_kernel, dim3(p.n_units), dim3(kFinishThreads), smem, s, p, pref, wr);
 }
 
 }  // namespace mkv

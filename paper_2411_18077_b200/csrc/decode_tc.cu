@@ -250,8 +250,9 @@ __global__ void __maxnreg__(160) pages_tc_kernel(const PagesParams P) {
     const uint32_t tmem = *tmem_word + (uint32_t)(wg * 256);
 
     const int worker = blockIdx.x * 2 + wg;
-    const int start = worker * P.chunk;
-    const int end = min(start + P.chunk, P.total_pages);
+    const int Tb = P.total_pages / kTcBatch;
+    const int start = worker < P.n_warps ? kTcBatch * range_begin(worker, Tb, P.n_warps) : 0;
+    const int end = worker < P.n_warps ? kTcBatch * range_begin(worker + 1, Tb, P.n_warps) : 0;
     const bool active = start < end;
     // diagnostics (P.trace): globaltimer stamps of batches 4..7 of this worker
     auto stamp = [&](int b, int base, int per, int k) {

@@ -44,6 +44,18 @@ cudaError_t launch_select(const SelectParams& p, cudaStream_t s);
 cudaError_t launch_score_variance(const float* a, int64_t a_stride, int n, int length, float* out, cudaStream_t s);
 
 // ---- K4: decode (decode.cu) ----
+// Balanced worker ranges: the plan's padded page sequence is T = total_pages / batch whole
+// batches; worker w of W owns batches [range_begin(w), range_begin(w + 1)) -- range sizes
+// differ by at most one batch, so every SM gets the same share of pages (a fixed chunk rounded
+// up to whole batches left up to 1/16 of the SMs' capacity idle).
+__host__ __device__ inline int range_begin(int w, int T, int W) { return (int)(((int64_t)w * T) / W); }
+// the worker whose range holds batch b (the largest w with range_begin(w) <= b)
+__host__ __device__ inline int worker_of_batch(int b, int T, int W) { return (int)((((int64_t)b + 1) * W - 1) / T); }
+struct WorkerRanges {
+    int workers;        // W
+    int total_batches;  // T
+    int batch;          // pages per batch
+};
 struct ResidualParams {
     UnitMeta* meta;
     int unit_begin, n_units, group, n_r;
@@ -74,7 +86,8 @@ struct AppendSegs {
     const __half* v_new[kMaxAppendSegs];
 };
 cudaError_t launch_append_segments(const ResidualParams& p, const AppendSegs& segs, cudaStream_t s);
-cudaError_t launch_finish(const ResidualParams& p, const int32_t* pref, int chunk, bool after_pages, cudaStream_t s);
+cudaError_t launch_finish(const ResidualParams& p, const int32_t* pref, WorkerRanges wr, bool after_pages,
+                          cudaStream_t s);
 
 // Per-unit page-run record of a K4 plan (host-computed from the cache mirror).
 struct UnitRec {
@@ -86,7 +99,7 @@ struct UnitRec {
 };
 // device-side plan construction (flush steps of a multi-layer call)
 struct PlanBuildJob {
-    int unit_begin, n, chunk, warps, batch;
+    int unit_begin, n, warps, batch;
     int32_t* pref;    // [n + 1]
     int32_t* wstart;  // [warps]
     UnitRec* rec;     // [n]
@@ -106,7 +119,7 @@ struct PagesParams {
     const int32_t* pref;    // [n_units + 1] local page prefix
     const int32_t* wstart;  // [n_warps] first (non-empty) unit of each warp's page range
     const UnitRec* rec;     // [n_units]
-    int chunk, total_pages, n_warps;
+    int total_pages, n_warps;  // padded pages of the plan; W = workers with a (balanced) range
     float* part_ml;         // [slots][2][kMaxG]   slot = warp + unit
     float* part_o;          // [slots][kMaxG][d]
     float scale_log2;
