@@ -352,3 +352,41 @@ def test_decode_variant_parity(env):
                         "-k", "not variant"], cwd=root, env=dict(os.environ, **env), capture_output=True, text=True,
                        timeout=1200)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+def test_decode_256k_mha_units_parity(mkv):
+    """configs[4]'s decode units (LWM-Text-7B MHA, 256K context, G = 1) at the pyramid's extreme
+    layers (hh 48683 and 3745, rw 26214: ~4.7K and ~1.9K pages per unit), through a flush, against
+    the oracle per head."""
+    from tests.gpu_util import f32
+    d, G, L, n_r = 128, 1, 262144, 128
+    P = oracle.port()
+    hh_all = [int(h) for h in P.allocate_pyramid(int(0.10 * L), 32, 7, True)]
+    rw = int(0.10 * L)
+    hh = [hh_all[0], hh_all[-1]]
+    n = 2
+    k = mkv.synth_fp16((n, L * d), SEED, 2 << 48, 1 << 16).view(n, L, d)
+    v = mkv.synth_fp16((n, L * d), SEED, 3 << 48, 1 << 16).view(n, L, d)
+    a = mkv.synth_uniform((n, L), SEED, 7 << 48, 1 << 16)
+    cache = mkv.KVCache(n, [h + rw for h in hh], max_decode_tokens=256, n_r=n_r)
+    cache.prefill(k, v, a, hh, rw)
+    kh, vh, ah = k.cpu().numpy(), v.cpu().numpy(), a.cpu().numpy()
+    ocs = []
+    for u in range(n):
+        oc = P.cache(d=d, n_r=n_r)
+        oc.prefill(f32(kh[u]), f32(vh[u]), ah[u], hh[u], rw)
+        ocs.append(oc)
+    scale = 1.0 / np.sqrt(d)
+    worst = 0.0
+    for s in range(130):
+        q = mkv.synth_fp16((n, G * d), SEED, (4 << 48) | (s + 1), 1 << 16).view(n, G, d)
+        tk = mkv.synth_fp16((n, d), SEED, (5 << 48) | (s + 1), 1 << 16)
+        tv = mkv.synth_fp16((n, d), SEED, (6 << 48) | (s + 1), 1 << 16)
+        out = cache.decode_step(q, tk, tv, scale).float().cpu().numpy()
+        qh, tkh, tvh = q.cpu().numpy(), tk.cpu().numpy(), tv.cpu().numpy()
+        for u in range(n):
+            ocs[u].append(f32(tkh[u]), f32(tvh[u]))
+            if s in (0, 126, 127, 129):
+                worst = max(worst, max_abs(out[u, 0], ocs[u].attend(f32(qh[u, 0]), scale, param_fp16=True)))
+    cache.check()
+    assert worst <= TOL, worst

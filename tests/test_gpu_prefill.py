@@ -135,3 +135,24 @@ def test_prefill_128k_sampled_rows_and_columns(mkv):
     assert res["x_o_max_abs"] <= TOL_O, res
     assert res["lse_max_abs"] <= TOL_LSE, res
     assert res["a_cumul_excess_over_rel_tol"] <= TOL_A_ABS, res
+
+
+def test_prefill_256k_mha_sampled_rows_and_columns(mkv):
+    """configs[4]'s prefill layer (LWM-Text-7B: 32 MHA heads, 256K causal): sampled X_O / LSE rows
+    and A_cumul columns against the reference (as the 128K test), plus sum A_cumul = lq per head."""
+    import bench
+    Hq = Hkv = 32
+    L, d = 262144, 128
+    q = mkv.synth_fp16((1, Hq, L, d), SEED, 1 << 48, 1 << 16)
+    k = mkv.synth_fp16((1, Hkv, L, d), SEED, 2 << 48, 1 << 16)
+    v = mkv.synth_fp16((1, Hkv, L, d), SEED, 3 << 48, 1 << 16)
+    scale = 1.0 / math.sqrt(d)
+    r = mkv.selective_flash_attn(q, k, v, scale, True)
+    torch.cuda.synchronize()
+    sums = r.a_cumul[0].double().sum(-1)
+    assert float((sums - L).abs().max()) <= 1e-3 * L
+    res = bench.prefill_parity(q, k, v, r, Hq, Hkv, L, d, scale, rows=(0, 131071, L - 1),
+                               cols=[0, 5, L // 2, L - 3, L - 1])
+    assert res["x_o_max_abs"] <= TOL_O, res
+    assert res["lse_max_abs"] <= TOL_LSE, res
+    assert res["a_cumul_excess_over_rel_tol"] <= TOL_A_ABS, res
