@@ -215,12 +215,14 @@ __global__ void __maxnreg__(208) pages_kernel(const PagesParams P) {
     prefetch_q(ci);
 
     int cg = start;
+    int n_segments = 0;  // diagnostics (trace word 3)
     int stage = 0;
     uint32_t phase = 0;
     const float sl2 = P.scale_log2;
     const float sk = kTwo24 * sl2;
 
     while (cg < end) {
+        ++n_segments;
         const int unit = ci;
         const int upre = rec_pbeg(unit);
         const int uend_g = rec_pend(unit);
@@ -427,6 +429,7 @@ __global__ void __maxnreg__(208) pages_kernel(const PagesParams P) {
         }
     }
     stamp(2);
+    if (P.trace != nullptr && lane == 0) P.trace[(size_t)wg * 4 + 3] = (uint64_t)n_segments;
     if (P.early) asm volatile("griddepcontrol.wait;\n" ::: "memory");
 }
 
@@ -458,7 +461,10 @@ PagesConfig pages_config() {
         PagesConfig c{8, 2, 4, 0};
         if (const char* e = getenv("MKV_PAGES_CFG")) {
             int w = 0, st = 0;
-            if (sscanf(e, "%dx%d", &w, &st) == 2 && w == 8 && (st == 2 || st == 3)) c.stages = st;
+            if (sscanf(e, "%dx%d", &w, &st) == 2 && (w == 8 || w == 4) && (st == 2 || st == 3)) {
+                c.warps = w;
+                c.stages = st;
+            }
         }
         const char* impl = getenv("MKV_PAGES_IMPL");
         if (impl && impl[0] == 't') c = PagesConfig{2, 3, 8, 1};
@@ -470,6 +476,7 @@ PagesConfig pages_config() {
 cudaError_t launch_pages(const PagesParams& p, int grid, cudaStream_t s, bool pdl) {
     const PagesConfig c = pages_config();
     if (c.tc) return launch_pages_tc(p, grid, s, pdl);
+    if (c.warps == 4) return c.stages == 3 ? launch_pages_t<4, 3>(p, grid, s, pdl) : launch_pages_t<4, 2>(p, grid, s, pdl);
     if (c.stages == 3) return launch_pages_t<8, 3>(p, grid, s, pdl);
     return launch_pages_t<8, 2>(p, grid, s, pdl);
 }
