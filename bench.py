@@ -12,10 +12,13 @@ heads, d = 128, 32 layers, pyramid budget, 20% = 10% HH + 10% RW of a 32K contex
 
 A "step" = one decode step through all 32 layers: per layer decode_append (+ the n_r flush)
 and 2-bit attention over [pages ; residual] for every (seq, kv-head) unit (K4).  ``value``
-is whole-job decode tokens/s with inputs resident in HBM (every layer's q known up front:
-mkv_decode_step_layers); ``serving`` is the same with one mkv_decode_step per layer and
-layer l+1's q = layer l's output (the dependency a model has); ``e2e`` is the same metric
-through the C ABI with pinned host buffers copied in and out inside the timed region.
+is whole-job decode tokens/s with inputs resident in HBM, every layer's q known up front (the
+reference arm's workload: independent units): one mkv_decode_step_layers call whose 32 layers
+are laid out back to back, which the call runs as ONE page pass + ONE finish pass over all
+(layer, seq, kv-head) units (MKV_LAYERS_SPLIT=1: one pass per layer, the A/B).  ``serving`` is
+the same step as 32 mkv_decode_step calls with layer l+1's q = layer l's output (the
+dependency a model has); ``e2e`` is ``value``'s form through the C ABI with pinned host buffers
+copied in and out inside the timed region.
 
 Also reported on rank 0 at N = 1: ``parity`` (the GPU decode outputs of the last timed step
 vs the unmodified reference decode on the CPU sample units, same synthetic streams and the
@@ -51,6 +54,7 @@ sys.path.insert(0, ROOT)
 UNIT = "tokens/s"
 SEED = 2024
 DECODE_TOL = 5e-3  # max |t_O - reference| (SURVEY 8(d) tolerances)
+SPLIT = bool(os.environ.get("MKV_LAYERS_SPLIT"))  # A/B: one page + finish pass per layer
 
 LLAMA = dict(layers=32, n_q_heads=32, n_kv_heads=8, head_dim=128, context=32768,
              alpha_hh=0.10, alpha_rw=0.10, pyramid_depth=7, n_r=128, group_size=16)
@@ -214,13 +218,14 @@ class ClockSampler:
                 "samples": len(rows), "source": src, "nvidia_smi_samples": len(smi_rows)}
 
 
-def load_traffic(kernel):
-    """DRAM bytes per launch of `kernel` from the newest committed ncu capture (profiles/), or None."""
-    for name in ("r2_pages_traffic.json", "r1_pages_traffic.json"):
+def load_traffic(kernel, launch_units):
+    """DRAM bytes per launch of `kernel` over `launch_units` units from the newest committed ncu
+    capture of that launch shape (profiles/), or None."""
+    for name in ("r2_pages_traffic_all_layers.json", "r2_pages_traffic.json", "r1_pages_traffic.json"):
         try:
             with open(os.path.join(ROOT, "profiles", name)) as f:
                 t = json.load(f)
-            if t.get("kernel") == kernel:
+            if t.get("kernel") == kernel and t.get("launch_units", 128) == launch_units:
                 return float(t["traffic_bytes_per_launch"]), f"profiles/{name}"
         except Exception:
             continue
@@ -349,6 +354,8 @@ def run_mkv(args, rank, world):
     all_args = [step_args(s) for s in range(steps_total)]
 
     def do_step(s):
+        # q / k / v / out of the 32 layers are back to back ([NL, upl, ...]): the call coalesces
+        # them into one page pass + one finish pass over all n_units (MKV_LAYERS_SPLIT=1: one per layer)
         _capi.check(L_.mkv_decode_step_layers(cache.h, NL, all_args[s], sp), "decode")
 
     # pre-roll residual appends so that exactly one n_r flush lands inside the timed steps (the
@@ -393,9 +400,10 @@ def run_mkv(args, rank, world):
     res = dict(ms_per_step=ms_per_step, tokens_per_s=tokens_per_s,
                hbm_gbs=dist_max(bytes_timed, 1) / (ms / 1e3) / 1e9,
                setup_s=setup_s, preroll=preroll, flushes_in_timed=flushes,
-               # per step: a page kernel + a finish kernel per layer; a flush step adds ONE append
-               # launch for every layer and one plan-build launch (mkv_decode_step_layers)
-               gpu_launches=args.steps * NL * 2 + 2 * flushes,
+               # coalesced (default): a page kernel + a finish kernel per step, a flush step adds one
+               # append launch for every unit.  MKV_LAYERS_SPLIT: both per layer, and a flush step
+               # adds one append launch for every layer and one plan-build launch.
+               gpu_launches=(args.steps * NL * 2 + 2 * flushes) if SPLIT else (args.steps * 2 + flushes),
                B_local=B_local, upl=upl, n_units=n_units, pages=base_pages)
     # bytes of every rank (whole-job GB/s)
     if world > 1:
@@ -435,21 +443,25 @@ def run_mkv(args, rank, world):
                 "no host round trip): each page kernel waits for the previous layer's merge",
             steps=s_steps)
 
-    # ---- dominant kernel alone (K4 page kernel), CUDA events on its stream ----
+    # ---- dominant kernel alone (K4 page kernel, as the timed steps launch it: one launch over
+    #      all n_units, or one per layer under MKV_LAYERS_SPLIT), CUDA events on its stream ----
     reps = 20
-    attend_args = step_args(steps_total - 1)
+    s_last = steps_total - 1
+    attend_args = step_args(s_last) if SPLIT else [
+        _capi.DecodeArgs(0, n_units, G, qs[s_last].data_ptr(), None, None, out.data_ptr(), scale)]
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(reps):
-        for l in range(NL):
-            _capi.check(L_.mkv_decode_pages_only(cache.h, C.byref(attend_args[l]), sp), "pages")
+        for a_ in attend_args:
+            _capi.check(L_.mkv_decode_pages_only(cache.h, C.byref(a_), sp), "pages")
     e1.record(stream)
     torch.cuda.synchronize()
-    k_ms = e0.elapsed_time(e1) / (reps * NL)
+    k_ms = e0.elapsed_time(e1) / (reps * len(attend_args))
     page_bytes_per_launch = (sum(cache.unit_info(u)["n_pages"] for u in range(n_units)) * 2048 +
-                             n_units * G * d * 2 * 2) / NL
+                             n_units * G * d * 2 * 2) / len(attend_args)
     res["kernel"] = dict(name="mkv::pages_kernel", avg_launch_ms=k_ms, bytes_per_launch=page_bytes_per_launch,
+                         launch_units=n_units // len(attend_args),
                          gbs=page_bytes_per_launch / (k_ms / 1e3) / 1e9)
 
     # ---- e2e through the C ABI with host buffers (pinned), copies inside the timed region.
@@ -1018,7 +1030,7 @@ def main():
     if rank != 0:
         return
     kern = res["kernel"]
-    traffic, traffic_src = load_traffic(kern["name"]) if args.workload == "llama3-8b" and world == 1 else (None, None)
+    traffic, traffic_src = load_traffic(kern["name"], kern["launch_units"]) if args.workload == "llama3-8b" and world == 1 else (None, None)
     line = {
         "metric": W["metric"], "value": res["tokens_per_s"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": res["ms_per_step"], "higher_is_better": True,
@@ -1030,11 +1042,17 @@ def main():
         "roofline": {"bound": "hbm", "achieved": kern["gbs"], "peak": hbm_peak, "unit": "GB/s",
                      "frac": kern["gbs"] / hbm_peak, "traffic": traffic, "traffic_source": traffic_src,
                      "kernel": kern["name"], "avg_launch_ms": kern["avg_launch_ms"],
-                     "bytes_per_launch": kern["bytes_per_launch"], "peak_kind": peak_kind},
+                     "bytes_per_launch": kern["bytes_per_launch"], "launch_units": kern["launch_units"],
+                     "peak_kind": peak_kind},
         "step_roofline_frac": res["hbm_gbs"] / (hbm_peak * world),
         "e2e": res["e2e"], "gpu_launches": res["gpu_launches"], "clocks": res["clocks"],
         "serving": res.get("serving"), "setup_s": res["setup_s"],
         "flushes_in_timed": res["flushes_in_timed"],
+        "step_form": ("per layer: 32 page + 32 finish passes per step, layer l+1's page pass overlapping "
+                      "layer l's merge (MKV_LAYERS_SPLIT)") if SPLIT else
+                     ("every layer's q known up front: mkv_decode_step_layers over [32 layers x units] back to "
+                      "back = one page pass + one finish pass over all units per step; 'serving' is the "
+                      "dependent per-layer form"),
     }
     line.update({k: extras.get(k) for k in ("cpu_baseline", "parity", "config0", "prefill")})
     print(json.dumps(line))

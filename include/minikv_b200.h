@@ -216,8 +216,13 @@ int mkv_decode_pages_only(mkv_cache* cache, const mkv_decode_args* args, void* s
  * runs with MKV_DECODE_TRACE set): 4 globaltimer stamps per warp {start, after
  * griddepcontrol.wait, pages done, 0}.  Returns words written. */
 int mkv_debug_decode_trace(const mkv_cache* cache, uint64_t* out, int max_words);
-/* Multi-layer decode step: n_layers consecutive mkv_decode_step calls in one FFI crossing
- * (same results, bit for bit, for any unit ranges, overlapping or not).
+/* Multi-layer decode step: n_layers consecutive mkv_decode_step calls in one FFI crossing.
+ * Layers that continue each other -- adjacent unit ranges, the same group and scale, and
+ * q / out / k_new / v_new back to back as in one [layers][units] array -- are coalesced into ONE
+ * pass over all their units (one page kernel + one finish kernel for the run): bit-identical
+ * to one mkv_decode_step over those units, equal to per-layer calls up to the fp32 rounding of
+ * a different split-K partition (MKV_LAYERS_SPLIT=1 disables coalescing).  Any other layer
+ * list (overlapping ranges included) gives the per-layer calls' results bit for bit.
  * Precondition -- every layer's q / k_new / v_new is already written when the call is made
  * (stream-ordered before it), and none of them aliases an earlier layer's `out`: a layer whose
  * unit range is disjoint from every earlier layer's starts its page pass (reading its q) while

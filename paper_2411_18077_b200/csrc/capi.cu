@@ -598,6 +598,26 @@ static int plan_alloc(mkv_cache* c, Plan& pl, int n) {
     return MKV_OK;
 }
 
+// A plan's host image ([ints plan_ints][UnitRec n], the layout of one d_buf) in the plan's pinned
+// staging buffer, once the previous upload from it has completed (pl.ready): uploads are then
+// plain DMA in stream order, never a host-blocking pageable copy.
+static int stage_plan(mkv_cache* c, Plan& pl, const HostPlan& hp, int n, size_t* bytes) {
+    if (!pl.ready) CK(cudaEventCreateWithFlags(&pl.ready, cudaEventDisableTiming));
+    CK(cudaEventSynchronize(pl.ready));
+    const size_t ib = sizeof(int32_t) * plan_ints(c), rb = sizeof(UnitRec) * n;
+    if (pl.stage_bytes < ib + rb) {
+        if (pl.h_stage) cudaFreeHost(pl.h_stage);
+        pl.h_stage = nullptr;
+        pl.stage_bytes = 0;
+        CK(cudaMallocHost(&pl.h_stage, ib + rb));
+        pl.stage_bytes = ib + rb;
+    }
+    memcpy(pl.h_stage, hp.buf.data(), ib);
+    memcpy(static_cast<uint8_t*>(pl.h_stage) + ib, hp.rec.data(), rb);
+    *bytes = ib + rb;
+    return MKV_OK;
+}
+
 // jobs != nullptr: a changed plan is not uploaded but queued for plan_build_kernel (the
 // caller launches it once the device meta holds the new page counts).  *swapped: the plan was
 // prepared ahead and uploaded on the copy stream (the stream now waits for it; the caller
@@ -633,8 +653,10 @@ static int get_plan(mkv_cache* c, int ub, int n, cudaStream_t s, Plan** out, Pla
         jb.unit_begin = ub; jb.n = n; jb.warps = hp.warps; jb.batch = pages_config().batch;
         jb.pref = pl.d_pref; jb.wstart = pl.d_wstart; jb.rec = pl.d_rec;
     } else {
-        CK(cudaMemcpyAsync(pl.d_pref, hp.buf.data(), sizeof(int32_t) * (n + 1 + hp.warps), cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(pl.d_rec, hp.rec.data(), sizeof(UnitRec) * n, cudaMemcpyHostToDevice, s));
+        size_t bytes = 0;
+        if (int r = stage_plan(c, pl, hp, n, &bytes)) return r;
+        CK(cudaMemcpyAsync(pl.d_pref, pl.h_stage, bytes, cudaMemcpyHostToDevice, s));
+        CK(cudaEventRecord(pl.ready, s));
     }
     pl.sig = sig;
     pl.total = hp.total;
@@ -655,22 +677,13 @@ static int prepare_next_plan(mkv_cache* c, int ub, int n, cudaStream_t s) {
         CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&c->ev_compute, cudaEventDisableTiming));
     }
-    if (!pl.ready) CK(cudaEventCreateWithFlags(&pl.ready, cudaEventDisableTiming));
-    CK(cudaEventSynchronize(pl.ready));  // the staging buffer's previous upload has completed
     HostPlan hp;
     host_plan(c, ub, n, hp);
-    const size_t ib = sizeof(int32_t) * plan_ints(c), rb = sizeof(UnitRec) * n;
-    if (pl.stage_bytes < ib + rb) {
-        if (pl.h_stage) cudaFreeHost(pl.h_stage);
-        pl.h_stage = nullptr;
-        CK(cudaMallocHost(&pl.h_stage, ib + rb));
-        pl.stage_bytes = ib + rb;
-    }
-    memcpy(pl.h_stage, hp.buf.data(), ib);
-    memcpy(static_cast<uint8_t*>(pl.h_stage) + ib, hp.rec.data(), rb);
+    size_t bytes = 0;
+    if (int r = stage_plan(c, pl, hp, n, &bytes)) return r;
     CK(cudaEventRecord(c->ev_compute, s));
     CK(cudaStreamWaitEvent(c->copy_stream, c->ev_compute, 0));
-    CK(cudaMemcpyAsync(pl.d_buf[pl.cur ^ 1], pl.h_stage, ib + rb, cudaMemcpyHostToDevice, c->copy_stream));
+    CK(cudaMemcpyAsync(pl.d_buf[pl.cur ^ 1], pl.h_stage, bytes, cudaMemcpyHostToDevice, c->copy_stream));
     CK(cudaEventRecord(pl.ready, c->copy_stream));
     range_signature(c, ub, n, pl.pending_sig);
     pl.pending = true;
@@ -863,9 +876,39 @@ int mkv_decode_pages_only(mkv_cache* c, const mkv_decode_args* a, void* stream) 
     return MKV_OK;
 }
 
+// Layer l+1 continues layer l: adjacent unit ranges, the same group and scale, and q / out (and
+// the appended k / v, if any) laid out back to back, as in one [layers][units] array.  Such
+// layers are one batch of independent units -- one page pass and one finish pass cover them.
+static bool continues(const mkv_decode_args& p, const mkv_decode_args& l) {
+    auto at = [](const void* base, int64_t bytes) { return static_cast<const uint8_t*>(base) + bytes; };
+    const int64_t n = p.n_units, G = p.group;
+    if (l.unit_begin != p.unit_begin + p.n_units || l.group != p.group || l.scale != p.scale) return false;
+    if (!p.q || !p.out || l.q != at(p.q, n * G * kHeadDim * 2) || l.out != at(p.out, n * G * kHeadDim * 2)) return false;
+    if ((p.k_new == nullptr) != (l.k_new == nullptr) || (p.v_new == nullptr) != (l.v_new == nullptr)) return false;
+    if (p.k_new && (l.k_new != at(p.k_new, n * kHeadDim * 2) || l.v_new != at(p.v_new, n * kHeadDim * 2))) return false;
+    return true;
+}
+
+static int decode_layers(mkv_cache* c, int n_layers, const mkv_decode_args* a, cudaStream_t s);
+
 int mkv_decode_step_layers(mkv_cache* c, int n_layers, const mkv_decode_args* a, void* stream) {
     if (!a || n_layers < 0) return fail(MKV_ERR_INVALID_ARGUMENT, "decode_step: bad layer list");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    // coalesce runs of continuing layers (MKV_LAYERS_SPLIT=1 keeps one pass per layer: A/B)
+    static const bool split = getenv("MKV_LAYERS_SPLIT") != nullptr;
+    if (split || n_layers < 2) return decode_layers(c, n_layers, a, s);
+    std::vector<mkv_decode_args> runs;
+    runs.reserve(n_layers);
+    for (int l = 0; l < n_layers; ++l) {
+        if (!runs.empty() && a[l].n_units > 0 && runs.back().n_units > 0 && continues(runs.back(), a[l]))
+            runs.back().n_units += a[l].n_units;
+        else
+            runs.push_back(a[l]);
+    }
+    return decode_layers(c, (int)runs.size(), runs.data(), s);
+}
+
+static int decode_layers(mkv_cache* c, int n_layers, const mkv_decode_args* a, cudaStream_t s) {
     // A layer's page kernel may skip its early griddepcontrol.wait (P.early) only if its unit
     // range is disjoint from every earlier layer's range in this call: the early kernel reads
     // meta/plan and triggers its dependents before the previous finish kernel (which appends

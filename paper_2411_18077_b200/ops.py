@@ -319,8 +319,9 @@ class KVCache:
                            scale: float, unit_begin: int = 0, out: Optional[torch.Tensor] = None, stream=None):
         """All layers of one decode step in one call: q fp16 [L, n, G, d], k_new/v_new fp16 [L, n, d]
         (None: attend only); layer l owns units unit_begin + l*n .. + n.  Every q must be written
-        before the call: layers after the first start their page pass while the previous layer's
-        finish kernel is still merging (mkv_decode_step_layers)."""
+        before the call.  Layers laid out back to back (contiguous q / out / k_new / v_new) are
+        one pass over all L * n units; otherwise layers after the first start their page pass
+        while the previous layer's finish kernel is still merging (mkv_decode_step_layers)."""
         L, n, G, d = q.shape
         if out is None:
             out = torch.empty_like(q)

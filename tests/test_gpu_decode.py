@@ -176,11 +176,43 @@ def test_decode_randomized_configs(mkv, seed):
     assert worst <= TOL, (n_units, G, n_r, L, rw, steps, worst)
 
 
+def padded(x):
+    """x [L, n, ...] as a view whose layers are NOT back to back (layer stride n + 1 rows): the
+    per-layer form of mkv_decode_step_layers, which does not coalesce such layers."""
+    big = torch.empty((x.shape[0], x.shape[1] + 1) + tuple(x.shape[2:]), dtype=x.dtype, device=x.device)
+    big[:, :x.shape[1]] = x
+    return big[:, :x.shape[1]]
+
+
+def layers_forms(caches, q, tk, tv, scale, n):
+    """One step through the three forms of a multi-layer decode step, on caches[0..3]:
+      0  mkv_decode_step_layers, layers not back to back -> per-layer page/finish passes with the
+         cross-layer overlap (bit-identical to 1);
+      1  one mkv_decode_step per layer;
+      2  mkv_decode_step_layers on one [L, n] array -> coalesced into a single pass over every
+         layer's units (bit-identical to 3; MKV_LAYERS_SPLIT=1 turns coalescing off -> to 1);
+      3  one mkv_decode_step over all L * n units."""
+    import os
+    layers = q.shape[0]
+    lay = caches[0].decode_step_layers(padded(q), padded(tk), padded(tv), scale, out=torch.empty_like(q))
+    per = torch.stack([caches[1].decode_step(q[l], tk[l], tv[l], scale, unit_begin=l * n) for l in range(layers)])
+    co = caches[2].decode_step_layers(q, tk, tv, scale)
+    flat = caches[3].decode_step(q.reshape(layers * n, *q.shape[2:]), tk.reshape(layers * n, -1),
+                                 tv.reshape(layers * n, -1), scale).view_as(q)
+    assert torch.equal(lay, per), f"per-layer form: max diff {(lay.float() - per.float()).abs().max()}"
+    exp = per if os.environ.get("MKV_LAYERS_SPLIT") else flat
+    assert torch.equal(co, exp), f"coalesced form: max diff {(co.float() - exp.float()).abs().max()}"
+    # a different split-K partition of the same units: equal up to fp32 merge rounding
+    assert (co.float() - per.float()).abs().max().item() <= 2e-3
+
+
 def test_decode_step_layers_matches_per_layer_calls(mkv):
-    """mkv_decode_step_layers overlaps layer l's finish kernel with layer l+1's page pass (q of
-    later layers read before griddepcontrol.wait, partial buffers shared by all layers): its
-    outputs must be bit-identical to one mkv_decode_step per layer, through a flush and with
-    very uneven layer sizes (partials of consecutive layers land in the same slots)."""
+    """mkv_decode_step_layers in both of its forms (layers_forms): per-layer passes that overlap
+    layer l's finish kernel with layer l+1's page pass (q of later layers read before
+    griddepcontrol.wait, partial buffers shared by all layers) are bit-identical to one
+    mkv_decode_step per layer; back-to-back layers are one pass, bit-identical to one
+    mkv_decode_step over all their units -- through a flush and with very uneven layer sizes
+    (partials of consecutive layers land in the same slots)."""
     d, n, G, L, layers, n_r = 128, 12, 4, 2000, 6, 32
     rng = np.random.default_rng(21)
     budgets = [1500, 40, 900, 16, 1200, 300]  # hh per layer: long, tiny, long, ...
@@ -189,7 +221,7 @@ def test_decode_step_layers_matches_per_layer_calls(mkv):
     v = torch.from_numpy(rng.standard_normal((layers * n, L, d)).astype(np.float16)).cuda()
     a = torch.from_numpy(rng.random((layers * n, L)).astype(np.float32)).cuda()
     caches = []
-    for _ in range(2):
+    for _ in range(4):
         c = mkv.KVCache(layers * n, caps, max_decode_tokens=80, n_r=n_r)
         for l in range(layers):
             c.prefill(k[l * n:(l + 1) * n], v[l * n:(l + 1) * n], a[l * n:(l + 1) * n], budgets[l], 64,
@@ -200,18 +232,17 @@ def test_decode_step_layers_matches_per_layer_calls(mkv):
         q = torch.from_numpy(rng.standard_normal((layers, n, G, d)).astype(np.float16)).cuda()
         tk = torch.from_numpy(rng.standard_normal((layers, n, d)).astype(np.float16)).cuda()
         tv = torch.from_numpy(rng.standard_normal((layers, n, d)).astype(np.float16)).cuda()
-        fused = caches[0].decode_step_layers(q, tk, tv, scale)
-        ref = torch.stack([caches[1].decode_step(q[l], tk[l], tv[l], scale, unit_begin=l * n)
-                           for l in range(layers)])
-        assert torch.equal(fused, ref), f"step {s}: max diff {(fused.float() - ref.float()).abs().max()}"
+        layers_forms(caches, q, tk, tv, scale, n)
     for c in caches:
         c.check()
-    assert caches[0].unit_info(0) == caches[1].unit_info(0)
+    for c in caches[1:]:
+        assert caches[0].unit_info(0) == c.unit_info(0)
 
 
 def test_decode_step_layers_partial_flush_matches_per_layer_calls(mkv):
-    """The fused flush path of mkv_decode_step_layers (one append launch for every layer) with
-    only some layers' units reaching n_r in a step: bit-identical to per-layer calls."""
+    """The fused flush path of the per-layer form (one append launch for every layer, plans built
+    on the device) and the coalesced form's single append, with only some layers' units reaching
+    n_r in a step: bit-identical as in layers_forms."""
     d, n, G, L, layers, n_r = 128, 8, 4, 700, 4, 16
     rng = np.random.default_rng(33)
     budgets = [300, 30, 200, 90]
@@ -220,7 +251,7 @@ def test_decode_step_layers_partial_flush_matches_per_layer_calls(mkv):
     v = torch.from_numpy(rng.standard_normal((layers * n, L, d)).astype(np.float16)).cuda()
     a = torch.from_numpy(rng.random((layers * n, L)).astype(np.float32)).cuda()
     caches = []
-    for _ in range(2):
+    for _ in range(4):
         c = mkv.KVCache(layers * n, caps, max_decode_tokens=96, n_r=n_r)
         for l in range(layers):
             c.prefill(k[l * n:(l + 1) * n], v[l * n:(l + 1) * n], a[l * n:(l + 1) * n], budgets[l], 32,
@@ -236,14 +267,12 @@ def test_decode_step_layers_partial_flush_matches_per_layer_calls(mkv):
         q = torch.from_numpy(rng.standard_normal((layers, n, G, d)).astype(np.float16)).cuda()
         tk = torch.from_numpy(rng.standard_normal((layers, n, d)).astype(np.float16)).cuda()
         tv = torch.from_numpy(rng.standard_normal((layers, n, d)).astype(np.float16)).cuda()
-        fused = caches[0].decode_step_layers(q, tk, tv, scale)
-        ref = torch.stack([caches[1].decode_step(q[l], tk[l], tv[l], scale, unit_begin=l * n)
-                           for l in range(layers)])
-        assert torch.equal(fused, ref), f"step {s}: max diff {(fused.float() - ref.float()).abs().max()}"
+        layers_forms(caches, q, tk, tv, scale, n)
     for c in caches:
         c.check()
     for u in range(0, layers * n, n):
-        assert caches[0].unit_info(u) == caches[1].unit_info(u)
+        for c in caches[1:]:
+            assert caches[0].unit_info(u) == c.unit_info(u)
 
 
 def test_decode_step_layers_overlapping_ranges_match_per_layer_calls(mkv):
@@ -335,8 +364,8 @@ def test_decode_headline_shape_parity(mkv):
     assert worst <= TOL, worst
 
 
-@pytest.mark.parametrize("env", [{"MKV_PAGES_IMPL": "tc"}, {"MKV_FLUSH": "fused"}],
-                         ids=["tcgen05-page-pass", "fused-flush"])
+@pytest.mark.parametrize("env", [{"MKV_PAGES_IMPL": "tc"}, {"MKV_FLUSH": "fused"}, {"MKV_LAYERS_SPLIT": "1"}],
+                         ids=["tcgen05-page-pass", "fused-flush", "layers-split"])
 def test_decode_variant_parity(env):
     """The decode variants kept as measured A/Bs pass the same oracle parity tests (G = 1 / 4 / 8,
     flushes, partial pages, split units, the headline shape, bit-identity of the multi-layer

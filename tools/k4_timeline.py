@@ -112,3 +112,41 @@ for name, (p, f) in zip(("layer n-2", "layer n-1"), lays):
         print("  finish resid done", pct(f[:, 1], t0))
         print("  finish wait rel. ", pct(f[:, 2], t0))
         print("  finish end       ", pct(f[:, 3], t0))
+
+# ---- serving: one mkv_decode_step per layer, layer l+1's q = layer l's output ----
+outs = torch.empty_like(q)
+for _ in range(2):
+    for l in range(NL):
+        qp = q[0].data_ptr() if l == 0 else outs[l - 1].data_ptr()
+        a = _capi.DecodeArgs(l * upl, upl, G, qp, None, None, outs[l].data_ptr(), scale)
+        _capi.check(_capi.lib().mkv_decode_step(cache.h, C.byref(a), sp), "serve")
+    torch.cuda.synchronize()
+e0.record()
+for l in range(NL):
+    qp = q[0].data_ptr() if l == 0 else outs[l - 1].data_ptr()
+    a = _capi.DecodeArgs(l * upl, upl, G, qp, None, None, outs[l].data_ptr(), scale)
+    _capi.check(_capi.lib().mkv_decode_step(cache.h, C.byref(a), sp), "serve")
+e1.record()
+torch.cuda.synchronize()
+print(f"serving: {NL} dependent layers in {e0.elapsed_time(e1) * 1e3:.1f} us by events "
+      f"({e0.elapsed_time(e1) * 1e3 / NL:.1f} us per layer)")
+slots = read_slots()
+lays = []
+for t in slots:
+    p = t[:PAGE_WORDS].reshape(-1, 4)[:sms * 8]
+    p = p[p[:, 2] > 0]
+    f = t[PAGE_WORDS:].reshape(-1, 4)
+    f = f[f[:, 0] > 0]
+    lays.append((p, f))
+lays.sort(key=lambda x: x[0][:, 0].min())
+t0 = lays[0][0][:, 0].min()
+for name, (p, f) in zip(("layer n-2", "layer n-1"), lays):
+    print(f"{name}: {len(p)} page warps, {len(f)} finish CTAs [us from layer n-2's first warp]")
+    print("  pages start      ", pct(p[:, 0], t0))
+    print("  pages after wait ", pct(p[:, 1], t0))
+    print("  pages done       ", pct(p[:, 2], t0))
+    if len(f):
+        print("  finish start     ", pct(f[:, 0], t0))
+        print("  finish resid done", pct(f[:, 1], t0))
+        print("  finish wait rel. ", pct(f[:, 2], t0))
+        print("  finish end       ", pct(f[:, 3], t0))
