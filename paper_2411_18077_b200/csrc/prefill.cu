@@ -26,6 +26,8 @@
 #include <stdio.h>
 #include <stdlib.h>
 
+#include <type_traits>
+
 #include "mkv_kernels.h"
 #include "mkv_sm100.cuh"
 
@@ -50,6 +52,12 @@ __host__ __device__ constexpr bool poly_slot(int c) {
     return kPoly <= 0 ? false : ((c & 7) * kPoly) % 8 + kPoly >= 8;
 }
 
+// pair p of every 4 exponential PAIRS runs on the FMA pipe when it is one of kPoly spread slots
+template <int kPoly>
+__host__ __device__ constexpr bool poly_pair(int p) {
+    return kPoly <= 0 ? false : ((p & 3) * kPoly) % 4 + kPoly >= 4;
+}
+
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
     return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
 }
@@ -70,6 +78,30 @@ __device__ __forceinline__ float exp2_fma(float x) {
     p = fmaf(p, f, 0.6931471806f);
     p = fmaf(p, f, 1.0f);
     return __int_as_float(__float_as_int(p) + ((__float_as_int(xr) - 0x4B400000) << 23));
+}
+
+// Two exp2's on the FMA pipe with packed fp32 (FADD2 / FFMA2: one issue slot per PAIR).
+// Same split and polynomial as exp2_fma.  2^j goes into the exponent with one shift-add
+// per element: bits(xr) = 0x4B400000 + j and (0x4B400000 << 23) == 0 mod 2^32, so
+// bits(2^j * p) = bits(p) + (bits(xr) << 23).
+__device__ __forceinline__ float2 exp2_fma2(float2 x) {
+    x.x = fmaxf(x.x, -127.0f);  // ALU pipe
+    x.y = fmaxf(x.y, -127.0f);
+    const float2 xr = __fadd2_rn(x, make_float2(12582912.0f, 12582912.0f));
+    const float2 t = __fadd2_rn(xr, make_float2(-12582912.0f, -12582912.0f));
+    const float2 f = __ffma2_rn(t, make_float2(-1.0f, -1.0f), x);  // x - t, exact
+    float2 p = __ffma2_rn(make_float2(0.0096181291f, 0.0096181291f), f, make_float2(0.0555041087f, 0.0555041087f));
+    p = __ffma2_rn(p, f, make_float2(0.2402265070f, 0.2402265070f));
+    p = __ffma2_rn(p, f, make_float2(0.6931471806f, 0.6931471806f));
+    p = __ffma2_rn(p, f, make_float2(1.0f, 1.0f));
+    return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(xr.x) << 23)),
+                       __int_as_float(__float_as_int(p.y) + (__float_as_int(xr.y) << 23)));
+}
+
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];\n" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
 }
 
 // ---------------------------------------------------------------------------
@@ -102,8 +134,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int n_qt = (P.lq + kTile - 1) / kTile;
     const int n_pairs = (n_qt + 1) / 2;
-    const int pair = n_pairs - 1 - blockIdx.x;  // longest causal rows first
-    const int hq = blockIdx.y, b = blockIdx.z;
+    // grid (hq * batch, n_pairs): every head's longest causal pair is scheduled before any
+    // head's next one (longest-processing-time-first across the whole grid)
+    const int pair = n_pairs - 1 - blockIdx.y;
+    const int hq = blockIdx.x % P.hq, b = blockIdx.x / P.hq;
     const int G = P.hq / P.hkv;
     const int hk = hq / G;
     const int offset = P.causal ? P.lk - P.lq : 0;
@@ -323,19 +357,33 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 // ---------------------------------------------------------------------------
 // pass 2: column-parallel A_cumul
 // ---------------------------------------------------------------------------
-constexpr int kQStages = 3;
-constexpr int kAcThreads = 320;  // warps 0-7: two exp warpgroups (even / odd items), 8: TMA, 9: MMA
+constexpr int kQStages = 4;
+constexpr int kAcWG = 3;                           // exp warpgroups: item it goes to warpgroup it % kAcWG
+constexpr int kAcThreads = kAcWG * 128 + 64;       // + TMA warp + MMA warp
+constexpr int kAcTma = kAcWG * 4, kAcMma = kAcWG * 4 + 1;
 struct AcBars {
-    uint64_t k_full, q_full[kQStages], q_empty[kQStages], s_full[2], s_free[2];
+    uint64_t k_full, q_full[kQStages], q_empty[kQStages], s_full[kAcWG], s_free[kAcWG];
     uint32_t tmem;
-    float lse2[2][2][kTile];  // [warpgroup][item parity][query]
-    float acc1[kTile];        // warpgroup 1 partial sums
+    alignas(16) float lse2[kAcWG][2][kTile];  // [warpgroup][item parity][query], -lse*log2e (ld.shared.v4)
+    float part[kAcWG - 1][kTile];             // partial sums of warpgroups 1..
 };
 constexpr int kAcSmem = (1 + kQStages) * kTileB + 1024 + (int)sizeof(AcBars) + 64;
 
-// kPoly of every 8 exponentials run as a polynomial on the FMA pipe (the rest on MUFU):
-// per element the pass costs 1 exp + ~2 FMA-pipe ops, so splitting the exponentials
-// balances the two pipes.
+// item -> (q-head g of the kv-head, query tile t); items run g-major from the block's first
+// visible query tile.  Advanced incrementally (no integer division per item).
+struct ItemPos {
+    int g, t;
+    __device__ __forceinline__ void advance(int by, int t_first, int n_qt) {
+        t += by;
+        while (t >= n_qt) {
+            t -= n_qt - t_first;
+            ++g;
+        }
+    }
+};
+
+// kPoly of every 4 exponential PAIRS run as a polynomial on the FMA pipe (FFMA2, the rest
+// on MUFU.EX2).  Per element the pass costs 1 exponential + half an FFMA2 + half an FADD2.
 template <int kPoly>
 __global__ void __launch_bounds__(kAcThreads, 1)
     acumul_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
@@ -347,7 +395,9 @@ __global__ void __launch_bounds__(kAcThreads, 1)
     AcBars& B = *reinterpret_cast<AcBars*>(sm + (1 + kQStages) * kTileB);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int kt = blockIdx.x, hk = blockIdx.y, b = blockIdx.z;
+    // grid (hkv * batch, n_kt): key block 0 (seen by every query) of every head first -- the
+    // causal work per CTA falls with kt, so this is longest-processing-time-first
+    const int kt = blockIdx.y, hk = blockIdx.x % P.hkv, b = blockIdx.x / P.hkv;
     const int G = P.hq / P.hkv;
     const int key0 = kt * kTile;
     const int offset = P.causal ? P.lk - P.lq : 0;
@@ -357,17 +407,17 @@ __global__ void __launch_bounds__(kAcThreads, 1)
     const int per_head = n_qt - t_first;
     const int n_items = G * per_head;
 
-    if (warp == 9) {
-        tmem_alloc(&B.tmem, 256);
+    if (warp == kAcMma) {
+        tmem_alloc(&B.tmem, 512);
         tmem_relinquish();
     }
-    if (tid == 256) {
+    if (tid == kAcTma * 32) {
         mbar_init(&B.k_full, 1);
         for (int s = 0; s < kQStages; ++s) {
             mbar_init(&B.q_full[s], 1);
             mbar_init(&B.q_empty[s], 1);
         }
-        for (int s = 0; s < 2; ++s) {
+        for (int s = 0; s < kAcWG; ++s) {
             mbar_init(&B.s_full[s], 1);
             mbar_init(&B.s_free[s], 128);
         }
@@ -380,28 +430,30 @@ __global__ void __launch_bounds__(kAcThreads, 1)
     tc_fence_after();
     const uint32_t tmem = B.tmem;
 
-    if (warp == 8) {
+    if (warp == kAcTma) {
         if (lane == 0) {
             mbar_expect_tx(&B.k_full, kTileB);
             tma_load_4d(sK, &tk, 0, key0, hk, b, &B.k_full);
             tma_load_4d(sK + kHalf, &tk, 64, key0, hk, b, &B.k_full);
-            for (int it = 0; it < n_items; ++it) {
+            ItemPos pos{0, t_first};
+            for (int it = 0; it < n_items; ++it, pos.advance(1, t_first, n_qt)) {
                 const int s = it % kQStages;
                 if (it >= kQStages) mbar_wait(&B.q_empty[s], ((it / kQStages) - 1) & 1);
-                const int g = it / per_head, t = t_first + it % per_head;
-                const int hq = hk * G + g;
+                const int hq = hk * G + pos.g;
                 mbar_expect_tx(&B.q_full[s], kTileB);
-                tma_load_4d(sQ + s * kTileB, &tq, 0, t * kTile, hq, b, &B.q_full[s]);
-                tma_load_4d(sQ + s * kTileB + kHalf, &tq, 64, t * kTile, hq, b, &B.q_full[s]);
+                tma_load_4d(sQ + s * kTileB, &tq, 0, pos.t * kTile, hq, b, &B.q_full[s]);
+                tma_load_4d(sQ + s * kTileB + kHalf, &tq, 64, pos.t * kTile, hq, b, &B.q_full[s]);
             }
         }
-    } else if (warp == 9) {
+    } else if (warp == kAcMma) {
         if (lane == 0) {
             mbar_wait(&B.k_full, 0);
             for (int it = 0; it < n_items; ++it) {
-                const int s = it % kQStages, bb = it & 1;
+                // S^T(item) = K_blk Q_t^T into the TMEM buffer of warpgroup it % kAcWG.  (Split
+                // into two N = 64 halves with their own barriers it measured 1.46x slower.)
+                const int s = it % kQStages, bb = it % kAcWG;
                 mbar_wait(&B.q_full[s], (it / kQStages) & 1);
-                if (it >= 2) mbar_wait(&B.s_free[bb], ((it >> 1) - 1) & 1);
+                if (it >= kAcWG) mbar_wait(&B.s_free[bb], ((it / kAcWG) - 1) & 1);
                 tc_fence_after();
                 const uint8_t* q = sQ + s * kTileB;
 #pragma unroll
@@ -412,73 +464,105 @@ __global__ void __launch_bounds__(kAcThreads, 1)
             }
         }
     } else {
-        // warpgroup wg handles items it = wg, wg + 2, ...; thread = key row; each warpgroup
-        // accumulates in a fixed order and the two partial sums are added in a fixed order.
+        // warpgroup wg handles items it = wg, wg + kAcWG, ...; thread = key row; each
+        // warpgroup accumulates in a fixed order and the partial sums are added in a fixed order.
         const int wg = warp >> 2;
         const int kr = tid & 127;
         const int kj = key0 + kr;
         const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16) + 128 * wg;
         const float sl2 = P.scale * kLog2e;
-        float acc = 0.0f;
-        // the LSE of the query row this thread stages is loaded one item ahead (its global
-        // latency then hides behind the previous item's exponentials)
-        auto load_lse = [&](int item) -> float {
-            if (item >= n_items) return INFINITY;
-            const int g = item / per_head, t = t_first + item % per_head;
-            const int i = t * kTile + kr;
-            return (i < P.lq) ? __ldg(P.lse + ((size_t)b * P.hq + hk * G + g) * P.lq + i) * kLog2e : INFINITY;
+        // the LSE of the query row this thread stages is loaded one item ahead: its global
+        // latency hides behind the current item's exponentials (consumed only at the next one)
+        const float* lse_b = P.lse + ((size_t)b * P.hq + hk * G) * P.lq;
+        auto load_lse = [&](int item, const ItemPos& ps) -> float {
+            const int i = ps.t * kTile + kr;
+            return (item < n_items && i < P.lq) ? __ldg(lse_b + (size_t)ps.g * P.lq + i) : INFINITY;
         };
-        float lse_next = load_lse(wg);
-        for (int it = wg; it < n_items; it += 2) {
-            const int t = t_first + it % per_head;
-            const int k = it >> 1;  // use count of this TMEM buffer
+        // packed fp32: one FFMA2 per 2 scores (s * scale*log2e - lse*log2e), one FADD2 per 2
+        // exponentials into four pair accumulators
+        const float2 s2 = make_float2(sl2, sl2);
+        float2 a0 = make_float2(0.0f, 0.0f), a1 = a0, a2 = a0, a3 = a0;
+        ItemPos pos{0, t_first};
+        pos.advance(wg, t_first, n_qt);
+        ItemPos nxt = pos;
+        nxt.advance(kAcWG, t_first, n_qt);
+        float lse_next = load_lse(wg, pos);
+        for (int it = wg, k = 0; it < n_items; it += kAcWG, ++k) {
             float* l2 = B.lse2[wg][k & 1];
-            l2[kr] = lse_next;
+            l2[kr] = lse_next * -kLog2e;  // INFINITY -> -inf: masked rows add exact zeros
             named_bar_sync(1 + wg, 128);
-            lse_next = load_lse(it + 2);
+            lse_next = load_lse(it + kAcWG, nxt);
+            const int t = pos.t;
+            pos = nxt;
+            nxt.advance(kAcWG, t_first, n_qt);
+            const uint32_t l2a = smem_u32(l2);
             mbar_wait(&B.s_full[wg], k & 1);
             tc_fence_after();
             // query i = t*128 + c visible iff kj <= offset + i  <=>  c >= kj - offset - t*128
             const int c_min = P.causal ? (kj - offset - t * kTile) : -1;
             const bool full = __all_sync(0xffffffffu, c_min <= 0);
-            float part = 0.0f;
+            // the two loops differ only in the causal mask (diagonal items): separate copies keep
+            // the full-tile loop free of per-column compares
+            auto tile = [&](auto masked) {
 #pragma unroll
-            for (int half = 0; half < 2; ++half) {
-                uint32_t x[64];
-                tmem_ld32(trow + 64 * half, *reinterpret_cast<uint32_t(*)[32]>(x));
-                tmem_ld32(trow + 64 * half + 32, *reinterpret_cast<uint32_t(*)[32]>(x + 32));
-                tmem_wait_ld();
-                if (half == 1) {
-                    tc_fence_before();
-                    mbar_arrive(&B.s_free[wg]);  // TMEM buffer free for the next MMA
-                }
-                if (full) {
-#pragma unroll
-                    for (int c = 0; c < 64; ++c) {
-                        const float v = fmaf(__uint_as_float(x[c]), sl2, -l2[64 * half + c]);
-                        part += poly_slot<kPoly>(c) ? exp2_fma(v) : fast_exp2(v);
+                for (int half = 0; half < 2; ++half) {
+                    uint32_t x[64];
+                    tmem_ld32(trow + 64 * half, *reinterpret_cast<uint32_t(*)[32]>(x));
+                    tmem_ld32(trow + 64 * half + 32, *reinterpret_cast<uint32_t(*)[32]>(x + 32));
+                    tmem_wait_ld();
+                    if (half == 1) {
+                        tc_fence_before();
+                        mbar_arrive(&B.s_free[wg]);  // TMEM buffer free for the next MMA into it
                     }
-                } else {
 #pragma unroll
-                    for (int c = 0; c < 64; ++c) {
-                        const int col = 64 * half + c;
-                        const float v = fmaf(__uint_as_float(x[c]), sl2, -l2[col]);
-                        const float e = poly_slot<kPoly>(c) ? exp2_fma(v) : fast_exp2(v);
-                        part += (col >= c_min) ? e : 0.0f;
+                    for (int c = 0; c < 64; c += 4) {
+                        const float4 nl = lds128(l2a + (64 * half + c) * 4);
+                        const float2 v0 = __ffma2_rn(make_float2(__uint_as_float(x[c]), __uint_as_float(x[c + 1])),
+                                                     s2, make_float2(nl.x, nl.y));
+                        const float2 v1 = __ffma2_rn(
+                            make_float2(__uint_as_float(x[c + 2]), __uint_as_float(x[c + 3])), s2,
+                            make_float2(nl.z, nl.w));
+                        float2 e0 = poly_pair<kPoly>(c >> 1) ? exp2_fma2(v0)
+                                                              : make_float2(fast_exp2(v0.x), fast_exp2(v0.y));
+                        float2 e1 = poly_pair<kPoly>((c >> 1) + 1) ? exp2_fma2(v1)
+                                                                    : make_float2(fast_exp2(v1.x), fast_exp2(v1.y));
+                        if constexpr (decltype(masked)::value) {
+                            const int col = 64 * half + c;
+                            e0.x = col >= c_min ? e0.x : 0.0f;
+                            e0.y = col + 1 >= c_min ? e0.y : 0.0f;
+                            e1.x = col + 2 >= c_min ? e1.x : 0.0f;
+                            e1.y = col + 3 >= c_min ? e1.y : 0.0f;
+                        }
+                        if ((c & 4) == 0) {
+                            a0 = __fadd2_rn(a0, e0);
+                            a1 = __fadd2_rn(a1, e1);
+                        } else {
+                            a2 = __fadd2_rn(a2, e0);
+                            a3 = __fadd2_rn(a3, e1);
+                        }
                     }
                 }
-            }
-            acc += part;
+            };
+            if (full)
+                tile(std::false_type{});
+            else
+                tile(std::true_type{});
         }
-        if (wg == 1) B.acc1[kr] = acc;
-        named_bar_sync(3, 256);
-        if (wg == 0 && kj < P.lk) P.a_cumul[((size_t)b * P.hkv + hk) * P.lk + kj] = acc + B.acc1[kr];
+        const float acc = ((a0.x + a1.x) + (a0.y + a1.y)) + ((a2.x + a3.x) + (a2.y + a3.y));
+        if (wg > 0) B.part[wg - 1][kr] = acc;
+        named_bar_sync(1 + kAcWG, kAcWG * 128);
+        if (wg == 0 && kj < P.lk) {
+            float sum = acc;
+#pragma unroll
+            for (int w = 1; w < kAcWG; ++w) sum += B.part[w - 1][kr];
+            P.a_cumul[((size_t)b * P.hkv + hk) * P.lk + kj] = sum;
+        }
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 9) {
+    if (warp == kAcMma) {
         tc_fence_after();
-        tmem_dealloc(tmem, 256);
+        tmem_dealloc(tmem, 512);
     }
 }
 
@@ -524,10 +608,10 @@ static cudaError_t launch_prefill_t(const CUtensorMap& tq, const CUtensorMap& tk
         configured = true;
     }
     const int n_qt = (p.lq + kTile - 1) / kTile, n_kt = (p.lk + kTile - 1) / kTile;
-    attn_fwd_kernel<KF><<<dim3((n_qt + 1) / 2, p.hq, p.batch), kFwdThreads, kFwdSmem, s>>>(tq, tk, tv, p);
+    attn_fwd_kernel<KF><<<dim3(p.hq * p.batch, (n_qt + 1) / 2), kFwdThreads, kFwdSmem, s>>>(tq, tk, tv, p);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    acumul_kernel<KA><<<dim3(n_kt, p.hkv, p.batch), kAcThreads, kAcSmem, s>>>(tq, tk, p);
+    acumul_kernel<KA><<<dim3(p.hkv * p.batch, n_kt), kAcThreads, kAcSmem, s>>>(tq, tk, p);
     return cudaGetLastError();
 }
 
@@ -537,20 +621,18 @@ cudaError_t launch_prefill_attn(const PrefillAttnParams& p, cudaStream_t s) {
         !make_map(&tk, p.k, p.k_sb, p.k_sh, p.k_st, p.lk, p.hkv, p.batch) ||
         !make_map(&tv, p.v, p.v_sb, p.v_sh, p.v_st, p.lk, p.hkv, p.batch))
         return cudaErrorInvalidValue;
-    // exponentials per 8 on the FMA pipe (fwd, A_cumul); MKV_PREFILL_POLY="f,a" selects a variant
-    static int kf = 1, ka = 2;
+    // exponentials on the FMA pipe: fwd per 8, A_cumul pairs per 4; MKV_PREFILL_POLY="f,a"
+    static int kf = 1, ka = 1;
     static bool parsed = false;
     if (!parsed) {
         if (const char* e = getenv("MKV_PREFILL_POLY")) sscanf(e, "%d,%d", &kf, &ka);
         parsed = true;
     }
+    if (kf == 1 && ka == 0) return launch_prefill_t<1, 0>(tq, tk, tv, p, s);
     if (kf == 1 && ka == 2) return launch_prefill_t<1, 2>(tq, tk, tv, p, s);
-    if (kf == 1 && ka == 3) return launch_prefill_t<1, 3>(tq, tk, tv, p, s);
-    if (kf == 1 && ka == 4) return launch_prefill_t<1, 4>(tq, tk, tv, p, s);
-    if (kf == 2 && ka == 3) return launch_prefill_t<2, 3>(tq, tk, tv, p, s);
-    if (kf == 2 && ka == 2) return launch_prefill_t<2, 2>(tq, tk, tv, p, s);
-    if (kf == 0 && ka == 2) return launch_prefill_t<0, 2>(tq, tk, tv, p, s);
-    return launch_prefill_t<1, 2>(tq, tk, tv, p, s);
+    if (kf == 0 && ka == 1) return launch_prefill_t<0, 1>(tq, tk, tv, p, s);
+    if (kf == 2 && ka == 1) return launch_prefill_t<2, 1>(tq, tk, tv, p, s);
+    return launch_prefill_t<1, 1>(tq, tk, tv, p, s);
 }
 
 }  // namespace mkv

@@ -13,9 +13,9 @@ SHORT="--steps 2 --warmup 3 --no-prefill --no-cpu-baseline --no-config0 --no-ser
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file "$out/launches.csv" \
     python bench.py $SHORT > /dev/null 2>&1
 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
-    -k regex:pages_kernel -s 3 -c 4 --csv --log-file "$out/pages_traffic.csv" \
+    -k regex:'^pages_kernel' -s 3 -c 4 --csv --log-file "$out/pages_traffic.csv" \
     python bench.py $SHORT > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:pages_kernel -s 4 -c 1 -o "$out/prof_pages" -f \
+ncu --set full --clock-control none --import-source on -k regex:'^pages_kernel' -s 4 -c 1 -o "$out/prof_pages" -f \
     python bench.py $SHORT > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:finish_kernel -s 4 -c 1 -o "$out/prof_finish" -f \
     python bench.py $SHORT > /dev/null 2>&1
