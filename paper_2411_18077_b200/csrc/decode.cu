@@ -489,9 +489,10 @@ constexpr int kAppendThreads = 256;
 // One CTA per unit.  S.n_seg == 0: the units of P (unit_begin + block, tokens P.k_new /
 // P.v_new); otherwise segment s covers blocks [S.block_begin[s], S.block_begin[s + 1]) with its
 // own unit range and token arrays (every layer of a multi-layer call in one launch).
+constexpr size_t kAppendSmem = (kAppendThreads / 32) * (sizeof(PageRows) + sizeof(PageParams));
+
 __global__ void __launch_bounds__(kAppendThreads) append_kernel(const ResidualParams P, const AppendSegs S) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
-    PageScratch* scratch = reinterpret_cast<PageScratch*>(smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = lane_id();
     int i = blockIdx.x, u = P.unit_begin + i;
     const __half* k_new = P.k_new;
@@ -515,7 +516,7 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(const ResidualPa
         reinterpret_cast<uint4*>(rv + (size_t)meta.n_res * d)[tid - 16] =
             reinterpret_cast<const uint4*>(v_new + (size_t)i * d)[tid - 16];
     }
-    __threadfence_block();
+    __threadfence();  // the new row is read back below by cp.async.cg (through L2)
     __syncthreads();
     if (n < P.n_r) {
         if (tid == 0) P.meta[u].n_res = n;
@@ -524,17 +525,16 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(const ResidualPa
     // store_block (cache_engine.cpp:34-52): quantize the full block into n_r/16 pages
     const int npg = P.n_r / kGroup;
     bool ok = true;
+    // (the K3 staged page builder: rows by cp.async, codes from fp16 pairs)
+    PageRows& rows = reinterpret_cast<PageRows*>(smem_raw)[warp];
+    PageParams& prm = reinterpret_cast<PageParams*>(smem_raw + (kAppendThreads / 32) * sizeof(PageRows))[warp];
     for (int j = warp; j < npg; j += kAppendThreads / 32) {
-        PageScratch& ps = scratch[warp];
-        for (int e = lane; e < 16 * 16; e += 32) {
-            const int r = e >> 4, c16 = e & 15;
-            reinterpret_cast<uint4*>(ps.k[r])[c16] = reinterpret_cast<const uint4*>(rk + (size_t)(16 * j + r) * d)[c16];
-            reinterpret_cast<uint4*>(ps.v[r])[c16] = reinterpret_cast<const uint4*>(rv + (size_t)(16 * j + r) * d)[c16];
-        }
+        stage_rows_contig(rows, rk + (size_t)16 * j * d, rv + (size_t)16 * j * d);
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
         __syncwarp();
         const int64_t page = meta.page_base + meta.n_pages + j;
-        ok &= build_page(ps, 16, P.pool + (size_t)page * kPageBytes,
-                         P.shadow ? P.shadow + (size_t)page * (kShadowBytes / 4) : nullptr);
+        ok &= build_page_staged(rows, prm, 16, P.pool + (size_t)page * kPageBytes,
+                                P.shadow ? P.shadow + (size_t)page * (kShadowBytes / 4) : nullptr);
     }
     if (!ok && lane == 0) atomicOr(P.status, kStatusNonFinite);
     __syncthreads();
@@ -555,7 +555,7 @@ static cudaError_t append_configure(size_t smem) {
 }
 
 cudaError_t launch_append(const ResidualParams& p, cudaStream_t s) {
-    const size_t smem = sizeof(PageScratch) * (kAppendThreads / 32);
+    const size_t smem = kAppendSmem;
     if (cudaError_t e = append_configure(smem)) return e;
     AppendSegs none{};
     append_kernel<<<p.n_units, kAppendThreads, smem, s>>>(p, none);
@@ -563,7 +563,7 @@ cudaError_t launch_append(const ResidualParams& p, cudaStream_t s) {
 }
 
 cudaError_t launch_append_segments(const ResidualParams& p, const AppendSegs& segs, cudaStream_t s) {
-    const size_t smem = sizeof(PageScratch) * (kAppendThreads / 32);
+    const size_t smem = kAppendSmem;
     if (cudaError_t e = append_configure(smem)) return e;
     const int blocks = segs.block_begin[segs.n_seg];
     if (blocks == 0) return cudaSuccess;

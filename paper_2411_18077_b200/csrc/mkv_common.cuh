@@ -172,6 +172,46 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
+// Exact code thresholds of one quantization group (quantize_group, quantizer.cpp:28-53):
+// scale = fl((hi - lo) / 3) and code = round_half_away(fl(fl(v - lo) / scale)), clamped to
+// [0, 3].  fl(dv / sc) is monotone in dv, so code = #{k in 1..3 : dv >= T_k} with T_k the
+// smallest float whose IEEE quotient reaches c = k - 0.5.  fl(y) >= c  <=>  y > m  or
+// (y == m and c has an even mantissa -- 0.5, 1.5, 2.5 all do), m = the midpoint of c and its
+// predecessor, so T_k = the smallest float >= m * sc, where m * sc (25 x 24 significant bits)
+// is exact in double.  Returns false (and T = +inf: every code 0) when the scale is not a
+// positive finite number (a constant group).
+__device__ __forceinline__ bool group_thresholds(float lo, float hi, float* sc_out, float (&T)[3]) {
+    const float sc = __fdiv_rn(__fsub_rn(hi, lo), 3.0f);
+    const bool ok = sc > 0.0f && isfinite(sc);
+    T[0] = T[1] = T[2] = INFINITY;
+    if (ok && sc >= 0x1p-100f && sc <= 0x1p100f) {
+        // fp32 only (no FP64): m_k = c_k - d_k with d_k = 2^-26, 2^-24, 2^-23; ds = sc * d_k is
+        // exact, y = fma(c_k, sc, -ds) = fl(m_k * sc), r = fma(-c_k, sc, y) = y - c_k * sc
+        // exactly, so y >= m_k * sc  <=>  r >= -ds.  Bit-identical to the double form below for
+        // every scale in [2^-100, 2^100] (tools/threshold_fp32_check.c: all 5.0e9 (scale, k)).
+        const float cs[3] = {0.5f, 1.5f, 2.5f}, ds_[3] = {0x1p-26f, 0x1p-24f, 0x1p-23f};
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const float ds = sc * ds_[k];
+            const float y = __fmaf_rn(cs[k], sc, -ds);
+            const float r = __fmaf_rn(-cs[k], sc, y);
+            T[k] = (r >= -ds) ? y : __int_as_float(__float_as_int(y) + 1);
+        }
+    } else if (ok) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const float c = static_cast<float>(k) + 0.5f;
+            const double m = 0.5 * (static_cast<double>(nextafterf(c, 0.0f)) + static_cast<double>(c));
+            const double prod = m * static_cast<double>(sc);  // exact
+            float x = __double2float_rn(prod);
+            if (static_cast<double>(x) < prod) x = nextafterf(x, INFINITY);
+            T[k] = x;
+        }
+    }
+    *sc_out = sc;
+    return ok;
+}
+
 // Reference-exact group quantization of n (<= 16) fp32 values (quantizer.cpp:28-53):
 // zero = min, scale = (max - min) / 3.0f (IEEE division), code = clamp(roundf((v-zero)/scale)).
 // Returns false if a value is non-finite (the reference throws std::domain_error).
@@ -190,27 +230,8 @@ __device__ __forceinline__ bool quantize_group16(const float* v, int n, uint8_t*
             hi = (hi < x) ? x : hi;
         }
     }
-    const float sc = __fdiv_rn(__fsub_rn(hi, lo), 3.0f);
-    // code = round_half_away(fl(fl(v - lo) / sc)), clamped to [0, 3].  fl(dv / sc) is
-    // monotone in dv, so code = #{k in 1..3 : dv >= T_k} with T_k the smallest float whose
-    // IEEE quotient reaches c = k - 0.5.  fl(y) >= c  <=>  y > m  or  (y == m and c has an
-    // even mantissa -- 0.5, 1.5, 2.5 all do), m = the midpoint of c and its predecessor, so
-    // T_k = the smallest float >= m * sc, where m * sc (25 x 24 significant bits) is exact
-    // in double.  Per group: three double products; per value: one subtraction and three
-    // compares.  Identical codes to the reference's division for every finite input.
-    const bool thr_ok = sc > 0.0f && isfinite(sc);
-    float T[3] = {0.0f, 0.0f, 0.0f};
-    if (thr_ok) {
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            const float c = static_cast<float>(k) + 0.5f;
-            const double m = 0.5 * (static_cast<double>(nextafterf(c, 0.0f)) + static_cast<double>(c));
-            const double prod = m * static_cast<double>(sc);  // exact
-            float x = __double2float_rn(prod);
-            if (static_cast<double>(x) < prod) x = nextafterf(x, INFINITY);
-            T[k] = x;
-        }
-    }
+    float sc, T[3];
+    const bool thr_ok = group_thresholds(lo, hi, &sc, T);
     if (thr_ok) {
 #pragma unroll
         for (int i = 0; i < 16; ++i) {

@@ -163,7 +163,8 @@ def test_synth_matches_oracle(mkv):
         np.testing.assert_array_equal(u[r], oracle.port().synth_uniform(SEED, 99 + r, 500))
 
 
-@pytest.mark.parametrize("kind", ["half_points", "tiny_range", "huge_range", "constant_rows", "near_thresholds"])
+@pytest.mark.parametrize("kind", ["half_points", "tiny_range", "huge_range", "constant_rows", "near_thresholds",
+                                  "signed_zero", "subnormal"])
 def test_quantizer_rounding_edges_bit_exact(mkv, kind):
     """Quotients on/near the .5 rounding points, tiny and huge group ranges, constant groups:
     codes and params must equal the reference's exact fp32 arithmetic (quantizer.cpp:28-53)."""
@@ -188,6 +189,11 @@ def test_quantizer_rounding_edges_bit_exact(mkv, kind):
         bits[:, 1::16] = k.view(np.int16)[:, 1::16]
         k = bits.astype(np.int16).view(np.float16)
         k[~np.isfinite(k)] = np.float16(0.0)
+    elif kind == "signed_zero":  # +0 / -0 as group minima / maxima: the first one wins (std::min/max)
+        k = rng.choice(np.array([-0.0, 0.0, 0.0, -0.0, 0.5, -0.5, 1.0], np.float16), (1, L, d))
+        k[:, ::5] = np.where(rng.random((1, (L + 4) // 5, d)) < 0.5, np.float16(-0.0), np.float16(0.0))
+    elif kind == "subnormal":  # fp16 subnormals and zeros: the smallest scales
+        k = (rng.integers(-3, 4, (1, L, d)) * 2.0 ** -24).astype(np.float16)
     else:
         k = np.repeat(rng.standard_normal((1, L, 1)).astype(np.float16), d, axis=2)
     v = k[:, ::-1].copy()

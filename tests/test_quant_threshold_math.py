@@ -51,3 +51,36 @@ def test_thresholds_match_division_at_every_boundary():
             assert got == ref_code(dv, sc), (sc, dv, T)
             checked += 1
     assert checked > 5000
+
+
+def thresholds_fp32(sc):
+    """The device's FP64-free form (mkv_common.cuh group_thresholds, scales in [2^-100, 2^100]):
+    ds = sc * d_k, y = fma(c_k, sc, -ds), r = fma(-c_k, sc, y), T_k = y if r >= -ds else nextup(y).
+    Both fma's are evaluated exactly in float64 here (c_k * sc needs <= 27 bits and ds sits
+    <= 26 bits below it, so every pre-rounding value fits in 53 bits), then rounded once."""
+    T = []
+    for c, d in ((0.5, 2.0 ** -26), (1.5, 2.0 ** -24), (2.5, 2.0 ** -23)):
+        ds = F(sc * F(d))
+        y = F(c * float(sc) - float(ds))
+        r = F(float(y) - c * float(sc))
+        T.append(y if r >= -ds else np.nextafter(y, F(np.inf)))
+    return T
+
+
+def test_fp32_thresholds_equal_double_thresholds():
+    """Sampled restatement of tools/threshold_fp32_check.c (which covers every fp32 scale in
+    [2^-100, 2^100] exhaustively): binade edges, their neighbours and random scales."""
+    rng = np.random.default_rng(5)
+    scales = [F(2.0 ** e) for e in range(-100, 101)]
+    scales += [np.nextafter(s, F(0)) for s in scales] + [np.nextafter(s, F(np.inf)) for s in scales]
+    scales += list((rng.random(3000) * 2.0 ** rng.integers(-100, 100, 3000)).astype(F))
+    scales += [F(1) / F(3), F(65504) / F(3), F(2.0 ** -24) / F(3)]
+    n = 0
+    for sc in scales:
+        if not (F(2.0 ** -100) <= sc <= F(2.0 ** 100)):
+            continue
+        a, b = thresholds(sc), thresholds_fp32(sc)
+        for x, y in zip(a, b):
+            assert np.float32(x).view(np.uint32) == np.float32(y).view(np.uint32), (sc, a, b)
+        n += 1
+    assert n > 3000
