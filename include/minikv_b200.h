@@ -231,6 +231,25 @@ int mkv_debug_decode_trace(const mkv_cache* cache, uint64_t* out, int max_words)
  * layer l's output calls mkv_decode_step once per layer (bench.py reports both). */
 int mkv_decode_step_layers(mkv_cache* cache, int n_layers, const mkv_decode_args* args,
                            void* stream);
+/* n_steps consecutive decode steps of units [unit_begin, unit_begin + n_units) over a prepared
+ * token stream -- the decode loop of the reference's pipeline / CLI chain
+ * (minikv_cli.cpp:180-201, pipeline.cpp:199-215: decode_step per step, cache_engine.cpp:100-138)
+ * in one FFI crossing.  Step s reads q + s * q_step, k_new + s * kv_step, v_new + s * kv_step
+ * and writes out + s * out_step (strides in fp16 ELEMENTS; k_new / v_new may be null: attend
+ * only).  Bit-identical to n_steps mkv_decode_step calls; every step's inputs must be written
+ * before the call. */
+typedef struct {
+    int unit_begin, n_units, group, n_steps;
+    const void* q;              /* fp16, step s at q + s * q_step: [n_units, G, d] */
+    int64_t q_step;
+    const void* k_new;          /* fp16, step s at k_new + s * kv_step: [n_units, d] (or null) */
+    const void* v_new;
+    int64_t kv_step;
+    void* out;                  /* fp16, step s at out + s * out_step: [n_units, G, d] */
+    int64_t out_step;
+    float scale;
+} mkv_decode_steps_args;
+int mkv_decode_steps(mkv_cache* cache, const mkv_decode_steps_args* args, void* stream);
 
 /* ------------------------------------------------------------------------ */
 /* Reference-format export (synchronous): the unit's QuantizedTensor for     */

@@ -114,6 +114,12 @@ class DecodeArgs(C.Structure):
                 ("q", vp), ("k_new", vp), ("v_new", vp), ("out", vp), ("scale", C.c_float)]
 
 
+class DecodeStepsArgs(C.Structure):
+    _fields_ = [("unit_begin", i32), ("n_units", i32), ("group", i32), ("n_steps", i32),
+                ("q", vp), ("q_step", C.c_int64), ("k_new", vp), ("v_new", vp), ("kv_step", C.c_int64),
+                ("out", vp), ("out_step", C.c_int64), ("scale", C.c_float)]
+
+
 # every symbol the header declares (checked by tests/test_capi_symbols.py)
 EXPORTS = [
     "mkv_last_error", "mkv_abi_version", "mkv_device_check",
@@ -121,7 +127,7 @@ EXPORTS = [
     "mkv_allocate_variance", "mkv_score_variance",
     "mkv_cache_create", "mkv_cache_destroy", "mkv_cache_bytes", "mkv_cache_unit_info",
     "mkv_cache_prefill", "mkv_cache_prefill_select", "mkv_decode_step", "mkv_cache_append",
-    "mkv_decode_step_layers", "mkv_debug_decode_trace", "mkv_decode_pages_only", "mkv_cache_export_sizes", "mkv_cache_export_reference",
+    "mkv_decode_step_layers", "mkv_decode_steps", "mkv_debug_decode_trace", "mkv_decode_pages_only", "mkv_cache_export_sizes", "mkv_cache_export_reference",
     "mkv_cache_export_residual", "mkv_cache_check", "mkv_cache_save_mkvc", "mkv_cache_load_mkvc",
     "mkv_synth_fp16", "mkv_synth_fp16_rows", "mkv_synth_uniform_f32", "mkv_h2o_dynamic_baseline",
     "mkv_attention_f32", "mkv_decode_attention_f32", "mkv_quantize_block_f32", "mkv_dequantize_f32"]
@@ -156,6 +162,7 @@ def lib():
     L.mkv_decode_step.argtypes = [vp, C.POINTER(DecodeArgs), vp]
     L.mkv_decode_pages_only.argtypes = [vp, C.POINTER(DecodeArgs), vp]
     L.mkv_decode_step_layers.argtypes = [vp, i32, C.POINTER(DecodeArgs), vp]
+    L.mkv_decode_steps.argtypes = [vp, C.POINTER(DecodeStepsArgs), vp]
     L.mkv_cache_append.argtypes = [vp, i32, i32, vp, vp, vp]
     L.mkv_cache_export_sizes.argtypes = [vp, i32, i32] + [C.POINTER(C.c_int64)] * 3
     L.mkv_cache_export_reference.argtypes = [vp, i32, i32, vp, vp, vp]

@@ -113,6 +113,8 @@ struct mkv_cache {
     __half* d_res_v = nullptr;
     uint32_t* d_status = nullptr;
     uint64_t* d_trace = nullptr;  // diagnostics only (MKV_DECODE_TRACE)
+    int32_t* d_kept = nullptr;    // prefill selection scratch (grow-only: no allocation per call)
+    size_t kept_cap = 0;
     uint64_t trace_seq = 0;
     int part_slots = 0;  // upper bound of page-partial slots per plan (each plan owns its buffers)
     std::unordered_map<uint64_t, Plan> plans;  // key: (unit_begin, n_units)
@@ -133,6 +135,7 @@ struct mkv_cache {
         cudaFree(d_meta); cudaFree(d_pool); cudaFree(d_shadow); cudaFree(d_res_k); cudaFree(d_res_v);
         cudaFree(d_status);
         cudaFree(d_trace);
+        cudaFree(d_kept);
     }
 
     UnitMeta meta_of(int u) const {
@@ -504,15 +507,21 @@ int mkv_cache_prefill_select(mkv_cache* c, const mkv_prefill_select_args* a, voi
         return fail(MKV_ERR_INVALID_ARGUMENT, "prefill: K/V rows must be 16-byte aligned");
     if (int r = require_device()) return r;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    int32_t* kept = nullptr;
     const int64_t ks = std::max(a->length, 1);
-    CK(cudaMallocAsync(&kept, sizeof(int32_t) * ks * a->n_units, s));
+    const size_t need = (size_t)ks * a->n_units;
+    if (need > c->kept_cap) {  // grow-only scratch (cudaFree synchronizes: earlier users are done)
+        cudaFree(c->d_kept);
+        c->d_kept = nullptr;
+        c->kept_cap = 0;
+        CK(cudaMalloc(&c->d_kept, sizeof(int32_t) * need));
+        c->kept_cap = need;
+    }
+    int32_t* kept = c->d_kept;
     int r = do_select(a->a_cumul, a->a_stride, a->n_units, a->length, a->hh_count, a->rw_count, kept, ks,
                       nullptr, s);
     if (r == MKV_OK)
         r = prefill_pages_impl(c, a->unit_begin, a->n_units, a->k, a->k_su, a->k_st, a->v, a->v_su, a->v_st, kept,
                                ks, n_kept.data(), s);
-    cudaFreeAsync(kept, s);
     return r;
 }
 
@@ -858,6 +867,29 @@ int mkv_debug_decode_trace(const mkv_cache* c, uint64_t* out, int max_words) {
 int mkv_decode_step(mkv_cache* c, const mkv_decode_args* a, void* stream) {
     if (!a) return fail(MKV_ERR_INVALID_ARGUMENT, "decode_step: null args");
     return decode_impl(c, a, true, static_cast<cudaStream_t>(stream));
+}
+
+int mkv_decode_steps(mkv_cache* c, const mkv_decode_steps_args* a, void* stream) {
+    if (!a) return fail(MKV_ERR_INVALID_ARGUMENT, "decode_steps: null args");
+    if (a->n_steps < 0) return fail(MKV_ERR_INVALID_ARGUMENT, "decode_steps: negative step count");
+    if ((a->k_new == nullptr) != (a->v_new == nullptr)) return fail(MKV_ERR_INVALID_ARGUMENT, "decode_append: null v");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    auto at = [](const void* base, int64_t elems) -> const void* {
+        return base ? static_cast<const __half*>(base) + elems : nullptr;
+    };
+    for (int st = 0; st < a->n_steps; ++st) {
+        mkv_decode_args d;
+        d.unit_begin = a->unit_begin;
+        d.n_units = a->n_units;
+        d.group = a->group;
+        d.q = at(a->q, st * a->q_step);
+        d.k_new = at(a->k_new, st * a->kv_step);
+        d.v_new = at(a->v_new, st * a->kv_step);
+        d.out = const_cast<void*>(at(a->out, st * a->out_step));
+        d.scale = a->scale;
+        if (int r = decode_impl(c, &d, true, s)) return r;
+    }
+    return MKV_OK;
 }
 
 int mkv_decode_pages_only(mkv_cache* c, const mkv_decode_args* a, void* stream) {

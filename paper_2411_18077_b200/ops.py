@@ -334,6 +334,27 @@ class KVCache:
         check(lib().mkv_decode_step_layers(self.h, L, args, _stream_ptr(stream)), "decode_step_layers")
         return out
 
+    def decode_steps(self, q: torch.Tensor, k_new: Optional[torch.Tensor], v_new: Optional[torch.Tensor],
+                     scale: float, unit_begin: int = 0, out: Optional[torch.Tensor] = None, stream=None):
+        """S consecutive decode steps over a prepared token stream in one call (mkv_decode_steps):
+        q fp16 [S, n, G, d], k_new / v_new fp16 [S, n, d] (None: attend only); out [S, n, G, d].
+        Bit-identical to S decode_step calls."""
+        S, n, G, d = q.shape
+        if out is None:
+            out = torch.empty_like(q)
+        for t in (q, out) + ((k_new, v_new) if k_new is not None else ()):
+            if not t[0].is_contiguous():
+                raise _capi.InvalidArgument("decode_steps: each step's slice must be contiguous")
+        args = _capi.DecodeStepsArgs(unit_begin, n, G, S, q.data_ptr(), q.stride(0),
+                                     k_new.data_ptr() if k_new is not None else None,
+                                     v_new.data_ptr() if v_new is not None else None,
+                                     k_new.stride(0) if k_new is not None else 0,
+                                     out.data_ptr(), out.stride(0), float(scale))
+        if k_new is not None and v_new.stride(0) != k_new.stride(0):
+            raise _capi.InvalidArgument("decode_steps: k_new / v_new step strides differ")
+        check(lib().mkv_decode_steps(self.h, C.byref(args), _stream_ptr(stream)), "decode_steps")
+        return out
+
     def append(self, k_new: torch.Tensor, v_new: torch.Tensor, unit_begin: int = 0, stream=None):
         """decode_append (cache_engine.cpp:79-90)."""
         check(lib().mkv_cache_append(self.h, unit_begin, k_new.shape[0], k_new.data_ptr(), v_new.data_ptr(),

@@ -419,3 +419,32 @@ def test_decode_256k_mha_units_parity(mkv):
                 worst = max(worst, max_abs(out[u, 0], ocs[u].attend(f32(qh[u, 0]), scale, param_fp16=True)))
     cache.check()
     assert worst <= TOL, worst
+
+
+@pytest.mark.parametrize("append", [True, False])
+def test_decode_steps_matches_per_step_calls(mkv, append):
+    """mkv_decode_steps (one FFI crossing for a prepared token stream, the reference's decode loop
+    minikv_cli.cpp:180-201) equals the same steps as mkv_decode_step calls bit for bit, across two
+    residual flushes (n_r = 32) and on a strided output."""
+    d, G, n, L, hh, rw, S, n_r = 128, 4, 3, 700, 60, 50, 70, 32
+    scale = 1.0 / np.sqrt(d)
+    k = torch.from_numpy(np.stack([synth_np(SEED, oracle.stream_id(oracle.KIND_K, u), (L, d)) for u in range(n)])).cuda()
+    v = torch.from_numpy(np.stack([synth_np(SEED, oracle.stream_id(oracle.KIND_V, u), (L, d)) for u in range(n)])).cuda()
+    a = torch.rand((n, L), generator=torch.Generator().manual_seed(3)).cuda()
+    q = mkv.synth_fp16((S, n, G, d), SEED, 11 << 48, 1 << 16)
+    tk = mkv.synth_fp16((S, n, d), SEED, 12 << 48, 1 << 16)
+    tv = mkv.synth_fp16((S, n, d), SEED, 13 << 48, 1 << 16)
+    caches = [mkv.KVCache(n, hh + rw, max_decode_tokens=S + n_r, n_r=n_r) for _ in range(2)]
+    for c in caches:
+        c.prefill(k, v, a, hh, rw)
+    ref = torch.empty((S, n, G, d), dtype=torch.float16, device="cuda")
+    for s in range(S):
+        caches[0].decode_step(q[s], tk[s] if append else None, tv[s] if append else None, scale, out=ref[s])
+    big = torch.zeros((S, 2, n, G, d), dtype=torch.float16, device="cuda")
+    got = big[:, 1]  # step stride 2 n G d: exercises out_step != n G d
+    caches[1].decode_steps(q, tk if append else None, tv if append else None, scale, out=got)
+    torch.cuda.synchronize()
+    assert torch.equal(got, ref)
+    for c in caches:
+        c.check()
+        c.close()
