@@ -258,6 +258,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         for (int j = 0; j < n; ++j) {
             mbar_wait(&B.s_full[h], j & 1);  // also implies PV_h(j-1) completed (commit order)
             tc_fence_after();
+#ifdef MKV_AB_MMA_ONLY  // A/B probe (tools/abbuild_prefill.sh): the MMA / TMA pipeline without the softmax
+            tc_fence_before();
+            mbar_arrive(&B.p_full[h]);
+            continue;
+#endif
             // one TMEM read of the 128 scores; P is packed in place over x (x[c/2] <- c, c+1)
             uint32_t x[128];
             tmem_ld32(trow + 0, *reinterpret_cast<uint32_t(*)[32]>(x + 0));

@@ -38,9 +38,9 @@ for L in Ls:
     t = {}
     for e in prof.events():
         if e.device_type == torch.autograd.DeviceType.CUDA:
-            for name in ("attn_fwd_kernel", "acumul_kernel"):
+            for name, key in (("attn_fwd", "attn_fwd_kernel"), ("acumul_kernel", "acumul_kernel")):
                 if name in e.name:
-                    t.setdefault(name, []).append(e.device_time_total / 1e3)  # us -> ms
+                    t.setdefault(key, []).append(e.device_time_total / 1e3)  # us -> ms
     P = L * (L + 1) / 2
     f1, f2 = Hq * 4 * d * P, Hq * 2 * d * P
     a, b = min(t["attn_fwd_kernel"]), min(t["acumul_kernel"])
