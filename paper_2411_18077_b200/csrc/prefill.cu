@@ -366,8 +366,14 @@ constexpr int kQStages = 4;
 constexpr int kAcWG = 3;                           // exp warpgroups: item it goes to warpgroup it % kAcWG
 constexpr int kAcThreads = kAcWG * 128 + 64;       // + TMA warp + MMA warp
 constexpr int kAcTma = kAcWG * 4, kAcMma = kAcWG * 4 + 1;
+// The key block is the A operand of every S^T MMA of the CTA: it is copied once into TMEM
+// (columns kAcKCol .. + 63, fp16 pairs, lane = key row) so the MMAs read only the Q tile from
+// shared memory -- an SS MMA at M = N = 128 reads 8 KB of shared memory per 64-clk K step, the
+// whole 128 B/clk, a TS MMA half of it.
+constexpr int kAcKCol = 128 * kAcWG;
+static_assert(kAcKCol + 64 <= 512, "TMEM: S^T buffers + key block");
 struct AcBars {
-    uint64_t k_full, q_full[kQStages], q_empty[kQStages], s_full[kAcWG], s_free[kAcWG];
+    uint64_t k_full, k_tmem, q_full[kQStages], q_empty[kQStages], s_full[kAcWG], s_free[kAcWG];
     uint32_t tmem;
     alignas(16) float lse2[kAcWG][2][kTile];  // [warpgroup][item parity][query], -lse*log2e (ld.shared.v4)
     float part[kAcWG - 1][kTile];             // partial sums of warpgroups 1..
@@ -418,6 +424,7 @@ __global__ void __launch_bounds__(kAcThreads, 1)
     }
     if (tid == kAcTma * 32) {
         mbar_init(&B.k_full, 1);
+        mbar_init(&B.k_tmem, 128);
         for (int s = 0; s < kQStages; ++s) {
             mbar_init(&B.q_full[s], 1);
             mbar_init(&B.q_empty[s], 1);
@@ -452,7 +459,7 @@ __global__ void __launch_bounds__(kAcThreads, 1)
         }
     } else if (warp == kAcMma) {
         if (lane == 0) {
-            mbar_wait(&B.k_full, 0);
+            mbar_wait(&B.k_tmem, 0);  // the key block is in TMEM (A operand of every S^T MMA)
             for (int it = 0; it < n_items; ++it) {
                 // S^T(item) = K_blk Q_t^T into the TMEM buffer of warpgroup it % kAcWG.  (Split
                 // into two N = 64 halves with their own barriers it measured 1.46x slower.)
@@ -462,8 +469,8 @@ __global__ void __launch_bounds__(kAcThreads, 1)
                 tc_fence_after();
                 const uint8_t* q = sQ + s * kTileB;
 #pragma unroll
-                for (int kk = 0; kk < 8; ++kk)
-                    umma_f16(tmem + 128 * bb, kslice(sK, kk), kslice(q, kk), kIdescS, kk > 0 ? 1u : 0u);
+                for (int kk = 0; kk < 8; ++kk)  // A = K_blk from TMEM (8 columns = 16 d per step), B = Q tile
+                    umma_f16_ts(tmem + 128 * bb, tmem + kAcKCol + 8 * kk, kslice(q, kk), kIdescS, kk > 0 ? 1u : 0u);
                 umma_commit(&B.s_full[bb]);
                 umma_commit(&B.q_empty[s]);
             }
@@ -487,6 +494,24 @@ __global__ void __launch_bounds__(kAcThreads, 1)
         // exponentials into four pair accumulators
         const float2 s2 = make_float2(sl2, sl2);
         float2 a0 = make_float2(0.0f, 0.0f), a1 = a0, a2 = a0, a3 = a0;
+        if (wg == 0) {
+            // key row kr (SW128 tile: two 64-column halves, 16-byte chunk c of row r at
+            // r * 128 + ((c ^ (r & 7)) << 4)) -> TMEM lane kr, columns kAcKCol + d / 2
+            mbar_wait(&B.k_full, 0);
+            uint32_t kv[64];
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf)
+#pragma unroll
+                for (int c = 0; c < 8; ++c)
+                    *reinterpret_cast<uint4*>(kv + 32 * hf + 4 * c) =
+                        *reinterpret_cast<const uint4*>(sK + hf * kHalf + kr * 128 + ((c ^ (kr & 7)) << 4));
+            const uint32_t tk = tmem + ((uint32_t)((warp & 3) * 32) << 16) + kAcKCol;
+            tmem_st32(tk, *reinterpret_cast<uint32_t(*)[32]>(kv));
+            tmem_st32(tk + 32, *reinterpret_cast<uint32_t(*)[32]>(kv + 32));
+            tmem_wait_st();
+            tc_fence_before();
+            mbar_arrive(&B.k_tmem);
+        }
         ItemPos pos{0, t_first};
         pos.advance(wg, t_first, n_qt);
         ItemPos nxt = pos;
