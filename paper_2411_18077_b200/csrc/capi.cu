@@ -143,6 +143,7 @@ struct mkv_cache {
         m.page_base = page_base[u];
         m.n_pages = n_pages[u];
         m.n_prefill = n_prefill[u];
+        m.n_built = 0;  // (an upload restarts the block's page build: the flush builds every group)
         m.n_res = n_res[u];
         m.cap_pages = cap_pages[u];
         return m;

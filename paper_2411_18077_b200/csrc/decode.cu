@@ -484,7 +484,7 @@ cudaError_t launch_pages(const PagesParams& p, int grid, cudaStream_t s, bool pd
 // ---------------------------------------------------------------------------
 // append kernel: decode_append with flush (flush steps only)
 // ---------------------------------------------------------------------------
-constexpr int kAppendThreads = 256;
+constexpr int kAppendThreads = 32;  // one warp per unit: at a flush usually one group (of n_r / 16) is left to quantize
 
 // One CTA per unit.  S.n_seg == 0: the units of P (unit_begin + block, tokens P.k_new /
 // P.v_new); otherwise segment s covers blocks [S.block_begin[s], S.block_begin[s + 1]) with its
@@ -518,17 +518,35 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(const ResidualPa
     }
     __threadfence();  // the new row is read back below by cp.async.cg (through L2)
     __syncthreads();
+    // (the K3 staged page builder: rows by cp.async, codes from fp16 pairs)
+    PageRows& rows = reinterpret_cast<PageRows*>(smem_raw)[warp];
+    PageParams& prm = reinterpret_cast<PageParams*>(smem_raw + (kAppendThreads / 32) * sizeof(PageRows))[warp];
     if (n < P.n_r) {
-        if (tid == 0) P.meta[u].n_res = n;
+        // a filled 16-row group is quantized now into the page it occupies after the flush (as
+        // finish_kernel does on decode steps), so the flush builds only the groups still open
+        const bool early = (n & 15) == 0 && meta.n_built == (n >> 4) - 1 && meta.n_pages + (n >> 4) <= meta.cap_pages;
+        if (early && warp == 0) {
+            const int j = (n >> 4) - 1;
+            stage_rows_contig(rows, rk + (size_t)16 * j * d, rv + (size_t)16 * j * d);
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+            __syncwarp();
+            const int64_t page = meta.page_base + meta.n_pages + j;
+            if (!build_page_staged(rows, prm, 16, P.pool + (size_t)page * kPageBytes,
+                                   P.shadow ? P.shadow + (size_t)page * (kShadowBytes / 4) : nullptr) &&
+                lane == 0)
+                atomicOr(P.status, kStatusNonFinite);
+        }
+        if (tid == 0) {
+            P.meta[u].n_res = n;
+            if (early) P.meta[u].n_built = n >> 4;
+        }
         return;
     }
     // store_block (cache_engine.cpp:34-52): quantize the full block into n_r/16 pages
     const int npg = P.n_r / kGroup;
     bool ok = true;
-    // (the K3 staged page builder: rows by cp.async, codes from fp16 pairs)
-    PageRows& rows = reinterpret_cast<PageRows*>(smem_raw)[warp];
-    PageParams& prm = reinterpret_cast<PageParams*>(smem_raw + (kAppendThreads / 32) * sizeof(PageRows))[warp];
-    for (int j = warp; j < npg; j += kAppendThreads / 32) {
+    // groups [0, n_built) were quantized when they filled (finish_kernel): only the rest
+    for (int j = warp + meta.n_built; j < npg; j += kAppendThreads / 32) {
         stage_rows_contig(rows, rk + (size_t)16 * j * d, rv + (size_t)16 * j * d);
         asm volatile("cp.async.wait_group 0;\n" ::: "memory");
         __syncwarp();
@@ -541,6 +559,7 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(const ResidualPa
     if (tid == 0) {
         P.meta[u].n_pages = meta.n_pages + npg;
         P.meta[u].n_res = 0;
+        P.meta[u].n_built = 0;
     }
 }
 
@@ -657,7 +676,10 @@ constexpr int kFinishThreads = kFinishWarps * 32;
 // finish CTA keeps fitting beside a page-kernel CTA.
 constexpr int kFinishSlot = 8192;
 constexpr int kFinishSlotFlush = (int)sizeof(PageScratch);
-__host__ __device__ constexpr int finish_smem_bytes(int slot) { return kFinishWarps * slot + kFinishWarps * 2 * kMaxG * 4; }
+// + one PageParams (1 KB): the page a filled 16-row group becomes (finish_kernel, early build)
+__host__ __device__ constexpr int finish_smem_bytes(int slot) {
+    return kFinishWarps * slot + kFinishWarps * 2 * kMaxG * 4 + (int)sizeof(PageParams);
+}
 static_assert(offsetof(PageScratch, k) == 0 && offsetof(PageScratch, v) == 4096, "tile = PageScratch k, v");
 
 __device__ __forceinline__ void ldmatrix_x4_trans(uint32_t (&r)[4], const void* p) {
@@ -846,6 +868,21 @@ __global__ void __launch_bounds__(kFinishThreads, 5) finish_kernel(const Residua
         __syncwarp();
         attend_tile(n - row0);
     }
+    // Early page build: when this append fills a 16-row group of the residual block (and the
+    // block is not flushed now), the warp that attended that group's tile -- its 16 rows are in
+    // the tile, in the staged builder's swizzled layout -- quantizes it into the page it will
+    // occupy after the flush (store_block groups, cache_engine.cpp:34-52: each 16-row group is
+    // its own page, so the result is the flush's), so the flush step builds only the last one.
+    const bool early_build = app && !flush && (n & 15) == 0 && n < P.n_r && P.meta[u].n_built == (n >> 4) - 1 &&
+                             P.meta[u].n_pages + (n >> 4) <= P.meta[u].cap_pages;
+    if (early_build && warp == ((n >> 4) - 1) % kFinishWarps) {
+        PageParams& prm = *reinterpret_cast<PageParams*>(smem_raw + finish_smem_bytes(slot) - (int)sizeof(PageParams));
+        const int64_t page = P.meta[u].page_base + P.meta[u].n_pages + (n >> 4) - 1;
+        __syncwarp();
+        const bool ok = build_page_staged(*reinterpret_cast<PageRows*>(tile), prm, 16, P.pool + (size_t)page * kPageBytes,
+                                          P.shadow ? P.shadow + (size_t)page * (kShadowBytes / 4) : nullptr);
+        if (!ok && lane == 0) atomicOr(P.status, kStatusNonFinite);
+    }
 #pragma unroll
     for (int o = 4; o < 32; o <<= 1) {
         l0 += __shfl_xor_sync(0xffffffffu, l0, o);
@@ -864,12 +901,15 @@ __global__ void __launch_bounds__(kFinishThreads, 5) finish_kernel(const Residua
         if (h0 < G) { wml[warp][0][h0] = m0; wml[warp][1][h0] = l0; }
         if (h1 < G) { wml[warp][0][h1] = m1; wml[warp][1][h1] = l1; }
     }
+    __syncthreads();  // every read of this unit's meta above is done before it changes
     if (app && tid == 0) {  // only this CTA reads this unit's meta after the append
         if (flush) {
             P.meta[u].n_pages += P.n_r / kGroup;
             P.meta[u].n_res = 0;
+            P.meta[u].n_built = 0;
         } else {
             P.meta[u].n_res = n;
+            if (early_build) P.meta[u].n_built = n >> 4;
         }
     }
     // ---- the page partials are complete past this point ----

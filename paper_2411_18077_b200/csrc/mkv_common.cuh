@@ -75,6 +75,9 @@ struct UnitMeta {
     int32_t n_prefill;  // tokens in the prefill block (its last page may be partial)
     int32_t n_res;      // residual tokens
     int32_t cap_pages;
+    int32_t n_built;    // 16-row groups of the residual block already quantized into their pages
+                        // (pool pages n_pages .. n_pages + n_built - 1, not yet attended as pages:
+                        // the flush makes them visible and builds only the rest); device-side only
 };
 
 // Device status word bits
