@@ -20,7 +20,24 @@ for s in range(16):
     torch.cuda.synchronize()
     times.append(e0.elapsed_time(e1))
 print(" ".join(f"{t:.3f}" for t in times))
-print(f"flush step (8th) {times[7]:.3f} ms vs median {sorted(times)[8]:.3f} ms")
+print(f"flush step (8th) {times[7]:.3f} ms vs median {sorted(times)[8]:.3f} ms (each step synchronized)")
+
+# the same 16 steps issued back to back (events between steps, one synchronize at the end):
+# device time per step with the host running ahead, as in bench.py's timed loop
+for s in range(200):  # advance to 7 steps before the next flush
+    if cache.unit_info(0)["tokens_residual"] == cache.n_r - 8:
+        break
+    step()
+torch.cuda.synchronize()
+evs = [torch.cuda.Event(enable_timing=True) for _ in range(17)]
+evs[0].record()
+for s in range(16):
+    step()
+    evs[s + 1].record()
+torch.cuda.synchronize()
+dev = [evs[s].elapsed_time(evs[s + 1]) for s in range(16)]
+print(" ".join(f"{t:.3f}" for t in dev))
+print(f"flush step (8th) {dev[7]:.3f} ms vs median {sorted(dev)[8]:.3f} ms (back to back: device time)")
 
 # split the flush cost: the append kernels alone (append-only call) and the next attend
 # (which re-uploads the 32 changed plans)
