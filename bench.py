@@ -232,6 +232,24 @@ def load_traffic(kernel, launch_units):
     return None, None
 
 
+def host_cpu():
+    """The GPU host's CPU as the CPU baselines ran on it (record nproc and lscpu)."""
+    info = {"nproc": os.cpu_count()}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            k, _, v = line.partition(":")
+            if k.strip() in ("Model name", "Socket(s)", "Core(s) per socket", "Thread(s) per core", "CPU max MHz"):
+                info[k.strip()] = v.strip()
+    except Exception:
+        try:
+            with open("/proc/cpuinfo") as f:
+                info["Model name"] = next(l.split(":", 1)[1].strip() for l in f if l.startswith("model name"))
+        except Exception:
+            pass
+    return info
+
+
 def load_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -947,7 +965,8 @@ def reference_arm(args, world):
             "higher_is_better": True, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic (integer-exact N(0,1) fp16 K/V, uniform A_cumul)",
             "config": config_desc(args, world),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample,
+                             "host": host_cpu()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     if not args.no_config0:
         try:
@@ -1004,7 +1023,8 @@ def main():
                                   f"({args.cpu_units_per_layer}/layer, every pyramid budget), {args.steps} timed decode "
                                   f"steps, {threads} threads; x{factor:g} to a full step (units are independent)",
                         "one_thread_value": B / (r["one_thread_step_s"] * factor),
-                        "one_thread_sample_step_s": r["one_thread_step_s"], "sample_step_s": r["sample_step_s"]}
+                        "one_thread_sample_step_s": r["one_thread_step_s"], "sample_step_s": r["sample_step_s"],
+                        "host": host_cpu()}
                     extras["parity"] = {
                         "what": "GPU decode outputs of the last timed step (mkv_decode_step_layers, 32 layers, through "
                                 "the pre-roll and the in-window flush) vs the unmodified reference decode "
