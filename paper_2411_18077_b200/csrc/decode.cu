@@ -682,6 +682,12 @@ __host__ __device__ constexpr int finish_smem_bytes(int slot) {
 }
 static_assert(offsetof(PageScratch, k) == 0 && offsetof(PageScratch, v) == 4096, "tile = PageScratch k, v");
 
+// The early page build as a real call: inlined, the builder's registers would raise the finish
+// kernel's (capped at 96 so a finish CTA fits beside a page CTA) and spill in its hot loop.
+__device__ __noinline__ bool build_page_call(PageRows& rows, PageParams& prm, uint8_t* dst, float* shadow) {
+    return build_page_staged(rows, prm, 16, dst, shadow);
+}
+
 __device__ __forceinline__ void ldmatrix_x4_trans(uint32_t (&r)[4], const void* p) {
     asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
                  : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
@@ -879,8 +885,8 @@ __global__ void __launch_bounds__(kFinishThreads, 5) finish_kernel(const Residua
         PageParams& prm = *reinterpret_cast<PageParams*>(smem_raw + finish_smem_bytes(slot) - (int)sizeof(PageParams));
         const int64_t page = P.meta[u].page_base + P.meta[u].n_pages + (n >> 4) - 1;
         __syncwarp();
-        const bool ok = build_page_staged(*reinterpret_cast<PageRows*>(tile), prm, 16, P.pool + (size_t)page * kPageBytes,
-                                          P.shadow ? P.shadow + (size_t)page * (kShadowBytes / 4) : nullptr);
+        const bool ok = build_page_call(*reinterpret_cast<PageRows*>(tile), prm, P.pool + (size_t)page * kPageBytes,
+                                        P.shadow ? P.shadow + (size_t)page * (kShadowBytes / 4) : nullptr);
         if (!ok && lane == 0) atomicOr(P.status, kStatusNonFinite);
     }
 #pragma unroll
