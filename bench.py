@@ -664,13 +664,18 @@ def config0_gpu():
         cache.decode_steps(qdd, kdd, vdd, scale, out=outs)  # the 256 steps in one FFI crossing
         return r
 
-    for _ in range(2):  # warm-up (module load, kernel attributes, clocks up after the CPU phases)
+    # warm-up: module load, kernel attributes, and at least ~0.3 s of GPU work so the clocks are
+    # back up after the CPU phases that precede this leg (a short chain is launch-bound)
+    t_w = time.perf_counter()
+    n_w = 0
+    while n_w < 2 or time.perf_counter() - t_w < 0.3:
         cache = new_cache()
         r = chain(cache, q, k, v, qd, kd, vd)
         torch.cuda.synchronize()
         cache.close()
+        n_w += 1
     times, allocs = [], []
-    for _ in range(5):  # median of 5 timed chains
+    for _ in range(9):  # median of 9 timed chains
         t0 = time.perf_counter()
         cache = new_cache()
         torch.cuda.synchronize()
@@ -694,7 +699,7 @@ def config0_gpu():
     hqd, hkd, hvd = qd.cpu().pin_memory(), kd.cpu().pin_memory(), vd.cpu().pin_memory()
     hout = torch.empty_like(outs, device="cpu").pin_memory()
     e2es = []
-    for _ in range(3):  # median of 3
+    for _ in range(5):  # median of 5
         cache = new_cache()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -705,14 +710,14 @@ def config0_gpu():
         torch.cuda.synchronize()
         e2es.append((time.perf_counter() - t0) * 1e3)
         cache.close()
-    e2e_ms = sorted(e2es)[1]
+    e2e_ms = sorted(e2es)[len(e2es) // 2]
     total_ms = t_attn + t_pack + t_dec
     P = L * (L + 1) / 2
     return {
         "workload": "configs[0]: 1 layer, 8 heads (MHA), d=128, 4K causal prefill (K1) -> 20% budget select (K2, "
                     "409 HH + 409 RW) -> 2-bit pack (K3) -> 256 decode steps (K4, 2 flushes)",
         "gpu_ms": {"prefill_attn": t_attn, "select_pack": t_pack, "decode_256": t_dec, "total": total_ms,
-                   "e2e_total_from_host": e2e_ms, "make_cache_outside_timing": sorted(allocs)[2]},
+                   "e2e_total_from_host": e2e_ms, "make_cache_outside_timing": sorted(allocs)[len(allocs) // 2]},
         "how": "make_cache (the device pool allocation) before the timed region; K1 -> K2+K3 -> "
                "256 decode steps through KVCache.decode_steps (mkv_decode_steps: one FFI crossing); "
                "e2e copies Q/K/V and the decode tokens from pinned host buffers and reads every output back",
