@@ -449,8 +449,10 @@ def run_mkv(args, rank, world):
         barrier(world)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
+        th0 = time.perf_counter()
         for s in range(s_steps):
             serve_step(s, s & 1)
+        host_ms = (time.perf_counter() - th0) * 1e3  # the host's issue time (runs ahead of the GPU)
         e1.record(stream)
         torch.cuda.synchronize()
         sms = dist_max(e0.elapsed_time(e1), world)
@@ -459,7 +461,7 @@ def run_mkv(args, rank, world):
             step_roofline_frac_approx=(bytes_timed / args.steps) / (sms / s_steps / 1e3) / 1e9 / load_peaks()[0],
             how="32 mkv_decode_step calls per step; layer l+1's q is layer l's output (device buffer, "
                 "no host round trip): each page kernel waits for the previous layer's merge",
-            steps=s_steps)
+            host_issue_ms_per_step=host_ms / s_steps, steps=s_steps)
 
     # ---- dominant kernel alone (K4 page kernel, as the timed steps launch it: one launch over
     #      all n_units, or one per layer under MKV_LAYERS_SPLIT), CUDA events on its stream ----
