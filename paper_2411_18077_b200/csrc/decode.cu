@@ -666,7 +666,7 @@ cudaError_t launch_plan_build(const UnitMeta* meta, const PlanBuildJobs& jobs, c
 // page-kernel CTA (<= 208 x 256 registers, 150 KB), so layer l's finish runs its residual
 // attention while layer l's pages are still in flight and layer l + 1's pages overlap its merge.
 constexpr int kFinishWarps = 4;
-constexpr int kMergeBatch = 8;  // page partials folded per online-max round
+constexpr int kMergeBatch = 12;  // page partials folded per online-max round (one L2 round trip)
 constexpr int kFinishThreads = kFinishWarps * 32;
 
 // Shared memory: one slot per warp -- 16 K rows + 16 V rows (swizzled 16-byte chunks, 8 KB;
@@ -923,53 +923,62 @@ __global__ void __launch_bounds__(kFinishThreads, 5) finish_kernel(const Residua
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
     fstamp(2);
     __syncthreads();  // residual warp partials visible
-    // Merge: every thread loads (m, l, o) of kMergeBatch page partials at once and folds them
-    // with an online max (no global-max pass, no further barriers).
-    for (int e = tid; e < G * (d / 2); e += kFinishThreads) {
-        const int h = e / (d / 2), c2 = e % (d / 2);
-        float M = -INFINITY, L = 0.0f, ax = 0.0f, ay = 0.0f;
+    // Merge: every thread owns 4 consecutive channels of one head (float4: one chunk per thread
+    // at G = 4) and loads (m, l, o) of kMergeBatch page partials at once -- one L2 round trip
+    // for a unit split over up to kMergeBatch page warps -- folded with an online max (no
+    // global-max pass, no further barriers).  h is warp-uniform: the (m, l) loads broadcast.
+    for (int e = tid; e < G * (d / 4); e += kFinishThreads) {
+        const int h = e / (d / 4), c4 = e % (d / 4);
+        float M = -INFINITY, L = 0.0f;
+        float4 a = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
         for (int w = 0; w < kFinishWarps; ++w) {
             const float lw = wml[w][1][h];
             if (lw > 0.0f) {
                 const float mw = wml[w][0][h];
                 const float nm = fmaxf(M, mw);
                 const float f = fast_exp2(M - nm), s = fast_exp2(mw - nm);
-                const float2 wv = reinterpret_cast<const float2*>(smem_raw + w * slot)[h * (kHeadDim / 2) + c2];
-                ax = fmaf(wv.x, s, ax * f);
-                ay = fmaf(wv.y, s, ay * f);
+                const float4 wv = reinterpret_cast<const float4*>(smem_raw + w * slot)[h * (kHeadDim / 4) + c4];
+                a.x = fmaf(wv.x, s, a.x * f);
+                a.y = fmaf(wv.y, s, a.y * f);
+                a.z = fmaf(wv.z, s, a.z * f);
+                a.w = fmaf(wv.w, s, a.w * f);
                 L = fmaf(lw, s, L * f);
                 M = nm;
             }
         }
         for (int p0 = 0; p0 < n_part; p0 += kMergeBatch) {
             float pm[kMergeBatch], pl[kMergeBatch];
-            float2 po[kMergeBatch];
+            float4 po[kMergeBatch];
 #pragma unroll
             for (int k = 0; k < kMergeBatch; ++k) {
                 const int slot = w_first + p0 + k + i;
                 const bool ok = p0 + k < n_part;
                 pm[k] = ok ? __ldcg(P.part_ml + (size_t)slot * 2 * kMaxG + h) : -INFINITY;
                 pl[k] = ok ? __ldcg(P.part_ml + (size_t)slot * 2 * kMaxG + kMaxG + h) : 0.0f;
-                po[k] = ok ? __ldcg(reinterpret_cast<const float2*>(P.part_o + ((size_t)slot * kMaxG + h) * d) + c2)
-                           : make_float2(0.0f, 0.0f);
+                po[k] = ok ? __ldcg(reinterpret_cast<const float4*>(P.part_o + ((size_t)slot * kMaxG + h) * d) + c4)
+                           : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
             }
             float cm = pm[0];
 #pragma unroll
             for (int k = 1; k < kMergeBatch; ++k) cm = fmaxf(cm, pm[k]);
             const float nm = fmaxf(M, cm);
             const float f = fast_exp2(M - nm);
-            ax *= f; ay *= f; L *= f;
+            a.x *= f; a.y *= f; a.z *= f; a.w *= f; L *= f;
 #pragma unroll
             for (int k = 0; k < kMergeBatch; ++k) {
                 const float s = fast_exp2(pm[k] - nm);  // 0 for absent partials (m = -inf)
-                ax = fmaf(po[k].x, s, ax);
-                ay = fmaf(po[k].y, s, ay);
+                a.x = fmaf(po[k].x, s, a.x);
+                a.y = fmaf(po[k].y, s, a.y);
+                a.z = fmaf(po[k].z, s, a.z);
+                a.w = fmaf(po[k].w, s, a.w);
                 L = fmaf(pl[k], s, L);
             }
             M = nm;
         }
         const float li = 1.0f / L;
-        reinterpret_cast<__half2*>(P.out + ((size_t)i * G + h) * d)[c2] = __floats2half2_rn(ax * li, ay * li);
+        __half2* o2 = reinterpret_cast<__half2*>(P.out + ((size_t)i * G + h) * d) + 2 * c4;
+        o2[0] = __floats2half2_rn(a.x * li, a.y * li);
+        o2[1] = __floats2half2_rn(a.z * li, a.w * li);
     }
     __syncthreads();
     fstamp(3);
