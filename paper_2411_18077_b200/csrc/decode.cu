@@ -99,6 +99,19 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
     return cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 
+// The page kernel (146 KB) and a finish CTA (33 KB) share an SM only under the largest
+// shared-memory carveout; left to the driver, an SM may be configured for the page CTA alone,
+// and a finish CTA placed there waits for the page CTA to exit (its residual attention then
+// lands on the layer's critical path).  MKV_CARVEOUT=<percent> (-1: driver default) for A/B.
+static cudaError_t set_carveout(const void* fn) {
+    static const int pct = [] {
+        const char* e = getenv("MKV_CARVEOUT");
+        return e ? atoi(e) : 100;
+    }();
+    if (pct < 0) return cudaSuccess;
+    return cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -439,6 +452,7 @@ static cudaError_t launch_pages_t(const PagesParams& p, int grid, cudaStream_t s
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(pages_kernel<W, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess) e = set_carveout(reinterpret_cast<const void*>(pages_kernel<W, S>));
         if (e != cudaSuccess) return e;
         configured = true;
     }
@@ -991,6 +1005,7 @@ cudaError_t launch_finish(const ResidualParams& p, const int32_t* pref, WorkerRa
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              finish_smem_bytes(kFinishSlotFlush));
+        if (e == cudaSuccess) e = set_carveout(reinterpret_cast<const void*>(finish_kernel));
         if (e != cudaSuccess) return e;
         configured = true;
     }

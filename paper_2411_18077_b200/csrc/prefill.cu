@@ -371,9 +371,14 @@ constexpr int kAcTma = kAcWG * 4, kAcMma = kAcWG * 4 + 1;
 // shared memory -- an SS MMA at M = N = 128 reads 8 KB of shared memory per 64-clk K step, the
 // whole 128 B/clk, a TS MMA half of it.
 constexpr int kAcKCol = 128 * kAcWG;
-static_assert(kAcKCol + 64 <= 512, "TMEM: S^T buffers + key block");
+// kNB = kAcWG (default): one S^T buffer per warpgroup, the key block in TMEM (TS MMAs).
+// kNB = 4 (MKV_ACUMUL_BUFS=4, A/B): the key block stays in shared memory (SS MMAs) and its 64
+// TMEM columns become a fourth S^T buffer -- a ring of 4 buffers over the 3 warpgroups, so the
+// MMA of item it + 1 may run while every warpgroup still holds its current S^T.
+constexpr int kAcMaxBufs = 4;
+static_assert(kAcKCol + 64 <= 512 && 128 * kAcMaxBufs <= 512, "TMEM: S^T buffers + key block");
 struct AcBars {
-    uint64_t k_full, k_tmem, q_full[kQStages], q_empty[kQStages], s_full[kAcWG], s_free[kAcWG];
+    uint64_t k_full, k_tmem, q_full[kQStages], q_empty[kQStages], s_full[kAcMaxBufs], s_free[kAcMaxBufs];
     uint32_t tmem;
     alignas(16) float lse2[kAcWG][2][kTile];  // [warpgroup][item parity][query], -lse*log2e (ld.shared.v4)
     float part[kAcWG - 1][kTile];             // partial sums of warpgroups 1..
@@ -395,7 +400,10 @@ struct ItemPos {
 
 // kPoly of every 4 exponential PAIRS run as a polynomial on the FMA pipe (FFMA2, the rest
 // on MUFU.EX2).  Per element the pass costs 1 exponential + half an FFMA2 + half an FADD2.
-template <int kPoly>
+// kDirect (MKV_ACUMUL_LSE=direct, A/B; needs lq % 4 == 0): every thread reads the item's 128
+// LSE values straight from global memory (L1 broadcast, ld.global.nc.v4) instead of the
+// warpgroup staging them in shared memory behind a named barrier per item.
+template <int kPoly, int kNB, bool kDirect = false>
 __global__ void __launch_bounds__(kAcThreads, 1)
     acumul_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                   const PrefillAttnParams P) {
@@ -429,7 +437,7 @@ __global__ void __launch_bounds__(kAcThreads, 1)
             mbar_init(&B.q_full[s], 1);
             mbar_init(&B.q_empty[s], 1);
         }
-        for (int s = 0; s < kAcWG; ++s) {
+        for (int s = 0; s < kNB; ++s) {
             mbar_init(&B.s_full[s], 1);
             mbar_init(&B.s_free[s], 128);
         }
@@ -459,18 +467,25 @@ __global__ void __launch_bounds__(kAcThreads, 1)
         }
     } else if (warp == kAcMma) {
         if (lane == 0) {
-            mbar_wait(&B.k_tmem, 0);  // the key block is in TMEM (A operand of every S^T MMA)
+            if constexpr (kNB == kAcWG)
+                mbar_wait(&B.k_tmem, 0);  // the key block is in TMEM (A operand of every S^T MMA)
+            else
+                mbar_wait(&B.k_full, 0);
             for (int it = 0; it < n_items; ++it) {
-                // S^T(item) = K_blk Q_t^T into the TMEM buffer of warpgroup it % kAcWG.  (Split
-                // into two N = 64 halves with their own barriers it measured 1.46x slower.)
-                const int s = it % kQStages, bb = it % kAcWG;
+                // S^T(item) = K_blk Q_t^T into TMEM buffer it % kNB.  (Split into two N = 64
+                // halves with their own barriers it measured 1.46x slower.)
+                const int s = it % kQStages, bb = it % kNB;
                 mbar_wait(&B.q_full[s], (it / kQStages) & 1);
-                if (it >= kAcWG) mbar_wait(&B.s_free[bb], ((it / kAcWG) - 1) & 1);
+                if (it >= kNB) mbar_wait(&B.s_free[bb], ((it / kNB) - 1) & 1);
                 tc_fence_after();
                 const uint8_t* q = sQ + s * kTileB;
 #pragma unroll
-                for (int kk = 0; kk < 8; ++kk)  // A = K_blk from TMEM (8 columns = 16 d per step), B = Q tile
-                    umma_f16_ts(tmem + 128 * bb, tmem + kAcKCol + 8 * kk, kslice(q, kk), kIdescS, kk > 0 ? 1u : 0u);
+                for (int kk = 0; kk < 8; ++kk) {
+                    if constexpr (kNB == kAcWG)  // A = K_blk from TMEM (8 columns = 16 d per step), B = Q tile
+                        umma_f16_ts(tmem + 128 * bb, tmem + kAcKCol + 8 * kk, kslice(q, kk), kIdescS, kk > 0 ? 1u : 0u);
+                    else
+                        umma_f16(tmem + 128 * bb, kslice(sK, kk), kslice(q, kk), kIdescS, kk > 0 ? 1u : 0u);
+                }
                 umma_commit(&B.s_full[bb]);
                 umma_commit(&B.q_empty[s]);
             }
@@ -481,7 +496,7 @@ __global__ void __launch_bounds__(kAcThreads, 1)
         const int wg = warp >> 2;
         const int kr = tid & 127;
         const int kj = key0 + kr;
-        const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16) + 128 * wg;
+        const uint32_t trow0 = tmem + ((uint32_t)((warp & 3) * 32) << 16);
         const float sl2 = P.scale * kLog2e;
         // the LSE of the query row this thread stages is loaded one item ahead: its global
         // latency hides behind the current item's exponentials (consumed only at the next one)
@@ -494,7 +509,7 @@ __global__ void __launch_bounds__(kAcThreads, 1)
         // exponentials into four pair accumulators
         const float2 s2 = make_float2(sl2, sl2);
         float2 a0 = make_float2(0.0f, 0.0f), a1 = a0, a2 = a0, a3 = a0;
-        if (wg == 0) {
+        if (kNB == kAcWG && wg == 0) {
             // key row kr (SW128 tile: two 64-column halves, 16-byte chunk c of row r at
             // r * 128 + ((c ^ (r & 7)) << 4)) -> TMEM lane kr, columns kAcKCol + d / 2
             mbar_wait(&B.k_full, 0);
@@ -519,18 +534,24 @@ __global__ void __launch_bounds__(kAcThreads, 1)
         float lse_next = load_lse(wg, pos);
         for (int it = wg, k = 0; it < n_items; it += kAcWG, ++k) {
             float* l2 = B.lse2[wg][k & 1];
-            l2[kr] = lse_next * -kLog2e;  // INFINITY -> -inf: masked rows add exact zeros
-            named_bar_sync(1 + wg, 128);
-            lse_next = load_lse(it + kAcWG, nxt);
+            const float* lrow = lse_b + (size_t)pos.g * P.lq + (size_t)pos.t * kTile;
+            if constexpr (!kDirect) {
+                l2[kr] = lse_next * -kLog2e;  // INFINITY -> -inf: masked rows add exact zeros
+                named_bar_sync(1 + wg, 128);
+                lse_next = load_lse(it + kAcWG, nxt);
+            }
             const int t = pos.t;
+            const int c_lim = P.lq - t * kTile;  // columns >= c_lim are past the last query
             pos = nxt;
             nxt.advance(kAcWG, t_first, n_qt);
             const uint32_t l2a = smem_u32(l2);
-            mbar_wait(&B.s_full[wg], k & 1);
+            const int bb = it % kNB;
+            const uint32_t trow = trow0 + 128 * bb;
+            mbar_wait(&B.s_full[bb], (it / kNB) & 1);
             tc_fence_after();
             // query i = t*128 + c visible iff kj <= offset + i  <=>  c >= kj - offset - t*128
             const int c_min = P.causal ? (kj - offset - t * kTile) : -1;
-            const bool full = __all_sync(0xffffffffu, c_min <= 0);
+            const bool full = __all_sync(0xffffffffu, c_min <= 0) && (!kDirect || c_lim >= kTile);
             // the two loops differ only in the causal mask (diagonal items): separate copies keep
             // the full-tile loop free of per-column compares
             auto tile = [&](auto masked) {
@@ -542,11 +563,23 @@ __global__ void __launch_bounds__(kAcThreads, 1)
                     tmem_wait_ld();
                     if (half == 1) {
                         tc_fence_before();
-                        mbar_arrive(&B.s_free[wg]);  // TMEM buffer free for the next MMA into it
+                        mbar_arrive(&B.s_free[bb]);  // TMEM buffer free for the next MMA into it
                     }
 #pragma unroll
                     for (int c = 0; c < 64; c += 4) {
-                        const float4 nl = lds128(l2a + (64 * half + c) * 4);
+                        float4 nl;
+                        if constexpr (kDirect) {
+                            const int col = 64 * half + c;
+                            const float4 lv = (!decltype(masked)::value || col < c_lim)
+                                                  ? __ldg(reinterpret_cast<const float4*>(lrow + col))
+                                                  : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+                            const float2 m2 = make_float2(-kLog2e, -kLog2e);
+                            const float2 n0 = __fmul2_rn(make_float2(lv.x, lv.y), m2);
+                            const float2 n1 = __fmul2_rn(make_float2(lv.z, lv.w), m2);
+                            nl = make_float4(n0.x, n0.y, n1.x, n1.y);
+                        } else {
+                            nl = lds128(l2a + (64 * half + c) * 4);
+                        }
                         const float2 v0 = __ffma2_rn(make_float2(__uint_as_float(x[c]), __uint_as_float(x[c + 1])),
                                                      s2, make_float2(nl.x, nl.y));
                         const float2 v1 = __ffma2_rn(
@@ -558,10 +591,11 @@ __global__ void __launch_bounds__(kAcThreads, 1)
                                                                     : make_float2(fast_exp2(v1.x), fast_exp2(v1.y));
                         if constexpr (decltype(masked)::value) {
                             const int col = 64 * half + c;
-                            e0.x = col >= c_min ? e0.x : 0.0f;
-                            e0.y = col + 1 >= c_min ? e0.y : 0.0f;
-                            e1.x = col + 2 >= c_min ? e1.x : 0.0f;
-                            e1.y = col + 3 >= c_min ? e1.y : 0.0f;
+                            const int lo = c_min, hi = kDirect ? c_lim : kTile;  // visible: lo <= col < hi
+                            e0.x = (col >= lo && col < hi) ? e0.x : 0.0f;
+                            e0.y = (col + 1 >= lo && col + 1 < hi) ? e0.y : 0.0f;
+                            e1.x = (col + 2 >= lo && col + 2 < hi) ? e1.x : 0.0f;
+                            e1.y = (col + 3 >= lo && col + 3 < hi) ? e1.y : 0.0f;
                         }
                         if ((c & 4) == 0) {
                             a0 = __fadd2_rn(a0, e0);
@@ -626,14 +660,14 @@ bool make_map(CUtensorMap* m, const __half* base, int64_t sb, int64_t sh, int64_
 
 }  // namespace
 
-template <int KF, int KA>
+template <int KF, int KA, int NB = kAcWG, bool DIRECT = false>
 static cudaError_t launch_prefill_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                                    const PrefillAttnParams& p, cudaStream_t s) {
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel<KF>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFwdSmem);
         if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(acumul_kernel<KA>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAcSmem);
+        e = cudaFuncSetAttribute(acumul_kernel<KA, NB, DIRECT>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAcSmem);
         if (e != cudaSuccess) return e;
         configured = true;
     }
@@ -641,7 +675,7 @@ static cudaError_t launch_prefill_t(const CUtensorMap& tq, const CUtensorMap& tk
     attn_fwd_kernel<KF><<<dim3(p.hq * p.batch, (n_qt + 1) / 2), kFwdThreads, kFwdSmem, s>>>(tq, tk, tv, p);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    acumul_kernel<KA><<<dim3(p.hkv * p.batch, n_kt), kAcThreads, kAcSmem, s>>>(tq, tk, p);
+    acumul_kernel<KA, NB, DIRECT><<<dim3(p.hkv * p.batch, n_kt), kAcThreads, kAcSmem, s>>>(tq, tk, p);
     return cudaGetLastError();
 }
 
@@ -652,11 +686,21 @@ cudaError_t launch_prefill_attn(const PrefillAttnParams& p, cudaStream_t s) {
         !make_map(&tv, p.v, p.v_sb, p.v_sh, p.v_st, p.lk, p.hkv, p.batch))
         return cudaErrorInvalidValue;
     // exponentials on the FMA pipe: fwd per 8, A_cumul pairs per 4; MKV_PREFILL_POLY="f,a"
-    static int kf = 1, ka = 1;
+    static int kf = 1, ka = 1, nb = kAcWG;
+    static bool direct = false;
     static bool parsed = false;
     if (!parsed) {
         if (const char* e = getenv("MKV_PREFILL_POLY")) sscanf(e, "%d,%d", &kf, &ka);
+        if (const char* e = getenv("MKV_ACUMUL_BUFS")) nb = atoi(e);
+        if (const char* e = getenv("MKV_ACUMUL_LSE")) direct = e[0] == 'd';
         parsed = true;
+    }
+    if (direct && kf == 1 && ka == 1 && nb == kAcWG && p.lq % 4 == 0)
+        return launch_prefill_t<1, 1, kAcWG, true>(tq, tk, tv, p, s);
+    if (nb == 4 && kf == 1) {
+        if (ka == 0) return launch_prefill_t<1, 0, 4>(tq, tk, tv, p, s);
+        if (ka == 2) return launch_prefill_t<1, 2, 4>(tq, tk, tv, p, s);
+        return launch_prefill_t<1, 1, 4>(tq, tk, tv, p, s);
     }
     if (kf == 1 && ka == 0) return launch_prefill_t<1, 0>(tq, tk, tv, p, s);
     if (kf == 1 && ka == 2) return launch_prefill_t<1, 2>(tq, tk, tv, p, s);

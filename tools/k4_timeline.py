@@ -150,3 +150,11 @@ for name, (p, f) in zip(("layer n-2", "layer n-1"), lays):
         print("  finish resid done", pct(f[:, 1], t0))
         print("  finish wait rel. ", pct(f[:, 2], t0))
         print("  finish end       ", pct(f[:, 3], t0))
+    if len(f):
+        fw = f[f[:, 0] >= t0]
+        late = int((fw[:, 0] > p[:, 2].min()).sum())
+        print(f"  finish CTAs of this layer (in window): {len(fw)}, started after its first page warp finished: {late}")
+        print("  per CTA [us: min p10 median p90 max]")
+        print("    residual attention ", pct(fw[:, 1] - fw[:, 0], 0))
+        print("    wait release -> end", pct(fw[:, 3] - fw[:, 2], 0))
+        print("    last page done -> wait release", pct(fw[:, 2] - p[:, 2].max(), 0))
