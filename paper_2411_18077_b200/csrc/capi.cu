@@ -112,6 +112,9 @@ struct mkv_cache {
     __half* d_res_k = nullptr;
     __half* d_res_v = nullptr;
     uint32_t* d_status = nullptr;
+    int* d_unit_cnt = nullptr;    // split finish: per-unit arrival counters (zero between calls)
+    float* d_res_ml = nullptr;    // split finish: residual partial per unit
+    float* d_res_o = nullptr;
     uint64_t* d_trace = nullptr;  // diagnostics only (MKV_DECODE_TRACE)
     int32_t* d_kept = nullptr;    // prefill selection scratch (grow-only: no allocation per call)
     size_t kept_cap = 0;
@@ -134,6 +137,7 @@ struct mkv_cache {
         if (ev_compute) cudaEventDestroy(ev_compute);
         cudaFree(d_meta); cudaFree(d_pool); cudaFree(d_shadow); cudaFree(d_res_k); cudaFree(d_res_v);
         cudaFree(d_status);
+        cudaFree(d_unit_cnt); cudaFree(d_res_ml); cudaFree(d_res_o);
         cudaFree(d_trace);
         cudaFree(d_kept);
     }
@@ -400,6 +404,10 @@ int mkv_cache_create(const mkv_cache_config* cfg, mkv_cache** out) {
     if (e == cudaSuccess) e = al((void**)&c->d_res_v, (size_t)n * c->n_r * c->d * sizeof(__half));
     if (e == cudaSuccess) e = al((void**)&c->d_status, sizeof(uint32_t));
     if (e == cudaSuccess) e = cudaMemset(c->d_status, 0, sizeof(uint32_t));
+    if (e == cudaSuccess) e = al((void**)&c->d_unit_cnt, sizeof(int) * n);
+    if (e == cudaSuccess) e = cudaMemset(c->d_unit_cnt, 0, sizeof(int) * std::max(n, 1));
+    if (e == cudaSuccess) e = al((void**)&c->d_res_ml, sizeof(float) * 2 * kMaxG * n);
+    if (e == cudaSuccess) e = al((void**)&c->d_res_o, sizeof(float) * kMaxG * c->d * n);
     if (e == cudaSuccess) e = cudaMemset(c->d_pool, 0, (size_t)acc * kPageBytes);
     if (e == cudaSuccess) e = c->upload_meta(0, n, 0);
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
@@ -741,6 +749,25 @@ static void fill_pages_params(mkv_cache* c, const Plan* pl, const mkv_decode_arg
     pp.scale_log2 = a->scale * 1.4426950408889634f;
     pp.trace = trace_slot(c);
     pp.early = 0;
+    pp.unit_cnt = nullptr;
+}
+
+// The finish step in one kernel (finish_kernel: a CTA per unit attends the unit's residual
+// beside the page pass, waits for the page grid, merges) or two (launch_resid_merge: a
+// persistent residual kernel + a merge kernel on per-unit arrival counters).  One finish CTA
+// fits beside each page CTA, so with more units than SMs most finish CTAs -- residual attention
+// included -- would only start after the page pass; the split form then keeps the residual work
+// inside the page pass and leaves only the merges after it (headline step 0.622 -> 0.610 ms).
+// With at most one unit per SM the one-kernel form is faster (one grid hop less per call: the
+// dependent per-layer form, 0.84 vs 0.90 ms per 32-layer step).  MKV_MERGE=finish|split forces
+// a form.  The tcgen05 page-kernel A/B variant does not count arrivals: always one kernel.
+static bool split_finish(int n_units) {
+    static const int mode = [] {
+        const char* e = getenv("MKV_MERGE");
+        if (pages_config().tc || (e && e[0] == 'f')) return 0;
+        return (e && e[0] == 's') ? 1 : 2;
+    }();
+    return mode == 1 || (mode == 2 && n_units > num_sms());
 }
 
 // early: a later layer of one mkv_decode_step_layers call -- its q was written before the
@@ -826,6 +853,8 @@ static int decode_impl(mkv_cache* c, const mkv_decode_args* a, bool attend, cuda
     rp.status = c->d_status;
     rp.trace = nullptr;
     rp.fused_flush = fused && any_flush ? 1 : 0;
+    rp.unit_cnt = nullptr; rp.res_ml = c->d_res_ml; rp.res_o = c->d_res_o;
+    const bool split = attend && split_finish(n);
     // unfused flush steps (or append-only calls): append (+ quantize the full block) before the
     // page pass
     if (!fused && append && (any_flush || !attend)) {
@@ -839,7 +868,11 @@ static int decode_impl(mkv_cache* c, const mkv_decode_args* a, bool attend, cuda
     if (pl->total > 0) {
         PagesParams pp;
         fill_pages_params(c, pl, a, pp);
-        pp.early = early && (fused || !any_flush) ? 1 : 0;
+        // split finish: no early page passes -- the merge kernel does not wait for the page /
+        // residual grids, so a page kernel's start wait on the previous merge is what orders
+        // every later kernel after the previous layer's partials were consumed
+        pp.early = early && !split && (fused || !any_flush) ? 1 : 0;
+        if (split) pp.unit_cnt = c->d_unit_cnt;
         // full dependency when the plan was just written by a kernel or swapped in behind an
         // event wait (the page kernel reads it before its griddepcontrol.wait)
         CK(launch_pages(pp, pl->grid, s, !(after_plan_build || swapped)));
@@ -848,7 +881,12 @@ static int decode_impl(mkv_cache* c, const mkv_decode_args* a, bool attend, cuda
     rp.trace = trace_slot(c);
     if (rp.trace) rp.trace += trace_page_words();
     const WorkerRanges wr{std::max(pl->warps, 1), std::max(pl->total / pages_config().batch, 1), pages_config().batch};
-    CK(launch_finish(rp, pl->d_pref, wr, pl->total > 0, s));
+    if (split) {
+        rp.unit_cnt = c->d_unit_cnt;
+        CK(launch_resid_merge(rp, pl->d_pref, wr, pl->total > 0, std::min(n, num_sms()), s));
+    } else {
+        CK(launch_finish(rp, pl->d_pref, wr, pl->total > 0, s));
+    }
     ++c->trace_seq;
     // the next call's plan (new page counts), prepared and uploaded off the critical path
     if (fused && any_flush)

@@ -440,6 +440,11 @@ __global__ void __maxnreg__(208) pages_kernel(const PagesParams P) {
                 po[h1 * kHeadDim + c + 8] = fmaf(O[g][3], f, dv1);
             }
         }
+        if (P.unit_cnt != nullptr) {  // split finish: this segment's partial is visible, then counted
+            __threadfence();
+            __syncwarp();
+            if (lane == 0) atomicAdd(P.unit_cnt + P.unit_begin + unit, 1);
+        }
     }
     stamp(2);
     if (P.trace != nullptr && lane == 0) P.trace[(size_t)wg * 4 + 3] = (uint64_t)n_segments;
@@ -708,6 +713,11 @@ __device__ __forceinline__ void ldmatrix_x4_trans(uint32_t (&r)[4], const void* 
                  : "r"(smem_u32(p)));
 }
 
+// kSplit = false: one CTA per unit (residual attention, griddepcontrol.wait, merge).
+// kSplit = true (the residual kernel of launch_resid_merge): a persistent grid, CTA b attends the
+// residuals of units b, b + gridDim.x, ... and stores each unit's combined residual partial to
+// P.res_ml / P.res_o, then counts it on P.unit_cnt; merge_kernel does the rest.
+template <bool kSplit>
 __global__ void __launch_bounds__(kFinishThreads, 5) finish_kernel(const ResidualParams P, const int32_t* __restrict__ pref,
                                                                    const WorkerRanges wr) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -715,7 +725,11 @@ __global__ void __launch_bounds__(kFinishThreads, 5) finish_kernel(const Residua
     float (*wml)[2][kMaxG] = reinterpret_cast<float (*)[2][kMaxG]>(smem_raw + kFinishWarps * slot);
     const int tid = threadIdx.x, warp = tid >> 5, lane = lane_id();
     const int gid = lane >> 2, tig = lane & 3;
-    const int i = blockIdx.x;
+    // the next kernel may start its prologue on SMs this grid leaves free (the page kernel of the
+    // next layer reads nothing this kernel writes before its own griddepcontrol.wait; the merge
+    // kernel waits on the per-unit counters)
+    if (tid == 0) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    for (int i = blockIdx.x; i < P.n_units; i += kSplit ? gridDim.x : P.n_units) {
     const int u = P.unit_begin + i;
     const int d = kHeadDim;
     const int G = P.group;
@@ -743,7 +757,6 @@ __global__ void __launch_bounds__(kFinishThreads, 5) finish_kernel(const Residua
         }
     };
     fstamp(0);
-    if (tid == 0) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 
     // ---- residual attention (overlaps the page kernel): warp w owns tiles w, w + kFinishWarps, ... ----
     uint32_t qb[8][2];
@@ -932,6 +945,39 @@ __global__ void __launch_bounds__(kFinishThreads, 5) finish_kernel(const Residua
             if (early_build) P.meta[u].n_built = n >> 4;
         }
     }
+    if constexpr (kSplit) {
+        // combine the warps' residual partials into the unit's (online max over 4), store it,
+        // then count it: merge_kernel reads it once the unit's counter is complete
+        for (int e = tid; e < G * (d / 4); e += kFinishThreads) {
+            const int h = e / (d / 4), c4 = e % (d / 4);
+            float M = -INFINITY, L = 0.0f;
+            float4 a = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+            for (int w = 0; w < kFinishWarps; ++w) {
+                const float lw = wml[w][1][h];
+                if (lw > 0.0f) {
+                    const float mw = wml[w][0][h];
+                    const float nm = fmaxf(M, mw);
+                    const float f = fast_exp2(M - nm), sc = fast_exp2(mw - nm);
+                    const float4 wv = reinterpret_cast<const float4*>(smem_raw + w * slot)[h * (kHeadDim / 4) + c4];
+                    a.x = fmaf(wv.x, sc, a.x * f);
+                    a.y = fmaf(wv.y, sc, a.y * f);
+                    a.z = fmaf(wv.z, sc, a.z * f);
+                    a.w = fmaf(wv.w, sc, a.w * f);
+                    L = fmaf(lw, sc, L * f);
+                    M = nm;
+                }
+            }
+            reinterpret_cast<float4*>(P.res_o + ((size_t)u * kMaxG + h) * d)[c4] = a;
+            if (c4 == 0) {
+                P.res_ml[(size_t)u * 2 * kMaxG + h] = M;
+                P.res_ml[(size_t)u * 2 * kMaxG + kMaxG + h] = L;
+            }
+        }
+        __threadfence();
+        __syncthreads();  // (also: the next unit reuses the tiles and the warp partials)
+        if (tid == 0) atomicAdd(P.unit_cnt + u, 1);
+        fstamp(3);
+    } else {
     // ---- the page partials are complete past this point ----
     fstamp(1);
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
@@ -996,6 +1042,83 @@ __global__ void __launch_bounds__(kFinishThreads, 5) finish_kernel(const Residua
     }
     __syncthreads();
     fstamp(3);
+    }  // !kSplit
+    }  // units
+    // split: this grid completes after the page grid (the merge kernel's end wait chains on it)
+    if constexpr (kSplit) asm volatile("griddepcontrol.wait;\n" ::: "memory");
+}
+
+// Merge kernel of launch_resid_merge: one CTA per unit; waits until the unit's page segments and
+// its residual partial have been counted, merges them (as finish_kernel does), writes out and
+// resets the counter (its next increment comes from a kernel that waits for this grid).
+__global__ void __launch_bounds__(kFinishThreads) merge_kernel(const ResidualParams P, const int32_t* __restrict__ pref,
+                                                               const WorkerRanges wr) {
+    const int tid = threadIdx.x;
+    const int i = blockIdx.x, u = P.unit_begin + i;
+    const int d = kHeadDim, G = P.group;
+    if (tid == 0) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    const int upre = pref[i], uend = pref[i + 1];
+    const int w_first = uend > upre ? worker_of_batch(upre / wr.batch, wr.total_batches, wr.workers) : 0;
+    const int w_last = uend > upre ? worker_of_batch((uend - 1) / wr.batch, wr.total_batches, wr.workers) : -1;
+    const int n_part = w_last - w_first + 1;
+    if (tid == 0) {
+        const int want = n_part + 1;
+        int got;
+        for (;;) {
+            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(got) : "l"(P.unit_cnt + u) : "memory");
+            if (got >= want) break;
+            __nanosleep(128);
+        }
+    }
+    __syncthreads();
+    for (int e = tid; e < G * (d / 4); e += kFinishThreads) {
+        const int h = e / (d / 4), c4 = e % (d / 4);
+        float M = __ldcg(P.res_ml + (size_t)u * 2 * kMaxG + h), L = __ldcg(P.res_ml + (size_t)u * 2 * kMaxG + kMaxG + h);
+        float4 a = __ldcg(reinterpret_cast<const float4*>(P.res_o + ((size_t)u * kMaxG + h) * d) + c4);
+        if (!(L > 0.0f)) {
+            M = -INFINITY;
+            L = 0.0f;
+            a = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        }
+        for (int p0 = 0; p0 < n_part; p0 += kMergeBatch) {
+            float pm[kMergeBatch], pl[kMergeBatch];
+            float4 po[kMergeBatch];
+#pragma unroll
+            for (int k = 0; k < kMergeBatch; ++k) {
+                const int slot = w_first + p0 + k + i;
+                const bool ok = p0 + k < n_part;
+                pm[k] = ok ? __ldcg(P.part_ml + (size_t)slot * 2 * kMaxG + h) : -INFINITY;
+                pl[k] = ok ? __ldcg(P.part_ml + (size_t)slot * 2 * kMaxG + kMaxG + h) : 0.0f;
+                po[k] = ok ? __ldcg(reinterpret_cast<const float4*>(P.part_o + ((size_t)slot * kMaxG + h) * d) + c4)
+                           : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+            }
+            float cm = pm[0];
+#pragma unroll
+            for (int k = 1; k < kMergeBatch; ++k) cm = fmaxf(cm, pm[k]);
+            const float nm = fmaxf(M, cm);
+            const float f = fast_exp2(M - nm);
+            a.x *= f; a.y *= f; a.z *= f; a.w *= f; L *= f;
+#pragma unroll
+            for (int k = 0; k < kMergeBatch; ++k) {
+                const float sc = fast_exp2(pm[k] - nm);
+                a.x = fmaf(po[k].x, sc, a.x);
+                a.y = fmaf(po[k].y, sc, a.y);
+                a.z = fmaf(po[k].z, sc, a.z);
+                a.w = fmaf(po[k].w, sc, a.w);
+                L = fmaf(pl[k], sc, L);
+            }
+            M = nm;
+        }
+        const float li = 1.0f / L;
+        __half2* o2 = reinterpret_cast<__half2*>(P.out + ((size_t)i * G + h) * d) + 2 * c4;
+        o2[0] = __floats2half2_rn(a.x * li, a.y * li);
+        o2[1] = __floats2half2_rn(a.z * li, a.w * li);
+    }
+    __syncthreads();
+    if (tid == 0) P.unit_cnt[u] = 0;
+    // No griddepcontrol.wait: every write of the page and residual grids this call makes has been
+    // consumed through the counters, so the next kernel may start as soon as the merges are done
+    // (the residual grid's CTAs may still sit in their final wait for the page grid).
 }
 
 cudaError_t launch_finish(const ResidualParams& p, const int32_t* pref, WorkerRanges wr, bool after_pages,
@@ -1003,19 +1126,42 @@ cudaError_t launch_finish(const ResidualParams& p, const int32_t* pref, WorkerRa
     const size_t smem = finish_smem_bytes(p.fused_flush ? kFinishSlotFlush : kFinishSlot);
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(finish_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              finish_smem_bytes(kFinishSlotFlush));
-        if (e == cudaSuccess) e = set_carveout(reinterpret_cast<const void*>(finish_kernel));
+        if (e == cudaSuccess) e = set_carveout(reinterpret_cast<const void*>(finish_kernel<false>));
         if (e != cudaSuccess) return e;
         configured = true;
     }
     // PDL only behind a page kernel: a finish that follows another finish (no pages) reads
     // the n_res / residual rows that kernel writes, so it needs the full dependency
     if (!after_pages) {
-        finish_kernel<<<p.n_units, kFinishThreads, smem, s>>>(p, pref, wr);
+        finish_kernel<false><<<p.n_units, kFinishThreads, smem, s>>>(p, pref, wr);
         return cudaGetLastError();
     }
-    return launch_pdl(finish_kernel, dim3(p.n_units), dim3(kFinishThreads), smem, s, p, pref, wr);
+    return launch_pdl(finish_kernel<false>, dim3(p.n_units), dim3(kFinishThreads), smem, s, p, pref, wr);
+}
+
+cudaError_t launch_resid_merge(const ResidualParams& p, const int32_t* pref, WorkerRanges wr, bool after_pages,
+                               int resid_ctas, cudaStream_t s) {
+    const size_t smem = finish_smem_bytes(p.fused_flush ? kFinishSlotFlush : kFinishSlot);
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(finish_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             finish_smem_bytes(kFinishSlotFlush));
+        if (e == cudaSuccess) e = set_carveout(reinterpret_cast<const void*>(finish_kernel<true>));
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    const int grid = std::max(1, std::min(resid_ctas, p.n_units));
+    cudaError_t e;
+    if (!after_pages) {
+        finish_kernel<true><<<grid, kFinishThreads, smem, s>>>(p, pref, wr);
+        e = cudaGetLastError();
+    } else {
+        e = launch_pdl(finish_kernel<true>, dim3(grid), dim3(kFinishThreads), smem, s, p, pref, wr);
+    }
+    if (e != cudaSuccess) return e;
+    return launch_pdl(merge_kernel, dim3(p.n_units), dim3(kFinishThreads), 0, s, p, pref, wr);
 }
 
 }  // namespace mkv

@@ -73,6 +73,11 @@ struct ResidualParams {
     uint32_t* status;
     uint64_t* trace;      // diagnostics: per CTA {start, residual done, wait released, end}, or null
     int fused_flush;      // finish_kernel quantizes a residual block this append fills (no append_kernel)
+    // split finish (launch_resid_merge): per-unit arrival counters (page segments + the residual
+    // partial) and the residual partial of every unit, indexed by the global unit
+    int* unit_cnt;
+    float* res_ml;        // [total_units][2][kMaxG]
+    float* res_o;         // [total_units][kMaxG][d]
 };
 constexpr int kTraceFinishCtas = 8192;  // finish-kernel CTAs recorded per trace slot
 cudaError_t launch_append(const ResidualParams& p, cudaStream_t s);
@@ -88,6 +93,12 @@ struct AppendSegs {
 cudaError_t launch_append_segments(const ResidualParams& p, const AppendSegs& segs, cudaStream_t s);
 cudaError_t launch_finish(const ResidualParams& p, const int32_t* pref, WorkerRanges wr, bool after_pages,
                           cudaStream_t s);
+// The split form of launch_finish: a persistent residual kernel (resid_ctas CTAs, one beside each
+// page CTA: append + residual attention of every unit during the page pass, the residual partial
+// to global memory) and a merge kernel (one CTA per unit: waits on the unit's arrival counter,
+// merges, writes out), so the merges do not queue behind residual attention after the page pass.
+cudaError_t launch_resid_merge(const ResidualParams& p, const int32_t* pref, WorkerRanges wr, bool after_pages,
+                               int resid_ctas, cudaStream_t s);
 
 // Per-unit page-run record of a K4 plan (host-computed from the cache mirror).
 struct UnitRec {
@@ -125,6 +136,7 @@ struct PagesParams {
     float scale_log2;
     uint64_t* trace;        // diagnostics: per warp {start, after wait, done} (globaltimer), or null
     int early;              // q may be read before griddepcontrol.wait (see pages_kernel)
+    int* unit_cnt;          // split finish: +1 per (warp, unit) segment whose partial is written, or null
 };
 constexpr int kMaxPagesWarps = 12;  // partial-slot sizing
 // pages_tc_kernel trace (MKV_DECODE_TRACE): per worker, batches 4..7: 8 stamps of compute warp 0,

@@ -81,6 +81,13 @@ def test_decode_many_units_split(mkv):
     assert worst <= TOL
 
 
+def test_decode_more_units_than_sms(mkv):
+    # more units per call than SMs: the default finish step is the split form (persistent
+    # residual kernel + merge kernel on per-unit arrival counters), through a flush (n_r = 16)
+    worst = run_decode(mkv, n_units=300, G=4, L=700, hh=160, rw=64, steps=20, n_r=16, check_every=6)
+    assert worst <= TOL
+
+
 def test_decode_small_n_r(mkv):
     worst = run_decode(mkv, n_units=2, G=2, L=200, hh=20, rw=20, steps=70, n_r=32, check_every=5)
     assert worst <= TOL
@@ -364,15 +371,19 @@ def test_decode_headline_shape_parity(mkv):
     assert worst <= TOL, worst
 
 
-@pytest.mark.parametrize("env", [{"MKV_PAGES_IMPL": "tc"}, {"MKV_FLUSH": "fused"}, {"MKV_LAYERS_SPLIT": "1"}],
-                         ids=["tcgen05-page-pass", "fused-flush", "layers-split"])
+@pytest.mark.parametrize("env", [{"MKV_PAGES_IMPL": "tc"}, {"MKV_FLUSH": "fused"}, {"MKV_LAYERS_SPLIT": "1"},
+                                 {"MKV_MERGE": "split"}, {"MKV_MERGE": "finish"}],
+                         ids=["tcgen05-page-pass", "fused-flush", "layers-split", "split-finish", "one-kernel-finish"])
 def test_decode_variant_parity(env):
     """The decode variants kept as measured A/Bs pass the same oracle parity tests (G = 1 / 4 / 8,
     flushes, partial pages, split units, the headline shape, bit-identity of the multi-layer
     call): MKV_PAGES_IMPL=tc -- the tcgen05 page pass (decode_tc.cu: codes -> TMEM,
     tcgen05.mma with per-page scaled B operands); MKV_FLUSH=fused -- the residual flush done by
     the finish kernel of the step that fills the block (pages built there, the block attended
-    dequantized, the next plan uploaded off the critical path)."""
+    dequantized, the next plan uploaded off the critical path); MKV_MERGE=split / finish -- the
+    finish step forced into its two-kernel form (persistent residual kernel + merge kernel on
+    per-unit arrival counters) or its one-kernel form for every call size (the default picks by
+    unit count, so the small suite cases would otherwise only see the one-kernel form)."""
     import os
     import subprocess
     import sys
