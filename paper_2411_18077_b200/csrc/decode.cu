@@ -1051,6 +1051,10 @@ __global__ void __launch_bounds__(kFinishThreads, 5) finish_kernel(const Residua
 // Merge kernel of launch_resid_merge: one CTA per unit; waits until the unit's page segments and
 // its residual partial have been counted, merges them (as finish_kernel does), writes out and
 // resets the counter (its next increment comes from a kernel that waits for this grid).
+// kB page partials per L2 round trip: 12 for calls whose units spread over many page warps, 4
+// when units outnumber the page warps (~1-2 partials per unit; fewer registers, more resident
+// merge CTAs for the merge wave after the page pass).
+template <int kB>
 __global__ void __launch_bounds__(kFinishThreads) merge_kernel(const ResidualParams P, const int32_t* __restrict__ pref,
                                                                const WorkerRanges wr) {
     const int tid = threadIdx.x;
@@ -1080,11 +1084,11 @@ __global__ void __launch_bounds__(kFinishThreads) merge_kernel(const ResidualPar
             L = 0.0f;
             a = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
         }
-        for (int p0 = 0; p0 < n_part; p0 += kMergeBatch) {
-            float pm[kMergeBatch], pl[kMergeBatch];
-            float4 po[kMergeBatch];
+        for (int p0 = 0; p0 < n_part; p0 += kB) {
+            float pm[kB], pl[kB];
+            float4 po[kB];
 #pragma unroll
-            for (int k = 0; k < kMergeBatch; ++k) {
+            for (int k = 0; k < kB; ++k) {
                 const int slot = w_first + p0 + k + i;
                 const bool ok = p0 + k < n_part;
                 pm[k] = ok ? __ldcg(P.part_ml + (size_t)slot * 2 * kMaxG + h) : -INFINITY;
@@ -1094,12 +1098,12 @@ __global__ void __launch_bounds__(kFinishThreads) merge_kernel(const ResidualPar
             }
             float cm = pm[0];
 #pragma unroll
-            for (int k = 1; k < kMergeBatch; ++k) cm = fmaxf(cm, pm[k]);
+            for (int k = 1; k < kB; ++k) cm = fmaxf(cm, pm[k]);
             const float nm = fmaxf(M, cm);
             const float f = fast_exp2(M - nm);
             a.x *= f; a.y *= f; a.z *= f; a.w *= f; L *= f;
 #pragma unroll
-            for (int k = 0; k < kMergeBatch; ++k) {
+            for (int k = 0; k < kB; ++k) {
                 const float sc = fast_exp2(pm[k] - nm);
                 a.x = fmaf(po[k].x, sc, a.x);
                 a.y = fmaf(po[k].y, sc, a.y);
@@ -1161,7 +1165,9 @@ cudaError_t launch_resid_merge(const ResidualParams& p, const int32_t* pref, Wor
         e = launch_pdl(finish_kernel<true>, dim3(grid), dim3(kFinishThreads), smem, s, p, pref, wr);
     }
     if (e != cudaSuccess) return e;
-    return launch_pdl(merge_kernel, dim3(p.n_units), dim3(kFinishThreads), 0, s, p, pref, wr);
+    if (p.n_units >= 2 * wr.workers)
+        return launch_pdl(merge_kernel<4>, dim3(p.n_units), dim3(kFinishThreads), 0, s, p, pref, wr);
+    return launch_pdl(merge_kernel<kMergeBatch>, dim3(p.n_units), dim3(kFinishThreads), 0, s, p, pref, wr);
 }
 
 }  // namespace mkv
