@@ -440,10 +440,12 @@ __global__ void __maxnreg__(208) pages_kernel(const PagesParams P) {
                 po[h1 * kHeadDim + c + 8] = fmaf(O[g][3], f, dv1);
             }
         }
-        if (P.unit_cnt != nullptr) {  // split finish: this segment's partial is visible, then counted
-            __threadfence();
+        if (P.unit_cnt != nullptr) {  // split finish: count this segment's partial
+            // bar.warp.sync orders every lane's partial stores before lane 0's release add
+            // (release is cumulative); merge_kernel acquires the counter before reading them
             __syncwarp();
-            if (lane == 0) atomicAdd(P.unit_cnt + P.unit_begin + unit, 1);
+            if (lane == 0)
+                asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(P.unit_cnt + P.unit_begin + unit) : "memory");
         }
     }
     stamp(2);
