@@ -236,8 +236,12 @@ int mkv_decode_step_layers(mkv_cache* cache, int n_layers, const mkv_decode_args
  * (minikv_cli.cpp:180-201, pipeline.cpp:199-215: decode_step per step, cache_engine.cpp:100-138)
  * in one FFI crossing.  Step s reads q + s * q_step, k_new + s * kv_step, v_new + s * kv_step
  * and writes out + s * out_step (strides in fp16 ELEMENTS; k_new / v_new may be null: attend
- * only).  Bit-identical to n_steps mkv_decode_step calls; every step's inputs must be written
- * before the call. */
+ * only).  Every step's inputs must be written before the call.  Few short units (at most one
+ * per SM, <= 1024 pages each by the last step) are served by one launch that keeps each unit on
+ * one CTA for all the steps: outputs equal n_steps mkv_decode_step calls up to the fp32
+ * accumulation order of a different split of the pages, the cache state bit for bit; other
+ * calls run the per-step kernels and are bit-identical to mkv_decode_step calls
+ * (MKV_STEPS=off forces that path). */
 typedef struct {
     int unit_begin, n_units, group, n_steps;
     const void* q;              /* fp16, step s at q + s * q_step: [n_units, G, d] */

@@ -908,11 +908,74 @@ int mkv_decode_step(mkv_cache* c, const mkv_decode_args* a, void* stream) {
     return decode_impl(c, a, true, static_cast<cudaStream_t>(stream));
 }
 
+// The unit-resident steps kernel (one CTA per unit for all steps, decode.cu steps_kernel) serves
+// a decode_steps call when its units fit one CTA each and are short: at most one unit per SM and
+// at most kStepsMaxPages pages per unit by the last step.  MKV_STEPS=off keeps the per-step
+// kernels (page pass + finish per step), MKV_STEPS=on ignores the size limits.
+constexpr int kStepsMaxPages = 1024;
+static int steps_mode() {
+    static const int m = [] {
+        const char* e = getenv("MKV_STEPS");
+        if (!e) return 1;
+        return e[1] == 'f' ? 0 : (e[1] == 'n' ? 2 : 1);
+    }();
+    return m;
+}
+// validates every step up front (the per-step path checks each step as it goes) and, if the
+// steps kernel serves the call, launches it and moves the host mirror through the same appends
+static int decode_steps_resident(mkv_cache* c, const mkv_decode_steps_args* a, cudaStream_t s, bool* done) {
+    *done = false;
+    const int mode = steps_mode();
+    const int ub = a->unit_begin, n = a->n_units;
+    if (mode == 0 || n <= 0 || a->n_steps == 0 || n > num_sms() || check_range(c, ub, n) != MKV_OK) return MKV_OK;
+    if (a->group < 1 || a->group > kMaxG || !a->q || !a->out) return MKV_OK;  // the per-step path reports it
+    const bool append = a->k_new != nullptr;
+    if (!aligned16(a->q) || !aligned16(a->out) || a->q_step % 8 || a->out_step % 8 ||
+        (append && (!aligned16(a->k_new) || !aligned16(a->v_new) || a->kv_step % 8)))
+        return MKV_OK;
+    const int npg = c->n_r / kGroup;
+    for (int i = 0; i < n; ++i) {
+        const int u = ub + i;
+        if ((int64_t)c->n_pages[u] + c->n_res[u] == 0 && !append) return MKV_OK;
+        const int64_t flushes = append ? (c->n_res[u] + (int64_t)a->n_steps) / c->n_r : 0;
+        const int64_t pages = c->n_pages[u] + flushes * npg;
+        if (pages > c->cap_pages[u]) return MKV_OK;  // the per-step path fails at the right step
+        if (mode == 1 && pages > kStepsMaxPages) return MKV_OK;
+    }
+    if (int r = require_device()) return r;
+    StepsParams sp;
+    sp.meta = c->d_meta; sp.unit_begin = ub; sp.n_units = n; sp.group = a->group; sp.n_r = c->n_r;
+    sp.n_steps = a->n_steps;
+    sp.q = static_cast<const __half*>(a->q); sp.q_step = a->q_step;
+    sp.k_new = static_cast<const __half*>(a->k_new); sp.v_new = static_cast<const __half*>(a->v_new);
+    sp.kv_step = a->kv_step;
+    sp.out = static_cast<__half*>(a->out); sp.out_step = a->out_step;
+    sp.res_k = c->d_res_k; sp.res_v = c->d_res_v; sp.pool = c->d_pool; sp.shadow = c->d_shadow;
+    sp.scale_log2 = a->scale * 1.4426950408889634f;
+    sp.status = c->d_status;
+    CK(launch_steps(sp, s));
+    if (append)
+        for (int i = 0; i < n; ++i) {
+            const int u = ub + i;
+            const int64_t tot = (int64_t)c->n_res[u] + a->n_steps;
+            c->n_pages[u] += (int)(tot / c->n_r) * npg;
+            c->n_blocks[u] += (int)(tot / c->n_r);
+            c->n_res[u] = (int)(tot % c->n_r);
+        }
+    *done = true;
+    return MKV_OK;
+}
+
 int mkv_decode_steps(mkv_cache* c, const mkv_decode_steps_args* a, void* stream) {
     if (!a) return fail(MKV_ERR_INVALID_ARGUMENT, "decode_steps: null args");
     if (a->n_steps < 0) return fail(MKV_ERR_INVALID_ARGUMENT, "decode_steps: negative step count");
     if ((a->k_new == nullptr) != (a->v_new == nullptr)) return fail(MKV_ERR_INVALID_ARGUMENT, "decode_append: null v");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    {
+        bool done = false;
+        if (int r = decode_steps_resident(c, a, s, &done)) return r;
+        if (done) return MKV_OK;
+    }
     auto at = [](const void* base, int64_t elems) -> const void* {
         return base ? static_cast<const __half*>(base) + elems : nullptr;
     };

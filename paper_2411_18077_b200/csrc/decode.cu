@@ -1172,4 +1172,383 @@ cudaError_t launch_resid_merge(const ResidualParams& p, const int32_t* pref, Wor
     return launch_pdl(merge_kernel<kMergeBatch>, dim3(p.n_units), dim3(kFinishThreads), 0, s, p, pref, wr);
 }
 
+
+// ---------------------------------------------------------------------------
+// steps kernel: a prepared token stream's decode steps for few, short units in ONE launch
+// ---------------------------------------------------------------------------
+// mkv_decode_steps over few units with few pages (configs[0]: 8 units of ~60 pages, 256 steps)
+// is latency-bound as two kernels per step (~17 us a step).  Here one CTA owns one unit for all
+// the steps: per step it appends the token (quantizing the n_r block into pages with the K3
+// builder when it fills: store_block, cache_engine.cpp:34-52,79-90), attends its pages (8 warps,
+// contiguous 4-page batches each, the page kernel's batch arithmetic: same subnormal
+// dequantization, folded scales and zero-point mmas) and then its residual tiles in the same
+// online softmax, merges the 8 warp partials in shared memory and writes the step's output
+// (decode_step, cache_engine.cpp:100-138).  Units are independent: no grid synchronization.
+constexpr int kStepsWarps = 8;
+constexpr int kStepsThreads = kStepsWarps * 32;
+constexpr int kStepsRing = 2 * kBatch * kPageBytes;  // per warp: 2 stages of one 4-page batch (16 KB)
+static_assert(kStepsRing >= (int)sizeof(PageRows), "ring doubles as the residual tile / flush row buffer");
+constexpr size_t kStepsSmem = (size_t)kStepsWarps * (kStepsRing + sizeof(PageParams)) + kQBytes +
+                              (size_t)kStepsWarps * (2 * kMaxG + kMaxG * kHeadDim) * sizeof(float) + 64;
+
+__global__ void __launch_bounds__(kStepsThreads, 1) steps_kernel(const StepsParams P) {
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = lane_id();
+    const int gid = lane >> 2, tig = lane & 3;
+    const int i = blockIdx.x, u = P.unit_begin + i;
+    const int d = kHeadDim, G = P.group;
+    uint8_t* ring = smem_raw + (size_t)warp * kStepsRing;
+    PageParams& prm = reinterpret_cast<PageParams*>(smem_raw + (size_t)kStepsWarps * kStepsRing)[warp];
+    __half* qsm = reinterpret_cast<__half*>(smem_raw + (size_t)kStepsWarps * (kStepsRing + sizeof(PageParams)));
+    float* parts = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(qsm) + kQBytes);  // [warp][2][kMaxG] then o
+    float (*pml)[2][kMaxG] = reinterpret_cast<float (*)[2][kMaxG]>(parts);
+    float* po_all = parts + kStepsWarps * 2 * kMaxG;  // [warp][kMaxG][d]
+    const UnitMeta meta0 = P.meta[u];
+    const int64_t page_base = meta0.page_base;
+    int n_pages = meta0.n_pages, n_res = meta0.n_res, n_built = meta0.n_built;
+    const int n_prefill = meta0.n_prefill;
+    const int partial_page = (n_prefill & 15) ? ((n_prefill + 15) >> 4) - 1 : -1;
+    const int partial_valid = n_prefill & 15;
+    __half* rk = P.res_k + (size_t)u * P.n_r * d;
+    __half* rv = P.res_v + (size_t)u * P.n_r * d;
+    const float sl2 = P.scale_log2;
+    const float sk = kTwo24 * sl2;
+    const int h0 = 2 * tig, h1 = 2 * tig + 1;
+    // stale ring slots past a short batch must hold finite values (masked by selects)
+    for (int e = lane; e < kStepsRing / 16; e += 32) reinterpret_cast<uint4*>(ring)[e] = make_uint4(0, 0, 0, 0);
+    bool ok = true;
+
+    auto load_batch = [&](int b, int stage) {
+        const int n = min(kBatch, n_pages - kBatch * b);
+        const uint8_t* src = P.pool + (size_t)(page_base + kBatch * b) * kPageBytes;
+        uint8_t* dst = ring + (size_t)stage * kBatch * kPageBytes;
+        for (int e = lane; e < n * kPageBytes / 16; e += 32) cp_async16(dst + 16 * e, src + 16 * e);
+        cp_async_commit();
+    };
+    for (int st = 0; st < P.n_steps; ++st) {
+        // the warp's first page batch is requested before the append unless this step flushes
+        // (then the new pages are built first): its latency overlaps the q / token loads
+        const bool flushes = P.k_new != nullptr && n_res + 1 == P.n_r;
+        int nb = (n_pages + kBatch - 1) / kBatch;
+        int b0 = (int)(((int64_t)warp * nb) / kStepsWarps), b1 = (int)(((int64_t)(warp + 1) * nb) / kStepsWarps);
+        if (!flushes && b0 < b1) load_batch(b0, 0);
+        const __half* q = P.q + (size_t)st * P.q_step + (size_t)i * G * d;
+        for (int e = tid; e < G * d / 8; e += kStepsThreads)
+            reinterpret_cast<uint4*>(qsm)[e] = __ldg(reinterpret_cast<const uint4*>(q) + e);
+        // ---- decode_append (+ store_block of a full residual block) ----
+        if (P.k_new != nullptr) {
+            if (tid < 16)
+                reinterpret_cast<uint4*>(rk + (size_t)n_res * d)[tid] =
+                    __ldg(reinterpret_cast<const uint4*>(P.k_new + (size_t)st * P.kv_step + (size_t)i * d) + tid);
+            else if (tid < 32)
+                reinterpret_cast<uint4*>(rv + (size_t)n_res * d)[tid - 16] =
+                    __ldg(reinterpret_cast<const uint4*>(P.v_new + (size_t)st * P.kv_step + (size_t)i * d) + tid - 16);
+            ++n_res;
+            if (n_res == P.n_r) {
+                __threadfence();  // the rows are read back through L2 (cp.async.cg)
+                __syncthreads();
+                PageRows& rows = *reinterpret_cast<PageRows*>(ring);
+                for (int j = warp + n_built; j < P.n_r / kGroup; j += kStepsWarps) {
+                    stage_rows_contig(rows, rk + (size_t)16 * j * d, rv + (size_t)16 * j * d);
+                    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+                    __syncwarp();
+                    const int64_t page = page_base + n_pages + j;
+                    ok &= build_page_staged(rows, prm, 16, P.pool + (size_t)page * kPageBytes,
+                                            P.shadow ? P.shadow + (size_t)page * (kShadowBytes / 4) : nullptr);
+                    __syncwarp();
+                }
+                for (int e = lane; e < kStepsRing / 16; e += 32) reinterpret_cast<uint4*>(ring)[e] = make_uint4(0, 0, 0, 0);
+                n_pages += P.n_r / kGroup;
+                n_res = 0;
+                n_built = 0;
+            }
+        }
+        __threadfence();  // pages / residual row written above are read back through L2 below
+        __syncthreads();
+
+        // ---- q fragments (as pages_kernel: scales folded in, K-bias copy carries the softmax scale) ----
+        uint32_t qb[8][2], qsc[8][2];
+        load_q_frags(qsm, G, gid, tig, qb, qsc);
+        uint32_t qa[8][4];
+        {
+            const uint32_t s2 = pack_half2(sl2, sl2);
+#pragma unroll
+            for (int kc = 0; kc < 8; ++kc) {
+                qa[kc][0] = hmul2_u32(qb[kc][0], s2); qa[kc][1] = 0u;
+                qa[kc][2] = hmul2_u32(qb[kc][1], s2); qa[kc][3] = 0u;
+            }
+        }
+        float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.0f, l1 = 0.0f;
+        float O[8][4];
+#pragma unroll
+        for (int g = 0; g < 8; ++g) O[g][0] = O[g][1] = O[g][2] = O[g][3] = 0.0f;
+        float Dvb[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+
+        // ---- this warp's pages: batches [b0, b1) of the unit's ceil(n_pages / 4) ----
+        if (flushes) {
+            nb = (n_pages + kBatch - 1) / kBatch;
+            b0 = (int)(((int64_t)warp * nb) / kStepsWarps);
+            b1 = (int)(((int64_t)(warp + 1) * nb) / kStepsWarps);
+            if (b0 < b1) load_batch(b0, 0);
+        }
+        for (int b = b0; b < b1; ++b) {
+            const int stage = (b - b0) & 1;
+            if (b + 1 < b1) {
+                load_batch(b + 1, stage ^ 1);
+                asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+            } else {
+                asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+            }
+            __syncwarp();
+            const uint8_t* buf = ring + (size_t)stage * kBatch * kPageBytes;
+            const int n = min(kBatch, n_pages - kBatch * b);
+            const int pfirst = kBatch * b;
+            float S[kBatch][4];
+            uint4 kw[kBatch];
+#pragma unroll
+            for (int j = 0; j < kBatch; ++j) {
+                kw[j] = lds128(buf + j * kPageBytes + kKC + lane * 16);
+                S[j][0] = S[j][1] = S[j][2] = S[j][3] = 0.0f;
+            }
+#pragma unroll
+            for (int kc = 0; kc < 8; ++kc) {
+                const int sh = code_shift(kc);
+                const uint32_t mask = 0x00030003u << (2 * code_class(kc));
+#pragma unroll
+                for (int j = 0; j < kBatch; ++j) {
+                    const uint2 ks = lds64(buf + j * kPageBytes + kKS + ((kc >> 1) * 4 + tig) * 16 + (kc & 1) * 8);
+                    const uint32_t a[4] = {(kw[j].x >> sh) & mask, (kw[j].y >> sh) & mask,
+                                           (kw[j].z >> sh) & mask, (kw[j].w >> sh) & mask};
+                    mma_16816(S[j], a, hmul2_u32(qsc[kc][0], ks.x), hmul2_u32(qsc[kc][1], ks.y));
+                }
+            }
+            float Kb[4] = {0.0f, 0.0f, 0.0f, 0.0f}, Kb2[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+            {
+                uint4 z[4];
+                const uint8_t* zp = buf + (gid & (kBatch - 1)) * kPageBytes + kKZ + tig * 16;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) z[j] = lds128(zp + 64 * j);
+                const uint32_t* zz = reinterpret_cast<const uint32_t*>(z);
+#pragma unroll
+                for (int kc = 0; kc < 8; kc += 2) {
+                    mma_16816(Kb, qa[kc], zz[2 * kc], zz[2 * kc + 1]);
+                    mma_16816(Kb2, qa[kc + 1], zz[2 * kc + 2], zz[2 * kc + 3]);
+                }
+                Kb[0] += Kb2[0];
+                Kb[1] += Kb2[1];
+            }
+            const bool special = (n < kBatch) || (partial_page >= pfirst && partial_page < pfirst + n);
+            float x[kBatch][4];
+            float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+            for (int j = 0; j < kBatch; ++j) {
+                const float kb0 = __shfl_sync(0xffffffffu, Kb[j & 1], 8 * tig + (j >> 1));
+                const float kb1 = __shfl_sync(0xffffffffu, Kb[j & 1], 8 * tig + 4 + (j >> 1));
+                x[j][0] = fmaf(S[j][0], sk, kb0);
+                x[j][1] = fmaf(S[j][1], sk, kb1);
+                x[j][2] = fmaf(S[j][2], sk, kb0);
+                x[j][3] = fmaf(S[j][3], sk, kb1);
+            }
+            if (special) {
+#pragma unroll
+                for (int j = 0; j < kBatch; ++j) {
+                    const int lp = pfirst + j;
+                    const int valid = (j >= n) ? 0 : ((lp == partial_page) ? partial_valid : 16);
+                    if (gid >= valid) { x[j][0] = -INFINITY; x[j][1] = -INFINITY; }
+                    if (gid + 8 >= valid) { x[j][2] = -INFINITY; x[j][3] = -INFINITY; }
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < kBatch; ++j) {
+                mx0 = fmaxf(mx0, fmaxf(x[j][0], x[j][2]));
+                mx1 = fmaxf(mx1, fmaxf(x[j][1], x[j][3]));
+            }
+#pragma unroll
+            for (int o = 4; o < 32; o <<= 1) {
+                mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
+                mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
+            }
+            const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+            if (__any_sync(0xffffffffu, (mn0 > m0 + kLazy) | (mn1 > m1 + kLazy))) {
+                const float a0 = fast_exp2(m0 - mn0), a1 = fast_exp2(m1 - mn1);
+                l0 *= a0; l1 *= a1;
+#pragma unroll
+                for (int g = 0; g < 8; ++g) {
+                    O[g][0] *= a0; O[g][1] *= a1; O[g][2] *= a0; O[g][3] *= a1;
+                }
+                Dvb[0] *= a0; Dvb[1] *= a1;
+                m0 = mn0; m1 = mn1;
+            }
+            uint32_t pb0[kBatch], pb1[kBatch];
+#pragma unroll
+            for (int j = 0; j < kBatch; ++j) {
+                const float p0 = fast_exp2(x[j][0] - m0), p1 = fast_exp2(x[j][1] - m1);
+                const float p2 = fast_exp2(x[j][2] - m0), p3 = fast_exp2(x[j][3] - m1);
+                l0 += p0 + p2;
+                l1 += p1 + p3;
+                pb0[j] = movmatrix_trans(pack_half2(p0, p1));
+                pb1[j] = movmatrix_trans(pack_half2(p2, p3));
+            }
+#pragma unroll
+            for (int j = 0; j < kBatch; ++j) {
+                const uint8_t* page = buf + j * kPageBytes;
+                const uint2 vz = lds64(page + kVZ + lane * 8);
+                const uint32_t az[4] = {vz.x, 0u, vz.y, 0u};
+                mma_16816(Dvb, az, pb0[j], pb1[j]);
+                const uint4 vw = lds128(page + kVC + lane * 16);
+#pragma unroll
+                for (int g = 0; g < 8; ++g) {
+                    const int sh = code_shift(g);
+                    const uint32_t mask = 0x00030003u << (2 * code_class(g));
+                    const uint2 vs = lds64(page + kVS + ((g >> 1) * 4 + tig) * 16 + (g & 1) * 8);
+                    const uint32_t a[4] = {(vw.x >> sh) & mask, (vw.y >> sh) & mask, (vw.z >> sh) & mask,
+                                           (vw.w >> sh) & mask};
+                    mma_16816(O[g], a, hmul2_u32(pb0[j], vs.x), hmul2_u32(pb1[j], vs.y));
+                }
+            }
+            __syncwarp();
+        }
+        // page partial -> plain (m, l, o[c][h]) form: o = O * 2^24 * 4^s + value zero-point bias
+        // (Dvb[g][h] of lane 4 g + tig); l summed over the lane quads below
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+            const float dv0 = __shfl_sync(0xffffffffu, Dvb[0], 4 * g + tig);
+            const float dv1 = __shfl_sync(0xffffffffu, Dvb[1], 4 * g + tig);
+            const float f = extract_scale(g);
+            O[g][0] = fmaf(O[g][0], f, dv0);
+            O[g][2] = fmaf(O[g][2], f, dv0);
+            O[g][1] = fmaf(O[g][1], f, dv1);
+            O[g][3] = fmaf(O[g][3], f, dv1);
+        }
+#pragma unroll
+        for (int o = 4; o < 32; o <<= 1) {
+            l0 += __shfl_xor_sync(0xffffffffu, l0, o);
+            l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+        }
+
+        // ---- residual tiles (exact fp16 attention, as finish_kernel), same online softmax ----
+        // tile t goes to warp kStepsWarps - 1 - t % kStepsWarps (the page ranges differ by <= 1 batch)
+        for (int t = kStepsWarps - 1 - warp; 16 * t < n_res; t += kStepsWarps) {
+            const int nrows = min(16, n_res - 16 * t);
+            uint8_t* tile = ring;  // this warp's page batches are done: its ring holds the tile
+            for (int e = lane; e < 256; e += 32) {
+                const int r = e >> 4, cc = e & 15;
+                const int off = r * 256 + ((cc ^ (r & 7)) << 4);
+                if (r < nrows) {
+                    cp_async16(tile + off, rk + (size_t)(16 * t + r) * d + cc * 8);
+                    cp_async16(tile + 4096 + off, rv + (size_t)(16 * t + r) * d + cc * 8);
+                } else {  // rows past the residual are multiplied by p = 0: keep them finite
+                    *reinterpret_cast<uint4*>(tile + off) = make_uint4(0, 0, 0, 0);
+                    *reinterpret_cast<uint4*>(tile + 4096 + off) = make_uint4(0, 0, 0, 0);
+                }
+            }
+            cp_async_commit();
+            cp_async_wait_all();
+            __syncwarp();
+            float Sx[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+            for (int kc = 0; kc < 8; ++kc) {
+                uint32_t a[4];
+                a[0] = *reinterpret_cast<const uint32_t*>(tile + gid * 256 + (((2 * kc) ^ gid) << 4) + 4 * tig);
+                a[1] = *reinterpret_cast<const uint32_t*>(tile + (gid + 8) * 256 + (((2 * kc) ^ gid) << 4) + 4 * tig);
+                a[2] = *reinterpret_cast<const uint32_t*>(tile + gid * 256 + (((2 * kc + 1) ^ gid) << 4) + 4 * tig);
+                a[3] = *reinterpret_cast<const uint32_t*>(tile + (gid + 8) * 256 + (((2 * kc + 1) ^ gid) << 4) + 4 * tig);
+                mma_16816(Sx, a, qb[kc][0], qb[kc][1]);
+            }
+            float x0 = Sx[0] * sl2, x1 = Sx[1] * sl2, x2 = Sx[2] * sl2, x3 = Sx[3] * sl2;
+            if (gid >= nrows) { x0 = -INFINITY; x1 = -INFINITY; }
+            if (gid + 8 >= nrows) { x2 = -INFINITY; x3 = -INFINITY; }
+            float mx0 = fmaxf(x0, x2), mx1 = fmaxf(x1, x3);
+#pragma unroll
+            for (int o = 4; o < 32; o <<= 1) {
+                mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
+                mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
+            }
+            const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+            const float a0 = fast_exp2(m0 - mn0), a1 = fast_exp2(m1 - mn1);
+            m0 = mn0; m1 = mn1;
+            l0 *= a0; l1 *= a1;
+#pragma unroll
+            for (int g = 0; g < 8; ++g) { O[g][0] *= a0; O[g][1] *= a1; O[g][2] *= a0; O[g][3] *= a1; }
+            const float p0 = fast_exp2(x0 - m0), p1 = fast_exp2(x1 - m1);
+            const float p2 = fast_exp2(x2 - m0), p3 = fast_exp2(x3 - m1);
+            float ls0 = p0 + p2, ls1 = p1 + p3;
+#pragma unroll
+            for (int o = 4; o < 32; o <<= 1) {  // l is kept quad-reduced in this phase
+                ls0 += __shfl_xor_sync(0xffffffffu, ls0, o);
+                ls1 += __shfl_xor_sync(0xffffffffu, ls1, o);
+            }
+            l0 += ls0;
+            l1 += ls1;
+            const uint32_t pb0 = movmatrix_trans(pack_half2(p0, p1));
+            const uint32_t pb1 = movmatrix_trans(pack_half2(p2, p3));
+            const int mi = lane >> 3, ri = lane & 7;
+            const int vr = ri + 8 * (mi >> 1);
+#pragma unroll
+            for (int g = 0; g < 8; ++g) {
+                uint32_t a[4];
+                ldmatrix_x4_trans(a, tile + 4096 + vr * 256 + ((((2 * g) + (mi & 1)) ^ (vr & 7)) << 4));
+                mma_16816(O[g], a, pb0, pb1);
+            }
+            __syncwarp();
+        }
+
+        // ---- warp partial -> shared memory, merge of the 8 partials, out ----
+        float* wo = po_all + (size_t)warp * kMaxG * d;
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+            const int c = 16 * g + gid;
+            if (h0 < G) { wo[h0 * d + c] = O[g][0]; wo[h0 * d + c + 8] = O[g][2]; }
+            if (h1 < G) { wo[h1 * d + c] = O[g][1]; wo[h1 * d + c + 8] = O[g][3]; }
+        }
+        if (gid == 0) {
+            if (h0 < G) { pml[warp][0][h0] = m0; pml[warp][1][h0] = l0; }
+            if (h1 < G) { pml[warp][0][h1] = m1; pml[warp][1][h1] = l1; }
+        }
+        __syncthreads();
+        for (int e = tid; e < G * (d / 4); e += kStepsThreads) {
+            const int h = e / (d / 4), c4 = e % (d / 4);
+            float M = -INFINITY, L = 0.0f;
+            float4 a = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+            for (int w = 0; w < kStepsWarps; ++w) {
+                const float lw = pml[w][1][h];
+                if (lw > 0.0f) {
+                    const float mw = pml[w][0][h];
+                    const float nm = fmaxf(M, mw);
+                    const float f = fast_exp2(M - nm), sc = fast_exp2(mw - nm);
+                    const float4 wv = reinterpret_cast<const float4*>(po_all + ((size_t)w * kMaxG + h) * d)[c4];
+                    a.x = fmaf(wv.x, sc, a.x * f);
+                    a.y = fmaf(wv.y, sc, a.y * f);
+                    a.z = fmaf(wv.z, sc, a.z * f);
+                    a.w = fmaf(wv.w, sc, a.w * f);
+                    L = fmaf(lw, sc, L * f);
+                    M = nm;
+                }
+            }
+            const float li = 1.0f / L;
+            __half2* o2 = reinterpret_cast<__half2*>(P.out + (size_t)st * P.out_step + ((size_t)i * G + h) * d) + 2 * c4;
+            o2[0] = __floats2half2_rn(a.x * li, a.y * li);
+            o2[1] = __floats2half2_rn(a.z * li, a.w * li);
+        }
+        __syncthreads();  // partials / q staging are reused by the next step
+    }
+    if (!ok && lane == 0) atomicOr(P.status, kStatusNonFinite);
+    if (tid == 0) {
+        P.meta[u].n_pages = n_pages;
+        P.meta[u].n_res = n_res;
+        P.meta[u].n_built = n_built;
+    }
+}
+
+cudaError_t launch_steps(const StepsParams& p, cudaStream_t s) {
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(steps_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStepsSmem);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    steps_kernel<<<p.n_units, kStepsThreads, kStepsSmem, s>>>(p);
+    return cudaGetLastError();
+}
+
 }  // namespace mkv

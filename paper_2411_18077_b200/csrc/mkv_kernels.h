@@ -151,6 +151,26 @@ PagesConfig pages_config();
 // pdl = false: a full stream dependency (the previous kernel wrote the plan this kernel reads
 // before its griddepcontrol.wait, e.g. plan_build_kernel on a fused flush step)
 cudaError_t launch_pages(const PagesParams& p, int grid, cudaStream_t s, bool pdl = true);
+// A prepared token stream's decode steps, one CTA per unit for all steps (few short units:
+// mkv_decode_steps picks it when every unit's pages fit one CTA's share; see steps_kernel).
+struct StepsParams {
+    UnitMeta* meta;
+    int unit_begin, n_units, group, n_r, n_steps;
+    const __half* q;          // step st, unit i, head h: q + st * q_step + (i * G + h) * d
+    int64_t q_step;
+    const __half* k_new;      // step st, unit i: k_new + st * kv_step + i * d (null: attend only)
+    const __half* v_new;
+    int64_t kv_step;
+    __half* out;              // like q
+    int64_t out_step;
+    __half* res_k;
+    __half* res_v;
+    uint8_t* pool;
+    float* shadow;
+    float scale_log2;
+    uint32_t* status;
+};
+cudaError_t launch_steps(const StepsParams& p, cudaStream_t s);
 cudaError_t launch_pages_tc(const PagesParams& p, int grid, cudaStream_t s, bool pdl);
 
 // ---- H2O baseline (h2o.cu) ----
