@@ -402,11 +402,14 @@ def run_mkv(args, rank, world):
     clk = ClockSampler(torch.cuda.current_device())
     clk.__enter__()
     torch.cuda.synchronize()
+    from paper_2411_18077_b200 import _capi
+    launches0 = int(_capi.lib().mkv_debug_launch_count())
     ev0.record(stream)
     for s in range(args.warmup, steps_total):
         do_step(s)
     ev1.record(stream)
     torch.cuda.synchronize()
+    launches_timed = int(_capi.lib().mkv_debug_launch_count()) - launches0
     ms = dist_max(ev0.elapsed_time(ev1), world)
     # outputs of the last timed step, for the parity check against the reference
     last_out = out.float().cpu()
@@ -418,10 +421,10 @@ def run_mkv(args, rank, world):
     res = dict(ms_per_step=ms_per_step, tokens_per_s=tokens_per_s,
                hbm_gbs=dist_max(bytes_timed, 1) / (ms / 1e3) / 1e9,
                setup_s=setup_s, preroll=preroll, flushes_in_timed=flushes,
-               # coalesced (default): a page kernel + a finish kernel per step, a flush step adds one
-               # append launch for every unit.  MKV_LAYERS_SPLIT: both per layer, and a flush step
-               # adds one append launch for every layer and one plan-build launch.
-               gpu_launches=(args.steps * NL * 2 + 2 * flushes) if SPLIT else (args.steps * 2 + flushes),
+               # counted by the library (mkv_debug_launch_count) over the timed steps: per step a
+               # page kernel + residual + merge kernel (calls with more units than SMs) or + one
+               # finish kernel; a flush step adds the append launch
+               gpu_launches=launches_timed,
                B_local=B_local, upl=upl, n_units=n_units, pages=base_pages)
     # bytes of every rank (whole-job GB/s)
     if world > 1:

@@ -216,6 +216,9 @@ int mkv_decode_pages_only(mkv_cache* cache, const mkv_decode_args* args, void* s
  * runs with MKV_DECODE_TRACE set): 4 globaltimer stamps per warp {start, after
  * griddepcontrol.wait, pages done, 0}.  Returns words written. */
 int mkv_debug_decode_trace(const mkv_cache* cache, uint64_t* out, int max_words);
+/* Diagnostics: how many decode-path kernels (page / finish / residual / merge / append / plan
+ * build / steps) this library has launched so far in the process (host-side counter). */
+uint64_t mkv_debug_launch_count(void);
 /* Multi-layer decode step: n_layers consecutive mkv_decode_step calls in one FFI crossing.
  * Layers that continue each other -- adjacent unit ranges, the same group and scale, and
  * q / out / k_new / v_new back to back as in one [layers][units] array -- are coalesced into ONE

@@ -127,7 +127,7 @@ EXPORTS = [
     "mkv_allocate_variance", "mkv_score_variance",
     "mkv_cache_create", "mkv_cache_destroy", "mkv_cache_bytes", "mkv_cache_unit_info",
     "mkv_cache_prefill", "mkv_cache_prefill_select", "mkv_decode_step", "mkv_cache_append",
-    "mkv_decode_step_layers", "mkv_decode_steps", "mkv_debug_decode_trace", "mkv_decode_pages_only", "mkv_cache_export_sizes", "mkv_cache_export_reference",
+    "mkv_decode_step_layers", "mkv_decode_steps", "mkv_debug_decode_trace", "mkv_debug_launch_count", "mkv_decode_pages_only", "mkv_cache_export_sizes", "mkv_cache_export_reference",
     "mkv_cache_export_residual", "mkv_cache_check", "mkv_cache_save_mkvc", "mkv_cache_load_mkvc",
     "mkv_synth_fp16", "mkv_synth_fp16_rows", "mkv_synth_uniform_f32", "mkv_h2o_dynamic_baseline",
     "mkv_attention_f32", "mkv_decode_attention_f32", "mkv_quantize_block_f32", "mkv_dequantize_f32"]
@@ -172,6 +172,9 @@ def lib():
     L.mkv_cache_load_mkvc.argtypes = [vp, i32, C.c_char_p]
     if hasattr(L, "mkv_debug_decode_trace"):  # diagnostics entry (absent in older A/B builds)
         L.mkv_debug_decode_trace.argtypes = [vp, vp, i32]
+    if hasattr(L, "mkv_debug_launch_count"):
+        L.mkv_debug_launch_count.argtypes = []
+        L.mkv_debug_launch_count.restype = C.c_uint64
     L.mkv_synth_fp16.argtypes = [vp, i64, C.c_uint64, C.c_uint64, vp]
     L.mkv_synth_fp16_rows.argtypes = [vp, i64, i64, i64, C.c_uint64, C.c_uint64, C.c_uint64, vp]
     L.mkv_synth_uniform_f32.argtypes = [vp, i64, i64, i64, C.c_uint64, C.c_uint64, C.c_uint64, vp]

@@ -894,6 +894,8 @@ static int decode_impl(mkv_cache* c, const mkv_decode_args* a, bool attend, cuda
     return MKV_OK;
 }
 
+uint64_t mkv_debug_launch_count(void) { return launch_count(); }
+
 int mkv_debug_decode_trace(const mkv_cache* c, uint64_t* out, int max_words) {
     if (!c || !out) return fail(MKV_ERR_INVALID_ARGUMENT, "trace: null");
     if (!c->d_trace) return fail(MKV_ERR_RUNTIME, "trace: run with MKV_DECODE_TRACE set");

@@ -30,10 +30,18 @@
 #include <stdio.h>
 #include <stdlib.h>
 
+#include <atomic>
+
 #include "mkv_kernels.h"
 #include "mkv_page.cuh"
 
 namespace mkv {
+
+// Host-side count of this library's decode-path kernel launches (mkv_debug_launch_count: bench.py
+// reports the launches of its timed region from it).
+static std::atomic<uint64_t> g_launches{0};
+void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
 namespace {
 
@@ -96,6 +104,7 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    count_launch(1);
     return cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 
@@ -464,6 +473,7 @@ static cudaError_t launch_pages_t(const PagesParams& p, int grid, cudaStream_t s
         configured = true;
     }
     if (!pdl) {
+        count_launch(1);
         pages_kernel<W, S><<<grid, W * 32, smem, s>>>(p);
         return cudaGetLastError();
     }
@@ -598,6 +608,7 @@ cudaError_t launch_append(const ResidualParams& p, cudaStream_t s) {
     const size_t smem = kAppendSmem;
     if (cudaError_t e = append_configure(smem)) return e;
     AppendSegs none{};
+    count_launch(1);
     append_kernel<<<p.n_units, kAppendThreads, smem, s>>>(p, none);
     return cudaGetLastError();
 }
@@ -607,6 +618,7 @@ cudaError_t launch_append_segments(const ResidualParams& p, const AppendSegs& se
     if (cudaError_t e = append_configure(smem)) return e;
     const int blocks = segs.block_begin[segs.n_seg];
     if (blocks == 0) return cudaSuccess;
+    count_launch(1);
     append_kernel<<<blocks, kAppendThreads, smem, s>>>(p, segs);
     return cudaGetLastError();
 }
@@ -673,6 +685,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_build_kernel(const UnitMeta
 
 cudaError_t launch_plan_build(const UnitMeta* meta, const PlanBuildJobs& jobs, cudaStream_t s) {
     if (jobs.n_jobs == 0) return cudaSuccess;
+    count_launch(1);
     plan_build_kernel<<<jobs.n_jobs, kPlanThreads, 0, s>>>(meta, jobs);
     return cudaGetLastError();
 }
@@ -1141,6 +1154,7 @@ cudaError_t launch_finish(const ResidualParams& p, const int32_t* pref, WorkerRa
     // PDL only behind a page kernel: a finish that follows another finish (no pages) reads
     // the n_res / residual rows that kernel writes, so it needs the full dependency
     if (!after_pages) {
+        count_launch(1);
         finish_kernel<false><<<p.n_units, kFinishThreads, smem, s>>>(p, pref, wr);
         return cudaGetLastError();
     }
@@ -1161,6 +1175,7 @@ cudaError_t launch_resid_merge(const ResidualParams& p, const int32_t* pref, Wor
     const int grid = std::max(1, std::min(resid_ctas, p.n_units));
     cudaError_t e;
     if (!after_pages) {
+        count_launch(1);
         finish_kernel<true><<<grid, kFinishThreads, smem, s>>>(p, pref, wr);
         e = cudaGetLastError();
     } else {
@@ -1547,6 +1562,7 @@ cudaError_t launch_steps(const StepsParams& p, cudaStream_t s) {
         if (e != cudaSuccess) return e;
         configured = true;
     }
+    count_launch(1);
     steps_kernel<<<p.n_units, kStepsThreads, kStepsSmem, s>>>(p);
     return cudaGetLastError();
 }

@@ -652,6 +652,7 @@ static cudaError_t launch_tc_t(const PagesParams& p, int grid, cudaStream_t s, b
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
+    count_launch(1);
     return cudaLaunchKernelEx(&cfg, pages_tc_kernel<GP>, p);
 }
 

@@ -171,6 +171,9 @@ struct StepsParams {
     uint32_t* status;
 };
 cudaError_t launch_steps(const StepsParams& p, cudaStream_t s);
+// host-side count of decode-path kernel launches (diagnostics: mkv_debug_launch_count)
+void count_launch(int n);
+uint64_t launch_count();
 cudaError_t launch_pages_tc(const PagesParams& p, int grid, cudaStream_t s, bool pdl);
 
 // ---- H2O baseline (h2o.cu) ----
