@@ -120,6 +120,12 @@ struct FwdBars {
 constexpr int kFwdThreads = 320;  // warps 0-3 softmax A, 4-7 softmax B, 8 TMA, 9 MMA
 constexpr int kFwdSmem = 6 * kTileB + 1024 + 256;  // Q[2], K[2], V[2] + alignment slack + barriers
 
+__device__ __forceinline__ float fmax3(float a, float b, float c) {  // FMNMX3 (sm_100)
+    float r;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+
 template <int kPoly>
 __global__ void __launch_bounds__(kFwdThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
@@ -273,15 +279,19 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             const int cut = lim - j * kTile;  // columns c > cut are masked
             const bool nomask = __all_sync(0xffffffffu, cut >= kTile - 1);
             float mt = -INFINITY;
-            if (nomask) {
+            if (!nomask) {
 #pragma unroll
-                for (int c = 0; c < 128; ++c) mt = fmaxf(mt, __uint_as_float(x[c]));
-            } else {
-#pragma unroll
-                for (int c = 0; c < 128; ++c) {
+                for (int c = 0; c < 128; ++c)
                     if (c > cut) x[c] = __float_as_uint(-INFINITY);
-                    mt = fmaxf(mt, __uint_as_float(x[c]));
+            }
+            {  // row max with the 3-input FMNMX3 (half the max instructions), 4 chains
+                float mc[4] = {__uint_as_float(x[0]), __uint_as_float(x[1]), __uint_as_float(x[2]), __uint_as_float(x[3])};
+#pragma unroll
+                for (int c = 4; c < 128; c += 8) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) mc[k] = fmax3(mc[k], __uint_as_float(x[c + 2 * k]), __uint_as_float(x[c + 2 * k + 1]));
                 }
+                mt = fmax3(fmaxf(mc[0], mc[1]), mc[2], mc[3]);
             }
             mt *= sl2;
             const float m_new = fmaxf(m, mt);
