@@ -1203,7 +1203,7 @@ constexpr int kStepsWarps = 8;
 constexpr int kStepsThreads = kStepsWarps * 32;
 constexpr int kStepsRing = 2 * kBatch * kPageBytes;  // per warp: 2 stages of one 4-page batch (16 KB)
 static_assert(kStepsRing >= (int)sizeof(PageRows), "ring doubles as the residual tile / flush row buffer");
-constexpr size_t kStepsSmem = (size_t)kStepsWarps * (kStepsRing + sizeof(PageParams)) + kQBytes +
+constexpr size_t kStepsSmem = (size_t)kStepsWarps * (kStepsRing + sizeof(PageParams)) + 2 * kQBytes +
                               (size_t)kStepsWarps * (2 * kMaxG + kMaxG * kHeadDim) * sizeof(float) + 64;
 
 __global__ void __launch_bounds__(kStepsThreads, 1) steps_kernel(const StepsParams P) {
@@ -1214,8 +1214,8 @@ __global__ void __launch_bounds__(kStepsThreads, 1) steps_kernel(const StepsPara
     const int d = kHeadDim, G = P.group;
     uint8_t* ring = smem_raw + (size_t)warp * kStepsRing;
     PageParams& prm = reinterpret_cast<PageParams*>(smem_raw + (size_t)kStepsWarps * kStepsRing)[warp];
-    __half* qsm = reinterpret_cast<__half*>(smem_raw + (size_t)kStepsWarps * (kStepsRing + sizeof(PageParams)));
-    float* parts = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(qsm) + kQBytes);  // [warp][2][kMaxG] then o
+    __half* qbuf = reinterpret_cast<__half*>(smem_raw + (size_t)kStepsWarps * (kStepsRing + sizeof(PageParams)));
+    float* parts = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(qbuf) + 2 * kQBytes);  // [warp][2][kMaxG] then o
     float (*pml)[2][kMaxG] = reinterpret_cast<float (*)[2][kMaxG]>(parts);
     float* po_all = parts + kStepsWarps * 2 * kMaxG;  // [warp][kMaxG][d]
     const UnitMeta meta0 = P.meta[u];
@@ -1240,24 +1240,35 @@ __global__ void __launch_bounds__(kStepsThreads, 1) steps_kernel(const StepsPara
         for (int e = lane; e < n * kPageBytes / 16; e += 32) cp_async16(dst + 16 * e, src + 16 * e);
         cp_async_commit();
     };
+    // step inputs are loaded one step ahead into registers (q: <= one 16-byte chunk per thread,
+    // the token: one chunk per thread of warp 0) and staged at the end of the previous step
+    auto q_chunk = [&](int st) {
+        const __half* q = P.q + (size_t)st * P.q_step + (size_t)i * G * d;
+        return tid < G * d / 8 ? __ldg(reinterpret_cast<const uint4*>(q) + tid) : make_uint4(0, 0, 0, 0);
+    };
+    auto tok_chunk = [&](int st) {
+        if (P.k_new == nullptr || tid >= 32) return make_uint4(0, 0, 0, 0);
+        const __half* src = (tid < 16 ? P.k_new : P.v_new) + (size_t)st * P.kv_step + (size_t)i * d;
+        return __ldg(reinterpret_cast<const uint4*>(src) + (tid & 15));
+    };
+    static_assert(kMaxG * kHeadDim / 8 <= kStepsThreads, "q chunk per thread");
+    if (tid < G * d / 8) reinterpret_cast<uint4*>(qbuf)[tid] = q_chunk(0);
+    uint4 tok = tok_chunk(0);
+    __syncthreads();
     for (int st = 0; st < P.n_steps; ++st) {
+        const __half* qsm = qbuf + (st & 1) * (kQBytes / 2);
         // the warp's first page batch is requested before the append unless this step flushes
-        // (then the new pages are built first): its latency overlaps the q / token loads
+        // (then the new pages are built first): its latency overlaps the append
         const bool flushes = P.k_new != nullptr && n_res + 1 == P.n_r;
         int nb = (n_pages + kBatch - 1) / kBatch;
         int b0 = (int)(((int64_t)warp * nb) / kStepsWarps), b1 = (int)(((int64_t)(warp + 1) * nb) / kStepsWarps);
         if (!flushes && b0 < b1) load_batch(b0, 0);
-        const __half* q = P.q + (size_t)st * P.q_step + (size_t)i * G * d;
-        for (int e = tid; e < G * d / 8; e += kStepsThreads)
-            reinterpret_cast<uint4*>(qsm)[e] = __ldg(reinterpret_cast<const uint4*>(q) + e);
+        const bool more = st + 1 < P.n_steps;
+        const uint4 q_next = more ? q_chunk(st + 1) : make_uint4(0, 0, 0, 0);
+        const uint4 tok_next = more ? tok_chunk(st + 1) : make_uint4(0, 0, 0, 0);
         // ---- decode_append (+ store_block of a full residual block) ----
         if (P.k_new != nullptr) {
-            if (tid < 16)
-                reinterpret_cast<uint4*>(rk + (size_t)n_res * d)[tid] =
-                    __ldg(reinterpret_cast<const uint4*>(P.k_new + (size_t)st * P.kv_step + (size_t)i * d) + tid);
-            else if (tid < 32)
-                reinterpret_cast<uint4*>(rv + (size_t)n_res * d)[tid - 16] =
-                    __ldg(reinterpret_cast<const uint4*>(P.v_new + (size_t)st * P.kv_step + (size_t)i * d) + tid - 16);
+            if (tid < 32) reinterpret_cast<uint4*>((tid < 16 ? rk : rv) + (size_t)n_res * d)[tid & 15] = tok;
             ++n_res;
             if (n_res == P.n_r) {
                 __threadfence();  // the rows are read back through L2 (cp.async.cg)
@@ -1278,7 +1289,10 @@ __global__ void __launch_bounds__(kStepsThreads, 1) steps_kernel(const StepsPara
                 n_built = 0;
             }
         }
-        __threadfence();  // pages / residual row written above are read back through L2 below
+        // pages built above are read back through L2 (cp.async.cg) below; the new residual row is
+        // staged from the step's input instead, and reaches L2 for later steps through the fence
+        // at the end of this step
+        if (flushes) __threadfence();
         __syncthreads();
 
         // ---- q fragments (as pages_kernel: scales folded in, K-bias copy carries the softmax scale) ----
@@ -1446,12 +1460,17 @@ __global__ void __launch_bounds__(kStepsThreads, 1) steps_kernel(const StepsPara
         for (int t = kStepsWarps - 1 - warp; 16 * t < n_res; t += kStepsWarps) {
             const int nrows = min(16, n_res - 16 * t);
             uint8_t* tile = ring;  // this warp's page batches are done: its ring holds the tile
+            const bool fresh = P.k_new != nullptr && !flushes;  // row n_res - 1 came with this step
             for (int e = lane; e < 256; e += 32) {
                 const int r = e >> 4, cc = e & 15;
                 const int off = r * 256 + ((cc ^ (r & 7)) << 4);
                 if (r < nrows) {
-                    cp_async16(tile + off, rk + (size_t)(16 * t + r) * d + cc * 8);
-                    cp_async16(tile + 4096 + off, rv + (size_t)(16 * t + r) * d + cc * 8);
+                    const int row = 16 * t + r;
+                    const bool tokrow = fresh && row == n_res - 1;
+                    cp_async16(tile + off, tokrow ? P.k_new + (size_t)st * P.kv_step + (size_t)i * d + cc * 8
+                                                  : rk + (size_t)row * d + cc * 8);
+                    cp_async16(tile + 4096 + off, tokrow ? P.v_new + (size_t)st * P.kv_step + (size_t)i * d + cc * 8
+                                                         : rv + (size_t)row * d + cc * 8);
                 } else {  // rows past the residual are multiplied by p = 0: keep them finite
                     *reinterpret_cast<uint4*>(tile + off) = make_uint4(0, 0, 0, 0);
                     *reinterpret_cast<uint4*>(tile + 4096 + off) = make_uint4(0, 0, 0, 0);
@@ -1545,6 +1564,10 @@ __global__ void __launch_bounds__(kStepsThreads, 1) steps_kernel(const StepsPara
             o2[0] = __floats2half2_rn(a.x * li, a.y * li);
             o2[1] = __floats2half2_rn(a.z * li, a.w * li);
         }
+        // next step's q into the other buffer; the appended row reaches L2 for later steps
+        if (more && tid < G * d / 8) reinterpret_cast<uint4*>(qbuf + ((st + 1) & 1) * (kQBytes / 2))[tid] = q_next;
+        tok = tok_next;
+        if (tid < 32) __threadfence();
         __syncthreads();  // partials / q staging are reused by the next step
     }
     if (!ok && lane == 0) atomicOr(P.status, kStatusNonFinite);
