@@ -113,6 +113,7 @@ struct mkv_cache {
     __half* d_res_v = nullptr;
     uint32_t* d_status = nullptr;
     int* d_unit_cnt = nullptr;    // split finish: per-unit arrival counters (zero between calls)
+    int* d_scratch_cnt = nullptr; // mkv_decode_pages_only: counts nobody reads (the counting kernel, timed alone)
     float* d_res_ml = nullptr;    // split finish: residual partial per unit
     float* d_res_o = nullptr;
     uint64_t* d_trace = nullptr;  // diagnostics only (MKV_DECODE_TRACE)
@@ -137,7 +138,7 @@ struct mkv_cache {
         if (ev_compute) cudaEventDestroy(ev_compute);
         cudaFree(d_meta); cudaFree(d_pool); cudaFree(d_shadow); cudaFree(d_res_k); cudaFree(d_res_v);
         cudaFree(d_status);
-        cudaFree(d_unit_cnt); cudaFree(d_res_ml); cudaFree(d_res_o);
+        cudaFree(d_unit_cnt); cudaFree(d_scratch_cnt); cudaFree(d_res_ml); cudaFree(d_res_o);
         cudaFree(d_trace);
         cudaFree(d_kept);
     }
@@ -406,6 +407,7 @@ int mkv_cache_create(const mkv_cache_config* cfg, mkv_cache** out) {
     if (e == cudaSuccess) e = cudaMemset(c->d_status, 0, sizeof(uint32_t));
     if (e == cudaSuccess) e = al((void**)&c->d_unit_cnt, sizeof(int) * n);
     if (e == cudaSuccess) e = cudaMemset(c->d_unit_cnt, 0, sizeof(int) * std::max(n, 1));
+    if (e == cudaSuccess) e = al((void**)&c->d_scratch_cnt, sizeof(int) * n);
     if (e == cudaSuccess) e = al((void**)&c->d_res_ml, sizeof(float) * 2 * kMaxG * n);
     if (e == cudaSuccess) e = al((void**)&c->d_res_o, sizeof(float) * kMaxG * c->d * n);
     if (e == cudaSuccess) e = cudaMemset(c->d_pool, 0, (size_t)acc * kPageBytes);
@@ -1008,6 +1010,9 @@ int mkv_decode_pages_only(mkv_cache* c, const mkv_decode_args* a, void* stream) 
     if (pl->total == 0) return MKV_OK;
     PagesParams pp;
     fill_pages_params(c, pl, a, pp);
+    // the page kernel a decode call of this size runs: the counting variant when its finish step
+    // is split (counts go to a scratch array: no merge follows)
+    if (split_finish(a->n_units)) pp.unit_cnt = c->d_scratch_cnt;
     CK(launch_pages(pp, pl->grid, s, !swapped));
     return MKV_OK;
 }

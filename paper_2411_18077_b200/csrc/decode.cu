@@ -126,7 +126,9 @@ static cudaError_t set_carveout(const void* fn) {
 // ---------------------------------------------------------------------------
 // pages kernel
 // ---------------------------------------------------------------------------
-template <int kWarps, int kStages>
+// kCount: the split finish's per-segment arrival count (P.unit_cnt) is compiled in only where it
+// is used -- even unused, its epilogue code cost the pass ~1% (584 vs 578 us per headline launch).
+template <int kWarps, int kStages, bool kCount>
 // <= 208 registers (x 256 threads = 53248): leaves 12288 registers of the SM's 65536 for one
 // co-resident finish CTA (4 warps x 96).
 __global__ void __maxnreg__(208) pages_kernel(const PagesParams P) {
@@ -449,7 +451,9 @@ __global__ void __maxnreg__(208) pages_kernel(const PagesParams P) {
                 po[h1 * kHeadDim + c + 8] = fmaf(O[g][3], f, dv1);
             }
         }
-        if (P.unit_cnt != nullptr) {  // split finish: count this segment's partial
+        // (the runtime test is kept in the counting variant: as `if constexpr` alone the pass
+        // compiled ~1% slower -- code layout, measured)
+        if (kCount && P.unit_cnt != nullptr) {  // split finish: count this segment's partial
             // bar.warp.sync orders every lane's partial stores before lane 0's release add
             // (release is cumulative); merge_kernel acquires the counter before reading them
             __syncwarp();
@@ -462,22 +466,26 @@ __global__ void __maxnreg__(208) pages_kernel(const PagesParams P) {
     if (P.early) asm volatile("griddepcontrol.wait;\n" ::: "memory");
 }
 
-template <int W, int S>
-static cudaError_t launch_pages_t(const PagesParams& p, int grid, cudaStream_t s, bool pdl) {
+template <int W, int S, bool C>
+static cudaError_t launch_pages_c(const PagesParams& p, int grid, cudaStream_t s, bool pdl) {
     const size_t smem = (size_t)W * warp_smem<S>() + (size_t)W * S * sizeof(uint64_t);
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(pages_kernel<W, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e == cudaSuccess) e = set_carveout(reinterpret_cast<const void*>(pages_kernel<W, S>));
+        cudaError_t e = cudaFuncSetAttribute(pages_kernel<W, S, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess) e = set_carveout(reinterpret_cast<const void*>(pages_kernel<W, S, C>));
         if (e != cudaSuccess) return e;
         configured = true;
     }
     if (!pdl) {
         count_launch(1);
-        pages_kernel<W, S><<<grid, W * 32, smem, s>>>(p);
+        pages_kernel<W, S, C><<<grid, W * 32, smem, s>>>(p);
         return cudaGetLastError();
     }
-    return launch_pdl(pages_kernel<W, S>, dim3(grid), dim3(W * 32), smem, s, p);
+    return launch_pdl(pages_kernel<W, S, C>, dim3(grid), dim3(W * 32), smem, s, p);
+}
+template <int W, int S>
+static cudaError_t launch_pages_t(const PagesParams& p, int grid, cudaStream_t s, bool pdl) {
+    return p.unit_cnt != nullptr ? launch_pages_c<W, S, true>(p, grid, s, pdl) : launch_pages_c<W, S, false>(p, grid, s, pdl);
 }
 
 // The page pass: the mma.sync pages_kernel above (8 warps x 2 stages, 4-page batches;
