@@ -17,3 +17,6 @@ for mode in default split; do
 done
 grep -E "SUMMARY|##" "$out/sanitizer.txt"
 bash tools/profile_round.sh "$out"
+timeout 900 python bench.py --workload lwm-7b > "$out/bench_lwm.json" 2> "$out/bench_lwm.err"; echo "lwm rc=$?"
+bash tools/multi_rank_check.sh > "$out/multirank.txt" 2>&1
+for f in mr_b2 mr_b2_headsplit mr_lwm2; do echo "== $f" >> "$out/multirank.txt"; tail -1 gpurun_out/$f.json >> "$out/multirank.txt"; done
