@@ -996,9 +996,9 @@ __global__ void __launch_bounds__(kFinishThreads, 5) finish_kernel(const Residua
                 P.res_ml[(size_t)u * 2 * kMaxG + kMaxG + h] = L;
             }
         }
-        __threadfence();
         __syncthreads();  // (also: the next unit reuses the tiles and the warp partials)
-        if (tid == 0) atomicAdd(P.unit_cnt + u, 1);
+        // bar.sync orders every thread's partial stores before thread 0's release add
+        if (tid == 0) asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(P.unit_cnt + u) : "memory");
         fstamp(3);
     } else {
     // ---- the page partials are complete past this point ----
