@@ -753,321 +753,322 @@ __global__ void __launch_bounds__(kFinishThreads, 5) finish_kernel(const Residua
     // kernel waits on the per-unit counters)
     if (tid == 0) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     for (int i = blockIdx.x; i < P.n_units; i += kSplit ? gridDim.x : P.n_units) {
-    const int u = P.unit_begin + i;
-    const int d = kHeadDim;
-    const int G = P.group;
-    // pre-wait prologue: meta / plan were produced before the page kernel started
-    const int n_old = P.meta[u].n_res;
-    const bool app = P.k_new != nullptr;
-    const int n = n_old + (app ? 1 : 0);
-    const bool flush = app && P.fused_flush && n == P.n_r;  // this append fills the residual block
-    const int ntiles = (n + 15) >> 4;
-    const int upre = pref[i], uend = pref[i + 1];
-    const int w_first = uend > upre ? worker_of_batch(upre / wr.batch, wr.total_batches, wr.workers) : 0;
-    const int w_last = uend > upre ? worker_of_batch((uend - 1) / wr.batch, wr.total_batches, wr.workers) : -1;
-    const int n_part = w_last - w_first + 1;
-    __half* rk = P.res_k + (size_t)u * P.n_r * d;
-    __half* rv = P.res_v + (size_t)u * P.n_r * d;
-    const float sl2 = P.scale_log2;
-    const int h0 = 2 * tig, h1 = 2 * tig + 1;
-    // the next layer's page kernel may start its prologue and first page loads on SMs this
-    // grid leaves free (it reads nothing this kernel writes before its own griddepcontrol.wait)
-    auto fstamp = [&](int k) {
-        if (P.trace != nullptr && tid == 0 && i < kTraceFinishCtas) {
-            uint64_t t;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-            P.trace[(size_t)i * 4 + k] = t;
-        }
-    };
-    fstamp(0);
+        const int u = P.unit_begin + i;
+        const int d = kHeadDim;
+        const int G = P.group;
+        // pre-wait prologue: meta / plan were produced before the page kernel started
+        const int n_old = P.meta[u].n_res;
+        const bool app = P.k_new != nullptr;
+        const int n = n_old + (app ? 1 : 0);
+        const bool flush = app && P.fused_flush && n == P.n_r;  // this append fills the residual block
+        const int ntiles = (n + 15) >> 4;
+        const int upre = pref[i], uend = pref[i + 1];
+        const int w_first = uend > upre ? worker_of_batch(upre / wr.batch, wr.total_batches, wr.workers) : 0;
+        const int w_last = uend > upre ? worker_of_batch((uend - 1) / wr.batch, wr.total_batches, wr.workers) : -1;
+        const int n_part = w_last - w_first + 1;
+        __half* rk = P.res_k + (size_t)u * P.n_r * d;
+        __half* rv = P.res_v + (size_t)u * P.n_r * d;
+        const float sl2 = P.scale_log2;
+        const int h0 = 2 * tig, h1 = 2 * tig + 1;
+        // the next layer's page kernel may start its prologue and first page loads on SMs this
+        // grid leaves free (it reads nothing this kernel writes before its own griddepcontrol.wait)
+        auto fstamp = [&](int k) {
+            if (P.trace != nullptr && tid == 0 && i < kTraceFinishCtas) {
+                uint64_t t;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                P.trace[(size_t)i * 4 + k] = t;
+            }
+        };
+        fstamp(0);
 
-    // ---- residual attention (overlaps the page kernel): warp w owns tiles w, w + kFinishWarps, ... ----
-    uint32_t qb[8][2];
-#pragma unroll
-    for (int kc = 0; kc < 8; ++kc)
-#pragma unroll
-        for (int p = 0; p < 2; ++p)
-            qb[kc][p] = (gid < G) ? __ldg(reinterpret_cast<const uint32_t*>(P.q + ((size_t)i * G + gid) * d + 16 * kc +
-                                                                              2 * tig + 8 * p))
-                                  : 0u;
-    float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.0f, l1 = 0.0f;
-    float O[8][4];
-#pragma unroll
-    for (int g = 0; g < 8; ++g) O[g][0] = O[g][1] = O[g][2] = O[g][3] = 0.0f;
-    uint8_t* tile = smem_raw + warp * slot;
-    // rows past the residual count are multiplied by p = 0: they must hold finite values
-    for (int e = lane; e < 8192 / 16; e += 32) reinterpret_cast<uint4*>(tile)[e] = make_uint4(0, 0, 0, 0);
-    __syncwarp();
-    // scores, online softmax and P V of one 16-row tile (rows >= valid masked)
-    auto attend_tile = [&](int valid) {
-        float Sx[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-#pragma unroll
-        for (int kc = 0; kc < 8; ++kc) {
-            uint32_t a[4];
-            a[0] = *reinterpret_cast<const uint32_t*>(tile + gid * 256 + (((2 * kc) ^ gid) << 4) + 4 * tig);
-            a[1] = *reinterpret_cast<const uint32_t*>(tile + (gid + 8) * 256 + (((2 * kc) ^ gid) << 4) + 4 * tig);
-            a[2] = *reinterpret_cast<const uint32_t*>(tile + gid * 256 + (((2 * kc + 1) ^ gid) << 4) + 4 * tig);
-            a[3] = *reinterpret_cast<const uint32_t*>(tile + (gid + 8) * 256 + (((2 * kc + 1) ^ gid) << 4) + 4 * tig);
-            mma_16816(Sx, a, qb[kc][0], qb[kc][1]);
-        }
-        float x0 = Sx[0] * sl2, x1 = Sx[1] * sl2, x2 = Sx[2] * sl2, x3 = Sx[3] * sl2;
-        if (gid >= valid) { x0 = -INFINITY; x1 = -INFINITY; }
-        if (gid + 8 >= valid) { x2 = -INFINITY; x3 = -INFINITY; }
-        float mx0 = fmaxf(x0, x2), mx1 = fmaxf(x1, x3);
-#pragma unroll
-        for (int o = 4; o < 32; o <<= 1) {
-            mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
-            mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
-        }
-        const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
-        const float a0 = fast_exp2(m0 - mn0), a1 = fast_exp2(m1 - mn1);
-        m0 = mn0; m1 = mn1;
-        l0 *= a0; l1 *= a1;
-#pragma unroll
-        for (int g = 0; g < 8; ++g) { O[g][0] *= a0; O[g][1] *= a1; O[g][2] *= a0; O[g][3] *= a1; }
-        const float p0 = fast_exp2(x0 - m0), p1 = fast_exp2(x1 - m1);
-        const float p2 = fast_exp2(x2 - m0), p3 = fast_exp2(x3 - m1);
-        l0 += p0 + p2;
-        l1 += p1 + p3;
-        const uint32_t pb0 = movmatrix_trans(pack_half2(p0, p1));
-        const uint32_t pb1 = movmatrix_trans(pack_half2(p2, p3));
-        // O[c][h] += sum_t V^T[c][t] P[t][h]; ldmatrix.trans of the swizzled V rows:
-        // m0 (t0-7, c0-7) m1 (t0-7, c8-15) m2 (t8-15, c0-7) m3 (t8-15, c8-15) = a0 a1 a2 a3
-        const int mi = lane >> 3, ri = lane & 7;
-        const int vr = ri + 8 * (mi >> 1);
-#pragma unroll
-        for (int g = 0; g < 8; ++g) {
-            uint32_t a[4];
-            ldmatrix_x4_trans(a, tile + 4096 + vr * 256 + ((((2 * g) + (mi & 1)) ^ (vr & 7)) << 4));
-            mma_16816(O[g], a, pb0, pb1);
-        }
+        // ---- residual attention (overlaps the page kernel): warp w owns tiles w, w + kFinishWarps, ... ----
+        uint32_t qb[8][2];
+    #pragma unroll
+        for (int kc = 0; kc < 8; ++kc)
+    #pragma unroll
+            for (int p = 0; p < 2; ++p)
+                qb[kc][p] = (gid < G) ? __ldg(reinterpret_cast<const uint32_t*>(P.q + ((size_t)i * G + gid) * d + 16 * kc +
+                                                                                  2 * tig + 8 * p))
+                                      : 0u;
+        float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.0f, l1 = 0.0f;
+        float O[8][4];
+    #pragma unroll
+        for (int g = 0; g < 8; ++g) O[g][0] = O[g][1] = O[g][2] = O[g][3] = 0.0f;
+        uint8_t* tile = smem_raw + warp * slot;
+        // rows past the residual count are multiplied by p = 0: they must hold finite values
+        for (int e = lane; e < 8192 / 16; e += 32) reinterpret_cast<uint4*>(tile)[e] = make_uint4(0, 0, 0, 0);
         __syncwarp();
-    };
-    if (flush) {
-        // ---- fused flush (decode_append's store_block, cache_engine.cpp:34-52,79-90): the new
-        // token completes the n_r-row residual block; quantize it into n_r / 16 pages here (the
-        // K3 page builder, same pages as append_kernel) and attend the block in its DEQUANTIZED
-        // form, as decode_step does after a flush (cache_engine.cpp:108-136).  This step's page
-        // pass covers the older pages only. ----
-        if (tid < 16) {
-            reinterpret_cast<uint4*>(rk + (size_t)n_old * d)[tid] = reinterpret_cast<const uint4*>(P.k_new + (size_t)i * d)[tid];
-        } else if (tid < 32) {
-            reinterpret_cast<uint4*>(rv + (size_t)n_old * d)[tid - 16] =
-                reinterpret_cast<const uint4*>(P.v_new + (size_t)i * d)[tid - 16];
-        }
-        __threadfence_block();
-        __syncthreads();
-        const UnitMeta meta = P.meta[u];
-        PageScratch& ps = *reinterpret_cast<PageScratch*>(tile);
-        bool ok = true;
-        for (int t = warp; t < P.n_r / kGroup; t += kFinishWarps) {
-            for (int e = lane; e < 16 * 16; e += 32) {
-                const int r = e >> 4, c16 = e & 15;
-                reinterpret_cast<uint4*>(ps.k[r])[c16] = reinterpret_cast<const uint4*>(rk + (size_t)(16 * t + r) * d)[c16];
-                reinterpret_cast<uint4*>(ps.v[r])[c16] = reinterpret_cast<const uint4*>(rv + (size_t)(16 * t + r) * d)[c16];
+        // scores, online softmax and P V of one 16-row tile (rows >= valid masked)
+        auto attend_tile = [&](int valid) {
+            float Sx[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    #pragma unroll
+            for (int kc = 0; kc < 8; ++kc) {
+                uint32_t a[4];
+                a[0] = *reinterpret_cast<const uint32_t*>(tile + gid * 256 + (((2 * kc) ^ gid) << 4) + 4 * tig);
+                a[1] = *reinterpret_cast<const uint32_t*>(tile + (gid + 8) * 256 + (((2 * kc) ^ gid) << 4) + 4 * tig);
+                a[2] = *reinterpret_cast<const uint32_t*>(tile + gid * 256 + (((2 * kc + 1) ^ gid) << 4) + 4 * tig);
+                a[3] = *reinterpret_cast<const uint32_t*>(tile + (gid + 8) * 256 + (((2 * kc + 1) ^ gid) << 4) + 4 * tig);
+                mma_16816(Sx, a, qb[kc][0], qb[kc][1]);
+            }
+            float x0 = Sx[0] * sl2, x1 = Sx[1] * sl2, x2 = Sx[2] * sl2, x3 = Sx[3] * sl2;
+            if (gid >= valid) { x0 = -INFINITY; x1 = -INFINITY; }
+            if (gid + 8 >= valid) { x2 = -INFINITY; x3 = -INFINITY; }
+            float mx0 = fmaxf(x0, x2), mx1 = fmaxf(x1, x3);
+    #pragma unroll
+            for (int o = 4; o < 32; o <<= 1) {
+                mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
+                mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
+            }
+            const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+            const float a0 = fast_exp2(m0 - mn0), a1 = fast_exp2(m1 - mn1);
+            m0 = mn0; m1 = mn1;
+            l0 *= a0; l1 *= a1;
+    #pragma unroll
+            for (int g = 0; g < 8; ++g) { O[g][0] *= a0; O[g][1] *= a1; O[g][2] *= a0; O[g][3] *= a1; }
+            const float p0 = fast_exp2(x0 - m0), p1 = fast_exp2(x1 - m1);
+            const float p2 = fast_exp2(x2 - m0), p3 = fast_exp2(x3 - m1);
+            l0 += p0 + p2;
+            l1 += p1 + p3;
+            const uint32_t pb0 = movmatrix_trans(pack_half2(p0, p1));
+            const uint32_t pb1 = movmatrix_trans(pack_half2(p2, p3));
+            // O[c][h] += sum_t V^T[c][t] P[t][h]; ldmatrix.trans of the swizzled V rows:
+            // m0 (t0-7, c0-7) m1 (t0-7, c8-15) m2 (t8-15, c0-7) m3 (t8-15, c8-15) = a0 a1 a2 a3
+            const int mi = lane >> 3, ri = lane & 7;
+            const int vr = ri + 8 * (mi >> 1);
+    #pragma unroll
+            for (int g = 0; g < 8; ++g) {
+                uint32_t a[4];
+                ldmatrix_x4_trans(a, tile + 4096 + vr * 256 + ((((2 * g) + (mi & 1)) ^ (vr & 7)) << 4));
+                mma_16816(O[g], a, pb0, pb1);
             }
             __syncwarp();
-            const int64_t page = meta.page_base + meta.n_pages + t;
-            ok &= build_page(ps, 16, P.pool + (size_t)page * kPageBytes,
-                             P.shadow ? P.shadow + (size_t)page * (kShadowBytes / 4) : nullptr);
-            // dequantize the page into the tile: v = fl(code * scale) + zero with the page's fp16
-            // (scale, zero), rounded to fp16 (the page pass's values, up to that rounding)
-            const __half* ks = reinterpret_cast<const __half*>(ps.page + kKS);
-            const __half* kz = reinterpret_cast<const __half*>(ps.page + kKZ);
-            const __half* vs = reinterpret_cast<const __half*>(ps.page + kVS);
-            const __half* vz = reinterpret_cast<const __half*>(ps.page + kVZ);
-            for (int e = lane; e < 16 * 16; e += 32) {
-                const int r = e >> 4, cc = e & 15, g = cc >> 1;
-                uint32_t kq[4], vq[4];
-                const float vsc = __half2float(vs[vs_param_idx(r, g)]), vzp = __half2float(vz[vz_param_idx(r, g)]);
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int c0 = 8 * cc + 2 * j, c1 = c0 + 1;
-                    const float k0 = __fadd_rn(__fmul_rn((float)ps.kc[r][c0], __half2float(ks[k_param_idx(c0)])),
-                                               __half2float(kz[k_param_idx(c0)]));
-                    const float k1 = __fadd_rn(__fmul_rn((float)ps.kc[r][c1], __half2float(ks[k_param_idx(c1)])),
-                                               __half2float(kz[k_param_idx(c1)]));
-                    kq[j] = pack_half2(k0, k1);
-                    vq[j] = pack_half2(__fadd_rn(__fmul_rn((float)ps.vc[r][c0], vsc), vzp),
-                                       __fadd_rn(__fmul_rn((float)ps.vc[r][c1], vsc), vzp));
-                }
-                __syncwarp();  // (ps.k / ps.v are overwritten: every lane has read its codes first)
-                *reinterpret_cast<uint4*>(tile + r * 256 + ((cc ^ (r & 7)) << 4)) = make_uint4(kq[0], kq[1], kq[2], kq[3]);
-                *reinterpret_cast<uint4*>(tile + 4096 + r * 256 + ((cc ^ (r & 7)) << 4)) =
-                    make_uint4(vq[0], vq[1], vq[2], vq[3]);
-            }
-            __syncwarp();
-            attend_tile(16);
-        }
-        if (!ok && lane == 0) atomicOr(P.status, kStatusNonFinite);
-    }
-    for (int t = warp; t < (flush ? 0 : ntiles); t += kFinishWarps) {
-        const int row0 = 16 * t;
-        const int nrows = min(16, n_old - row0);  // rows already in the residual buffer
-        for (int e = lane; e < 256; e += 32) {
-            const int r = e >> 4, cc = e & 15;
-            if (r < nrows) {
-                const int off = r * 256 + ((cc ^ (r & 7)) << 4);
-                cp_async16(tile + off, rk + (size_t)(row0 + r) * d + cc * 8);
-                cp_async16(tile + 4096 + off, rv + (size_t)(row0 + r) * d + cc * 8);
-            }
-        }
-        cp_async_commit();
-        if (app && n_old >= row0 && n_old < row0 + 16) {  // decode_append (cache_engine.cpp:79-90)
-            const int r = n_old - row0, cc = lane & 15;
-            const bool is_v = lane >= 16;
-            const uint4 x = reinterpret_cast<const uint4*>((is_v ? P.v_new : P.k_new) + (size_t)i * d)[cc];
-            reinterpret_cast<uint4*>((is_v ? rv : rk) + (size_t)n_old * d)[cc] = x;
-            *reinterpret_cast<uint4*>(tile + (is_v ? 4096 : 0) + r * 256 + ((cc ^ (r & 7)) << 4)) = x;
-        }
-        cp_async_wait_all();
-        __syncwarp();
-        attend_tile(n - row0);
-    }
-    // Early page build: when this append fills a 16-row group of the residual block (and the
-    // block is not flushed now), the warp that attended that group's tile -- its 16 rows are in
-    // the tile, in the staged builder's swizzled layout -- quantizes it into the page it will
-    // occupy after the flush (store_block groups, cache_engine.cpp:34-52: each 16-row group is
-    // its own page, so the result is the flush's), so the flush step builds only the last one.
-    const bool early_build = app && !flush && (n & 15) == 0 && n < P.n_r && P.meta[u].n_built == (n >> 4) - 1 &&
-                             P.meta[u].n_pages + (n >> 4) <= P.meta[u].cap_pages;
-    if (early_build && warp == ((n >> 4) - 1) % kFinishWarps) {
-        PageParams& prm = *reinterpret_cast<PageParams*>(smem_raw + finish_smem_bytes(slot) - (int)sizeof(PageParams));
-        const int64_t page = P.meta[u].page_base + P.meta[u].n_pages + (n >> 4) - 1;
-        __syncwarp();
-        const bool ok = build_page_call(*reinterpret_cast<PageRows*>(tile), prm, P.pool + (size_t)page * kPageBytes,
-                                        P.shadow ? P.shadow + (size_t)page * (kShadowBytes / 4) : nullptr);
-        if (!ok && lane == 0) atomicOr(P.status, kStatusNonFinite);
-    }
-#pragma unroll
-    for (int o = 4; o < 32; o <<= 1) {
-        l0 += __shfl_xor_sync(0xffffffffu, l0, o);
-        l1 += __shfl_xor_sync(0xffffffffu, l1, o);
-    }
-    // warp partial -> smem over the warp's (now idle) tile buffer (l = 0 for warps without tiles)
-    float* wo = reinterpret_cast<float*>(tile);  // [kMaxG][128]
-    __syncwarp();
-#pragma unroll
-    for (int g = 0; g < 8; ++g) {
-        const int c = 16 * g + gid;
-        if (h0 < G) { wo[h0 * kHeadDim + c] = O[g][0]; wo[h0 * kHeadDim + c + 8] = O[g][2]; }
-        if (h1 < G) { wo[h1 * kHeadDim + c] = O[g][1]; wo[h1 * kHeadDim + c + 8] = O[g][3]; }
-    }
-    if (gid == 0) {
-        if (h0 < G) { wml[warp][0][h0] = m0; wml[warp][1][h0] = l0; }
-        if (h1 < G) { wml[warp][0][h1] = m1; wml[warp][1][h1] = l1; }
-    }
-    __syncthreads();  // every read of this unit's meta above is done before it changes
-    if (app && tid == 0) {  // only this CTA reads this unit's meta after the append
+        };
         if (flush) {
-            P.meta[u].n_pages += P.n_r / kGroup;
-            P.meta[u].n_res = 0;
-            P.meta[u].n_built = 0;
-        } else {
-            P.meta[u].n_res = n;
-            if (early_build) P.meta[u].n_built = n >> 4;
+            // ---- fused flush (decode_append's store_block, cache_engine.cpp:34-52,79-90): the new
+            // token completes the n_r-row residual block; quantize it into n_r / 16 pages here (the
+            // K3 page builder, same pages as append_kernel) and attend the block in its DEQUANTIZED
+            // form, as decode_step does after a flush (cache_engine.cpp:108-136).  This step's page
+            // pass covers the older pages only. ----
+            if (tid < 16) {
+                reinterpret_cast<uint4*>(rk + (size_t)n_old * d)[tid] = reinterpret_cast<const uint4*>(P.k_new + (size_t)i * d)[tid];
+            } else if (tid < 32) {
+                reinterpret_cast<uint4*>(rv + (size_t)n_old * d)[tid - 16] =
+                    reinterpret_cast<const uint4*>(P.v_new + (size_t)i * d)[tid - 16];
+            }
+            __threadfence_block();
+            __syncthreads();
+            const UnitMeta meta = P.meta[u];
+            PageScratch& ps = *reinterpret_cast<PageScratch*>(tile);
+            bool ok = true;
+            for (int t = warp; t < P.n_r / kGroup; t += kFinishWarps) {
+                for (int e = lane; e < 16 * 16; e += 32) {
+                    const int r = e >> 4, c16 = e & 15;
+                    reinterpret_cast<uint4*>(ps.k[r])[c16] = reinterpret_cast<const uint4*>(rk + (size_t)(16 * t + r) * d)[c16];
+                    reinterpret_cast<uint4*>(ps.v[r])[c16] = reinterpret_cast<const uint4*>(rv + (size_t)(16 * t + r) * d)[c16];
+                }
+                __syncwarp();
+                const int64_t page = meta.page_base + meta.n_pages + t;
+                ok &= build_page(ps, 16, P.pool + (size_t)page * kPageBytes,
+                                 P.shadow ? P.shadow + (size_t)page * (kShadowBytes / 4) : nullptr);
+                // dequantize the page into the tile: v = fl(code * scale) + zero with the page's fp16
+                // (scale, zero), rounded to fp16 (the page pass's values, up to that rounding)
+                const __half* ks = reinterpret_cast<const __half*>(ps.page + kKS);
+                const __half* kz = reinterpret_cast<const __half*>(ps.page + kKZ);
+                const __half* vs = reinterpret_cast<const __half*>(ps.page + kVS);
+                const __half* vz = reinterpret_cast<const __half*>(ps.page + kVZ);
+                for (int e = lane; e < 16 * 16; e += 32) {
+                    const int r = e >> 4, cc = e & 15, g = cc >> 1;
+                    uint32_t kq[4], vq[4];
+                    const float vsc = __half2float(vs[vs_param_idx(r, g)]), vzp = __half2float(vz[vz_param_idx(r, g)]);
+    #pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int c0 = 8 * cc + 2 * j, c1 = c0 + 1;
+                        const float k0 = __fadd_rn(__fmul_rn((float)ps.kc[r][c0], __half2float(ks[k_param_idx(c0)])),
+                                                   __half2float(kz[k_param_idx(c0)]));
+                        const float k1 = __fadd_rn(__fmul_rn((float)ps.kc[r][c1], __half2float(ks[k_param_idx(c1)])),
+                                                   __half2float(kz[k_param_idx(c1)]));
+                        kq[j] = pack_half2(k0, k1);
+                        vq[j] = pack_half2(__fadd_rn(__fmul_rn((float)ps.vc[r][c0], vsc), vzp),
+                                           __fadd_rn(__fmul_rn((float)ps.vc[r][c1], vsc), vzp));
+                    }
+                    __syncwarp();  // (ps.k / ps.v are overwritten: every lane has read its codes first)
+                    *reinterpret_cast<uint4*>(tile + r * 256 + ((cc ^ (r & 7)) << 4)) = make_uint4(kq[0], kq[1], kq[2], kq[3]);
+                    *reinterpret_cast<uint4*>(tile + 4096 + r * 256 + ((cc ^ (r & 7)) << 4)) =
+                        make_uint4(vq[0], vq[1], vq[2], vq[3]);
+                }
+                __syncwarp();
+                attend_tile(16);
+            }
+            if (!ok && lane == 0) atomicOr(P.status, kStatusNonFinite);
         }
-    }
-    if constexpr (kSplit) {
-        // combine the warps' residual partials into the unit's (online max over 4), store it,
-        // then count it: merge_kernel reads it once the unit's counter is complete
-        for (int e = tid; e < G * (d / 4); e += kFinishThreads) {
-            const int h = e / (d / 4), c4 = e % (d / 4);
-            float M = -INFINITY, L = 0.0f;
-            float4 a = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-            for (int w = 0; w < kFinishWarps; ++w) {
-                const float lw = wml[w][1][h];
-                if (lw > 0.0f) {
-                    const float mw = wml[w][0][h];
-                    const float nm = fmaxf(M, mw);
-                    const float f = fast_exp2(M - nm), sc = fast_exp2(mw - nm);
-                    const float4 wv = reinterpret_cast<const float4*>(smem_raw + w * slot)[h * (kHeadDim / 4) + c4];
-                    a.x = fmaf(wv.x, sc, a.x * f);
-                    a.y = fmaf(wv.y, sc, a.y * f);
-                    a.z = fmaf(wv.z, sc, a.z * f);
-                    a.w = fmaf(wv.w, sc, a.w * f);
-                    L = fmaf(lw, sc, L * f);
+        for (int t = warp; t < (flush ? 0 : ntiles); t += kFinishWarps) {
+            const int row0 = 16 * t;
+            const int nrows = min(16, n_old - row0);  // rows already in the residual buffer
+            for (int e = lane; e < 256; e += 32) {
+                const int r = e >> 4, cc = e & 15;
+                if (r < nrows) {
+                    const int off = r * 256 + ((cc ^ (r & 7)) << 4);
+                    cp_async16(tile + off, rk + (size_t)(row0 + r) * d + cc * 8);
+                    cp_async16(tile + 4096 + off, rv + (size_t)(row0 + r) * d + cc * 8);
+                }
+            }
+            cp_async_commit();
+            if (app && n_old >= row0 && n_old < row0 + 16) {  // decode_append (cache_engine.cpp:79-90)
+                const int r = n_old - row0, cc = lane & 15;
+                const bool is_v = lane >= 16;
+                const uint4 x = reinterpret_cast<const uint4*>((is_v ? P.v_new : P.k_new) + (size_t)i * d)[cc];
+                reinterpret_cast<uint4*>((is_v ? rv : rk) + (size_t)n_old * d)[cc] = x;
+                *reinterpret_cast<uint4*>(tile + (is_v ? 4096 : 0) + r * 256 + ((cc ^ (r & 7)) << 4)) = x;
+            }
+            cp_async_wait_all();
+            __syncwarp();
+            attend_tile(n - row0);
+        }
+        // Early page build: when this append fills a 16-row group of the residual block (and the
+        // block is not flushed now), the warp that attended that group's tile -- its 16 rows are in
+        // the tile, in the staged builder's swizzled layout -- quantizes it into the page it will
+        // occupy after the flush (store_block groups, cache_engine.cpp:34-52: each 16-row group is
+        // its own page, so the result is the flush's), so the flush step builds only the last one.
+        const bool early_build = app && !flush && (n & 15) == 0 && n < P.n_r && P.meta[u].n_built == (n >> 4) - 1 &&
+                                 P.meta[u].n_pages + (n >> 4) <= P.meta[u].cap_pages;
+        if (early_build && warp == ((n >> 4) - 1) % kFinishWarps) {
+            PageParams& prm = *reinterpret_cast<PageParams*>(smem_raw + finish_smem_bytes(slot) - (int)sizeof(PageParams));
+            const int64_t page = P.meta[u].page_base + P.meta[u].n_pages + (n >> 4) - 1;
+            __syncwarp();
+            const bool ok = build_page_call(*reinterpret_cast<PageRows*>(tile), prm, P.pool + (size_t)page * kPageBytes,
+                                            P.shadow ? P.shadow + (size_t)page * (kShadowBytes / 4) : nullptr);
+            if (!ok && lane == 0) atomicOr(P.status, kStatusNonFinite);
+        }
+    #pragma unroll
+        for (int o = 4; o < 32; o <<= 1) {
+            l0 += __shfl_xor_sync(0xffffffffu, l0, o);
+            l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+        }
+        // warp partial -> smem over the warp's (now idle) tile buffer (l = 0 for warps without tiles)
+        float* wo = reinterpret_cast<float*>(tile);  // [kMaxG][128]
+        __syncwarp();
+    #pragma unroll
+        for (int g = 0; g < 8; ++g) {
+            const int c = 16 * g + gid;
+            if (h0 < G) { wo[h0 * kHeadDim + c] = O[g][0]; wo[h0 * kHeadDim + c + 8] = O[g][2]; }
+            if (h1 < G) { wo[h1 * kHeadDim + c] = O[g][1]; wo[h1 * kHeadDim + c + 8] = O[g][3]; }
+        }
+        if (gid == 0) {
+            if (h0 < G) { wml[warp][0][h0] = m0; wml[warp][1][h0] = l0; }
+            if (h1 < G) { wml[warp][0][h1] = m1; wml[warp][1][h1] = l1; }
+        }
+        __syncthreads();  // every read of this unit's meta above is done before it changes
+        if (app && tid == 0) {  // only this CTA reads this unit's meta after the append
+            if (flush) {
+                P.meta[u].n_pages += P.n_r / kGroup;
+                P.meta[u].n_res = 0;
+                P.meta[u].n_built = 0;
+            } else {
+                P.meta[u].n_res = n;
+                if (early_build) P.meta[u].n_built = n >> 4;
+            }
+        }
+        if constexpr (kSplit) {
+            // combine the warps' residual partials into the unit's (online max over 4), store it,
+            // then count it: merge_kernel reads it once the unit's counter is complete
+            for (int e = tid; e < G * (d / 4); e += kFinishThreads) {
+                const int h = e / (d / 4), c4 = e % (d / 4);
+                float M = -INFINITY, L = 0.0f;
+                float4 a = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+                for (int w = 0; w < kFinishWarps; ++w) {
+                    const float lw = wml[w][1][h];
+                    if (lw > 0.0f) {
+                        const float mw = wml[w][0][h];
+                        const float nm = fmaxf(M, mw);
+                        const float f = fast_exp2(M - nm), sc = fast_exp2(mw - nm);
+                        const float4 wv = reinterpret_cast<const float4*>(smem_raw + w * slot)[h * (kHeadDim / 4) + c4];
+                        a.x = fmaf(wv.x, sc, a.x * f);
+                        a.y = fmaf(wv.y, sc, a.y * f);
+                        a.z = fmaf(wv.z, sc, a.z * f);
+                        a.w = fmaf(wv.w, sc, a.w * f);
+                        L = fmaf(lw, sc, L * f);
+                        M = nm;
+                    }
+                }
+                reinterpret_cast<float4*>(P.res_o + ((size_t)u * kMaxG + h) * d)[c4] = a;
+                if (c4 == 0) {
+                    P.res_ml[(size_t)u * 2 * kMaxG + h] = M;
+                    P.res_ml[(size_t)u * 2 * kMaxG + kMaxG + h] = L;
+                }
+            }
+            __syncthreads();  // (also: the next unit reuses the tiles and the warp partials)
+            // bar.sync orders every thread's partial stores before thread 0's release add
+            if (tid == 0) asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(P.unit_cnt + u) : "memory");
+            fstamp(3);
+        } else {
+            // ---- the page partials are complete past this point ----
+            fstamp(1);
+            asm volatile("griddepcontrol.wait;\n" ::: "memory");
+            fstamp(2);
+            __syncthreads();  // residual warp partials visible
+            // Merge: every thread owns 4 consecutive channels of one head (float4: one chunk per thread
+            // at G = 4) and loads (m, l, o) of kMergeBatch page partials at once -- one L2 round trip
+            // for a unit split over up to kMergeBatch page warps -- folded with an online max (no
+            // global-max pass, no further barriers).  h is warp-uniform: the (m, l) loads broadcast.
+            for (int e = tid; e < G * (d / 4); e += kFinishThreads) {
+                const int h = e / (d / 4), c4 = e % (d / 4);
+                float M = -INFINITY, L = 0.0f;
+                float4 a = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+                for (int w = 0; w < kFinishWarps; ++w) {
+                    const float lw = wml[w][1][h];
+                    if (lw > 0.0f) {
+                        const float mw = wml[w][0][h];
+                        const float nm = fmaxf(M, mw);
+                        const float f = fast_exp2(M - nm), s = fast_exp2(mw - nm);
+                        const float4 wv = reinterpret_cast<const float4*>(smem_raw + w * slot)[h * (kHeadDim / 4) + c4];
+                        a.x = fmaf(wv.x, s, a.x * f);
+                        a.y = fmaf(wv.y, s, a.y * f);
+                        a.z = fmaf(wv.z, s, a.z * f);
+                        a.w = fmaf(wv.w, s, a.w * f);
+                        L = fmaf(lw, s, L * f);
+                        M = nm;
+                    }
+                }
+                for (int p0 = 0; p0 < n_part; p0 += kMergeBatch) {
+                    float pm[kMergeBatch], pl[kMergeBatch];
+                    float4 po[kMergeBatch];
+        #pragma unroll
+                    for (int k = 0; k < kMergeBatch; ++k) {
+                        const int slot = w_first + p0 + k + i;
+                        const bool ok = p0 + k < n_part;
+                        pm[k] = ok ? __ldcg(P.part_ml + (size_t)slot * 2 * kMaxG + h) : -INFINITY;
+                        pl[k] = ok ? __ldcg(P.part_ml + (size_t)slot * 2 * kMaxG + kMaxG + h) : 0.0f;
+                        po[k] = ok ? __ldcg(reinterpret_cast<const float4*>(P.part_o + ((size_t)slot * kMaxG + h) * d) + c4)
+                                   : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+                    }
+                    float cm = pm[0];
+        #pragma unroll
+                    for (int k = 1; k < kMergeBatch; ++k) cm = fmaxf(cm, pm[k]);
+                    const float nm = fmaxf(M, cm);
+                    const float f = fast_exp2(M - nm);
+                    a.x *= f; a.y *= f; a.z *= f; a.w *= f; L *= f;
+        #pragma unroll
+                    for (int k = 0; k < kMergeBatch; ++k) {
+                        const float s = fast_exp2(pm[k] - nm);  // 0 for absent partials (m = -inf)
+                        a.x = fmaf(po[k].x, s, a.x);
+                        a.y = fmaf(po[k].y, s, a.y);
+                        a.z = fmaf(po[k].z, s, a.z);
+                        a.w = fmaf(po[k].w, s, a.w);
+                        L = fmaf(pl[k], s, L);
+                    }
                     M = nm;
                 }
+                const float li = 1.0f / L;
+                __half2* o2 = reinterpret_cast<__half2*>(P.out + ((size_t)i * G + h) * d) + 2 * c4;
+                o2[0] = __floats2half2_rn(a.x * li, a.y * li);
+                o2[1] = __floats2half2_rn(a.z * li, a.w * li);
             }
-            reinterpret_cast<float4*>(P.res_o + ((size_t)u * kMaxG + h) * d)[c4] = a;
-            if (c4 == 0) {
-                P.res_ml[(size_t)u * 2 * kMaxG + h] = M;
-                P.res_ml[(size_t)u * 2 * kMaxG + kMaxG + h] = L;
-            }
-        }
-        __syncthreads();  // (also: the next unit reuses the tiles and the warp partials)
-        // bar.sync orders every thread's partial stores before thread 0's release add
-        if (tid == 0) asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(P.unit_cnt + u) : "memory");
-        fstamp(3);
-    } else {
-    // ---- the page partials are complete past this point ----
-    fstamp(1);
-    asm volatile("griddepcontrol.wait;\n" ::: "memory");
-    fstamp(2);
-    __syncthreads();  // residual warp partials visible
-    // Merge: every thread owns 4 consecutive channels of one head (float4: one chunk per thread
-    // at G = 4) and loads (m, l, o) of kMergeBatch page partials at once -- one L2 round trip
-    // for a unit split over up to kMergeBatch page warps -- folded with an online max (no
-    // global-max pass, no further barriers).  h is warp-uniform: the (m, l) loads broadcast.
-    for (int e = tid; e < G * (d / 4); e += kFinishThreads) {
-        const int h = e / (d / 4), c4 = e % (d / 4);
-        float M = -INFINITY, L = 0.0f;
-        float4 a = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-        for (int w = 0; w < kFinishWarps; ++w) {
-            const float lw = wml[w][1][h];
-            if (lw > 0.0f) {
-                const float mw = wml[w][0][h];
-                const float nm = fmaxf(M, mw);
-                const float f = fast_exp2(M - nm), s = fast_exp2(mw - nm);
-                const float4 wv = reinterpret_cast<const float4*>(smem_raw + w * slot)[h * (kHeadDim / 4) + c4];
-                a.x = fmaf(wv.x, s, a.x * f);
-                a.y = fmaf(wv.y, s, a.y * f);
-                a.z = fmaf(wv.z, s, a.z * f);
-                a.w = fmaf(wv.w, s, a.w * f);
-                L = fmaf(lw, s, L * f);
-                M = nm;
-            }
-        }
-        for (int p0 = 0; p0 < n_part; p0 += kMergeBatch) {
-            float pm[kMergeBatch], pl[kMergeBatch];
-            float4 po[kMergeBatch];
-#pragma unroll
-            for (int k = 0; k < kMergeBatch; ++k) {
-                const int slot = w_first + p0 + k + i;
-                const bool ok = p0 + k < n_part;
-                pm[k] = ok ? __ldcg(P.part_ml + (size_t)slot * 2 * kMaxG + h) : -INFINITY;
-                pl[k] = ok ? __ldcg(P.part_ml + (size_t)slot * 2 * kMaxG + kMaxG + h) : 0.0f;
-                po[k] = ok ? __ldcg(reinterpret_cast<const float4*>(P.part_o + ((size_t)slot * kMaxG + h) * d) + c4)
-                           : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-            }
-            float cm = pm[0];
-#pragma unroll
-            for (int k = 1; k < kMergeBatch; ++k) cm = fmaxf(cm, pm[k]);
-            const float nm = fmaxf(M, cm);
-            const float f = fast_exp2(M - nm);
-            a.x *= f; a.y *= f; a.z *= f; a.w *= f; L *= f;
-#pragma unroll
-            for (int k = 0; k < kMergeBatch; ++k) {
-                const float s = fast_exp2(pm[k] - nm);  // 0 for absent partials (m = -inf)
-                a.x = fmaf(po[k].x, s, a.x);
-                a.y = fmaf(po[k].y, s, a.y);
-                a.z = fmaf(po[k].z, s, a.z);
-                a.w = fmaf(po[k].w, s, a.w);
-                L = fmaf(pl[k], s, L);
-            }
-            M = nm;
-        }
-        const float li = 1.0f / L;
-        __half2* o2 = reinterpret_cast<__half2*>(P.out + ((size_t)i * G + h) * d) + 2 * c4;
-        o2[0] = __floats2half2_rn(a.x * li, a.y * li);
-        o2[1] = __floats2half2_rn(a.z * li, a.w * li);
-    }
-    __syncthreads();
-    fstamp(3);
-    }  // !kSplit
+            __syncthreads();
+            fstamp(3);
+        }  // !kSplit
     }  // units
-    // split: this grid completes after the page grid (the merge kernel's end wait chains on it)
+    // split: the residual CTAs stay resident until the page grid completes (their SM slot beside
+    // the page CTA is not released to merge CTAs, which would only poll their counters there)
     if constexpr (kSplit) asm volatile("griddepcontrol.wait;\n" ::: "memory");
 }
 
