@@ -494,3 +494,52 @@ def test_decode_steps_matches_per_step_calls(mkv, append):
     for c in caches:
         c.check()
         c.close()
+
+
+@pytest.mark.parametrize("G,n_r,append", [(1, 16, True), (8, 16, True), (4, 128, True), (2, 32, False)])
+def test_decode_steps_kernel_vs_oracle(mkv, G, n_r, append):
+    """The unit-resident steps kernel (mkv_decode_steps for few short units) against the oracle's
+    decode at every step: G = 1 / 2 / 4 / 8, flushes every 16 steps (n_r = 16), a partially
+    filled residual block carried in (n_r = 128), attend-only steps, a partial last prefill page."""
+    from tests.gpu_util import f32
+    d, n, L, hh, rw, S = 128, 5, 500, 70, 37, 40
+    scale = 1.0 / np.sqrt(d)
+    k = np.stack([synth_np(SEED, oracle.stream_id(oracle.KIND_K, u), (L, d)) for u in range(n)])
+    v = np.stack([synth_np(SEED, oracle.stream_id(oracle.KIND_V, u), (L, d)) for u in range(n)])
+    a = np.random.default_rng(SEED + G).random((n, L)).astype(np.float32)
+    q = mkv.synth_fp16((S, n, G, d), SEED, (21 << 48) | G, 1 << 16)
+    tk = mkv.synth_fp16((S, n, d), SEED, 22 << 48, 1 << 16)
+    tv = mkv.synth_fp16((S, n, d), SEED, 23 << 48, 1 << 16)
+    cache = mkv.KVCache(n, hh + rw, max_decode_tokens=S + 2 * n_r, n_r=n_r)
+    cache.prefill(torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda(), torch.from_numpy(a).cuda(), hh, rw)
+    P = oracle.port()
+    ocs = []
+    for u in range(n):
+        oc = P.cache(d=d, n_r=n_r)
+        oc.prefill(f32(k[u]), f32(v[u]), a[u], hh, rw)
+        ocs.append(oc)
+    pre = 5 if append else 0  # residual rows carried into the call (per-step path)
+    for s in range(pre):
+        qq = mkv.synth_fp16((n, G, d), SEED, (24 << 48) | s, 1 << 16)
+        kk = mkv.synth_fp16((n, d), SEED, (25 << 48) | s, 1 << 16)
+        vv = mkv.synth_fp16((n, d), SEED, (26 << 48) | s, 1 << 16)
+        cache.decode_step(qq, kk, vv, scale)
+        kn, vn = kk.cpu().numpy(), vv.cpu().numpy()
+        for u in range(n):
+            ocs[u].append(f32(kn[u]), f32(vn[u]))
+    out = cache.decode_steps(q, tk if append else None, tv if append else None, scale)
+    torch.cuda.synchronize()
+    got, qn, tkn, tvn = out.float().cpu().numpy(), q.cpu().numpy(), tk.cpu().numpy(), tv.cpu().numpy()
+    worst = 0.0
+    for s in range(S):
+        for u in range(n):
+            if append:
+                ocs[u].append(f32(tkn[s, u]), f32(tvn[s, u]))
+            for h in range(G):
+                exp = ocs[u].attend(f32(qn[s, u, h]), scale, param_fp16=True)
+                worst = max(worst, max_abs(got[s, u, h], exp))
+    cache.check()
+    info = cache.unit_info(0)
+    assert info["tokens_residual"] == ((pre + S) % n_r if append else 0)
+    assert worst <= TOL, worst
+    cache.close()
