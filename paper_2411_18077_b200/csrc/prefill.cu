@@ -18,10 +18,11 @@
 // Causal convention: query i sees keys 0 .. lk - lq + i (attention.cpp:42,60);
 // masked pairs contribute exactly 0.
 //
-// Warp roles (320 threads): pass 1 -- warps 0-3 / 4-7 softmax of query tile A / B
+// Warp roles: pass 1 (320 threads) -- warps 0-3 / 4-7 softmax of query tile A / B
 // (thread = TMEM lane = row), warp 8 TMA producer, warp 9 TMEM allocator +
-// single-thread MMA issuer; pass 2 -- warps 0-3 / 4-7 two exp warpgroups on
-// alternating query tiles (thread = key row), warp 8 TMA, warp 9 MMA.
+// single-thread MMA issuer; pass 2 (448 threads) -- warps 0-11 three exp warpgroups
+// taking query tiles round-robin (thread = key row, one 128-column S^T buffer each, the
+// key block held in TMEM as the A operand), warp 12 TMA, warp 13 MMA.
 #include <cudaTypedefs.h>
 #include <stdio.h>
 #include <stdlib.h>
