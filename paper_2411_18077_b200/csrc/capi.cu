@@ -408,6 +408,7 @@ int mkv_cache_create(const mkv_cache_config* cfg, mkv_cache** out) {
     if (e == cudaSuccess) e = al((void**)&c->d_unit_cnt, sizeof(int) * n);
     if (e == cudaSuccess) e = cudaMemset(c->d_unit_cnt, 0, sizeof(int) * std::max(n, 1));
     if (e == cudaSuccess) e = al((void**)&c->d_scratch_cnt, sizeof(int) * n);
+    if (e == cudaSuccess) e = cudaMemset(c->d_scratch_cnt, 0, sizeof(int) * std::max(n, 1));
     if (e == cudaSuccess) e = al((void**)&c->d_res_ml, sizeof(float) * 2 * kMaxG * n);
     if (e == cudaSuccess) e = al((void**)&c->d_res_o, sizeof(float) * kMaxG * c->d * n);
     if (e == cudaSuccess) e = cudaMemset(c->d_pool, 0, (size_t)acc * kPageBytes);
@@ -885,7 +886,11 @@ static int decode_impl(mkv_cache* c, const mkv_decode_args* a, bool attend, cuda
     const WorkerRanges wr{std::max(pl->warps, 1), std::max(pl->total / pages_config().batch, 1), pages_config().batch};
     if (split) {
         rp.unit_cnt = c->d_unit_cnt;
-        CK(launch_resid_merge(rp, pl->d_pref, wr, pl->total > 0, std::min(n, num_sms()), s));
+        if (cudaError_t e = launch_resid_merge(rp, pl->d_pref, wr, pl->total > 0, std::min(n, num_sms()), s)) {
+            // the page kernel may have counted: leave no stale arrivals for a later merge
+            cudaMemsetAsync(c->d_unit_cnt + ub, 0, sizeof(int) * n, s);
+            return cuda_fail(e, "decode: residual / merge kernels");
+        }
     } else {
         CK(launch_finish(rp, pl->d_pref, wr, pl->total > 0, s));
     }
@@ -1279,6 +1284,7 @@ int mkv_cache_check(mkv_cache* c) {
     if (st) {
         CK(cudaMemset(c->d_status, 0, sizeof(uint32_t)));
         if (st & kStatusNonFinite) return fail(MKV_ERR_DOMAIN, "quantize_group: non-finite input");
+        if (st & kStatusMergeTimeout) return fail(MKV_ERR_RUNTIME, "decode: a merge timed out waiting for its partials");
     }
     return MKV_OK;
 }

@@ -1092,9 +1092,15 @@ __global__ void __launch_bounds__(kFinishThreads) merge_kernel(const ResidualPar
     if (tid == 0) {
         const int want = n_part + 1;
         int got;
-        for (;;) {
+        // bounded: a lost arrival (an internal error) is reported through the status word
+        // instead of hanging the device
+        for (uint32_t spin = 0;; ++spin) {
             asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(got) : "l"(P.unit_cnt + u) : "memory");
             if (got >= want) break;
+            if (spin > (1u << 23)) {
+                atomicOr(P.status, kStatusMergeTimeout);
+                break;
+            }
             __nanosleep(128);
         }
     }

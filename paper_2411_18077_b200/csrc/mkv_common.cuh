@@ -83,6 +83,7 @@ struct UnitMeta {
 // Device status word bits
 constexpr uint32_t kStatusNonFinite = 1u;
 constexpr uint32_t kStatusOverflow = 2u;
+constexpr uint32_t kStatusMergeTimeout = 4u;  // a merge waited > ~1 s for its unit's arrivals (internal error)
 
 #if defined(__CUDACC__)
 // ---------------------------------------------------------------------------
