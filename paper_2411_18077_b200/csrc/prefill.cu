@@ -697,7 +697,10 @@ cudaError_t launch_prefill_attn(const PrefillAttnParams& p, cudaStream_t s) {
         !make_map(&tv, p.v, p.v_sb, p.v_sh, p.v_st, p.lk, p.hkv, p.batch))
         return cudaErrorInvalidValue;
     // exponentials on the FMA pipe: fwd per 8, A_cumul pairs per 4; MKV_PREFILL_POLY="f,a"
-    static int kf = 1, ka = 1, nb = kAcWG;
+    // default: no pass-1 exponentials on the FMA pipe (since the FMNMX3 row max the softmax
+    // warps' issue slots, not MUFU, bound pass 1: 0 of 8 measured 1-2.5% faster than 1 of 8),
+    // one A_cumul exponential pair in four
+    static int kf = 0, ka = 1, nb = kAcWG;
     static bool direct = false;
     static bool parsed = false;
     if (!parsed) {
@@ -706,18 +709,14 @@ cudaError_t launch_prefill_attn(const PrefillAttnParams& p, cudaStream_t s) {
         if (const char* e = getenv("MKV_ACUMUL_LSE")) direct = e[0] == 'd';
         parsed = true;
     }
-    if (direct && kf == 1 && ka == 1 && nb == kAcWG && p.lq % 4 == 0)
-        return launch_prefill_t<1, 1, kAcWG, true>(tq, tk, tv, p, s);
-    if (nb == 4 && kf == 1) {
-        if (ka == 0) return launch_prefill_t<1, 0, 4>(tq, tk, tv, p, s);
-        if (ka == 2) return launch_prefill_t<1, 2, 4>(tq, tk, tv, p, s);
-        return launch_prefill_t<1, 1, 4>(tq, tk, tv, p, s);
-    }
+    if (direct && kf == 0 && ka == 1 && nb == kAcWG && p.lq % 4 == 0)
+        return launch_prefill_t<0, 1, kAcWG, true>(tq, tk, tv, p, s);
+    if (nb == 4 && kf == 0 && ka == 1) return launch_prefill_t<0, 1, 4>(tq, tk, tv, p, s);
+    if (kf == 1 && ka == 1) return launch_prefill_t<1, 1>(tq, tk, tv, p, s);
     if (kf == 1 && ka == 0) return launch_prefill_t<1, 0>(tq, tk, tv, p, s);
     if (kf == 1 && ka == 2) return launch_prefill_t<1, 2>(tq, tk, tv, p, s);
-    if (kf == 0 && ka == 1) return launch_prefill_t<0, 1>(tq, tk, tv, p, s);
     if (kf == 2 && ka == 1) return launch_prefill_t<2, 1>(tq, tk, tv, p, s);
-    return launch_prefill_t<1, 1>(tq, tk, tv, p, s);
+    return launch_prefill_t<0, 1>(tq, tk, tv, p, s);
 }
 
 }  // namespace mkv
