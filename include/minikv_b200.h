@@ -222,14 +222,16 @@ uint64_t mkv_debug_launch_count(void);
 /* Multi-layer decode step: n_layers consecutive mkv_decode_step calls in one FFI crossing.
  * Layers that continue each other -- adjacent unit ranges, the same group and scale, and
  * q / out / k_new / v_new back to back as in one [layers][units] array -- are coalesced into ONE
- * pass over all their units (one page kernel + one finish kernel for the run): bit-identical
+ * pass over all their units (one page kernel + one finish step for the run): bit-identical
  * to one mkv_decode_step over those units, equal to per-layer calls up to the fp32 rounding of
  * a different split-K partition (MKV_LAYERS_SPLIT=1 disables coalescing).  Any other layer
  * list (overlapping ranges included) gives the per-layer calls' results bit for bit.
  * Precondition -- every layer's q / k_new / v_new is already written when the call is made
  * (stream-ordered before it), and none of them aliases an earlier layer's `out`: a layer whose
- * unit range is disjoint from every earlier layer's starts its page pass (reading its q) while
- * the previous layer's finish kernel is still merging.  This is the "all q known" form (a
+ * unit range is disjoint from every earlier layer's may start its page pass (reading its q)
+ * while the previous layer's finish kernel is still merging (calls of at most one unit per SM;
+ * larger calls split their finish step and start each page pass after the previous merges).
+ * This is the "all q known" form (a
  * benchmark/driver that has every layer's q up front); a model whose q of layer l+1 depends on
  * layer l's output calls mkv_decode_step once per layer (bench.py reports both). */
 int mkv_decode_step_layers(mkv_cache* cache, int n_layers, const mkv_decode_args* args,
