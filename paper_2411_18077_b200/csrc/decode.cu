@@ -1219,13 +1219,44 @@ constexpr int kStepsThreads = kStepsWarps * 32;
 constexpr int kStepsRing = 2 * kBatch * kPageBytes;  // per warp: 2 stages of one 4-page batch (16 KB)
 static_assert(kStepsRing >= (int)sizeof(PageRows), "ring doubles as the residual tile / flush row buffer");
 constexpr size_t kStepsSmem = (size_t)kStepsWarps * (kStepsRing + sizeof(PageParams)) + 2 * kQBytes +
-                              (size_t)kStepsWarps * (2 * kMaxG + kMaxG * kHeadDim) * sizeof(float) + 64;
+                              (size_t)kStepsWarps * (2 * kMaxG + kMaxG * kHeadDim) * sizeof(float) +
+                              2 * (2 * kMaxG + kMaxG * kHeadDim) * sizeof(float) + 64;
 
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ float4 ld_dsmem_f4(const void* local, uint32_t rank) {
+    uint32_t a;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(smem_u32(local)), "r"(rank));
+    float4 v;
+    asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ float ld_dsmem_f(const void* local, uint32_t rank) {
+    uint32_t a;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(smem_u32(local)), "r"(rank));
+    float v;
+    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
+    return v;
+}
+
+// kC > 1: a cluster of kC CTAs per unit (kC x 8 warps share its pages and residual tiles); each
+// CTA merges its 8 warp partials, rank 0 merges the kC CTA partials through distributed shared
+// memory and writes out; rank 0 alone appends / builds the flushed block's pages.
+template <int kC>
 __global__ void __launch_bounds__(kStepsThreads, 1) steps_kernel(const StepsParams P) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = lane_id();
     const int gid = lane >> 2, tig = lane & 3;
-    const int i = blockIdx.x, u = P.unit_begin + i;
+    const uint32_t crank = kC > 1 ? cluster_rank() : 0u;
+    constexpr int kGW = kC * kStepsWarps;  // warps sharing one unit
+    const int gw = (int)crank * kStepsWarps + warp;
+    const int i = blockIdx.x / kC, u = P.unit_begin + i;
     const int d = kHeadDim, G = P.group;
     uint8_t* ring = smem_raw + (size_t)warp * kStepsRing;
     PageParams& prm = reinterpret_cast<PageParams*>(smem_raw + (size_t)kStepsWarps * kStepsRing)[warp];
@@ -1233,6 +1264,7 @@ __global__ void __launch_bounds__(kStepsThreads, 1) steps_kernel(const StepsPara
     float* parts = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(qbuf) + 2 * kQBytes);  // [warp][2][kMaxG] then o
     float (*pml)[2][kMaxG] = reinterpret_cast<float (*)[2][kMaxG]>(parts);
     float* po_all = parts + kStepsWarps * 2 * kMaxG;  // [warp][kMaxG][d]
+    float* cta_part = po_all + kStepsWarps * kMaxG * kHeadDim;  // [2 step parities][ml 2*kMaxG | o kMaxG*d]
     const UnitMeta meta0 = P.meta[u];
     const int64_t page_base = meta0.page_base;
     int n_pages = meta0.n_pages, n_res = meta0.n_res, n_built = meta0.n_built;
@@ -1276,20 +1308,20 @@ __global__ void __launch_bounds__(kStepsThreads, 1) steps_kernel(const StepsPara
         // (then the new pages are built first): its latency overlaps the append
         const bool flushes = P.k_new != nullptr && n_res + 1 == P.n_r;
         int nb = (n_pages + kBatch - 1) / kBatch;
-        int b0 = (int)(((int64_t)warp * nb) / kStepsWarps), b1 = (int)(((int64_t)(warp + 1) * nb) / kStepsWarps);
+        int b0 = (int)(((int64_t)gw * nb) / kGW), b1 = (int)(((int64_t)(gw + 1) * nb) / kGW);
         if (!flushes && b0 < b1) load_batch(b0, 0);
         const bool more = st + 1 < P.n_steps;
         const uint4 q_next = more ? q_chunk(st + 1) : make_uint4(0, 0, 0, 0);
         const uint4 tok_next = more ? tok_chunk(st + 1) : make_uint4(0, 0, 0, 0);
         // ---- decode_append (+ store_block of a full residual block) ----
         if (P.k_new != nullptr) {
-            if (tid < 32) reinterpret_cast<uint4*>((tid < 16 ? rk : rv) + (size_t)n_res * d)[tid & 15] = tok;
+            if (crank == 0 && tid < 32) reinterpret_cast<uint4*>((tid < 16 ? rk : rv) + (size_t)n_res * d)[tid & 15] = tok;
             ++n_res;
             if (n_res == P.n_r) {
                 __threadfence();  // the rows are read back through L2 (cp.async.cg)
                 __syncthreads();
                 PageRows& rows = *reinterpret_cast<PageRows*>(ring);
-                for (int j = warp + n_built; j < P.n_r / kGroup; j += kStepsWarps) {
+                for (int j = warp + n_built; crank == 0 && j < P.n_r / kGroup; j += kStepsWarps) {
                     stage_rows_contig(rows, rk + (size_t)16 * j * d, rv + (size_t)16 * j * d);
                     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
                     __syncwarp();
@@ -1308,7 +1340,12 @@ __global__ void __launch_bounds__(kStepsThreads, 1) steps_kernel(const StepsPara
         // staged from the step's input instead, and reaches L2 for later steps through the fence
         // at the end of this step
         if (flushes) __threadfence();
-        __syncthreads();
+        if constexpr (kC > 1) {
+            if (flushes) cluster_sync_all();  // rank 0's new pages, before any CTA loads them
+            else __syncthreads();
+        } else {
+            __syncthreads();
+        }
 
         // ---- q fragments (as pages_kernel: scales folded in, K-bias copy carries the softmax scale) ----
         uint32_t qb[8][2], qsc[8][2];
@@ -1331,8 +1368,8 @@ __global__ void __launch_bounds__(kStepsThreads, 1) steps_kernel(const StepsPara
         // ---- this warp's pages: batches [b0, b1) of the unit's ceil(n_pages / 4) ----
         if (flushes) {
             nb = (n_pages + kBatch - 1) / kBatch;
-            b0 = (int)(((int64_t)warp * nb) / kStepsWarps);
-            b1 = (int)(((int64_t)(warp + 1) * nb) / kStepsWarps);
+            b0 = (int)(((int64_t)gw * nb) / kGW);
+            b1 = (int)(((int64_t)(gw + 1) * nb) / kGW);
             if (b0 < b1) load_batch(b0, 0);
         }
         for (int b = b0; b < b1; ++b) {
@@ -1471,8 +1508,8 @@ __global__ void __launch_bounds__(kStepsThreads, 1) steps_kernel(const StepsPara
         }
 
         // ---- residual tiles (exact fp16 attention, as finish_kernel), same online softmax ----
-        // tile t goes to warp kStepsWarps - 1 - t % kStepsWarps (the page ranges differ by <= 1 batch)
-        for (int t = kStepsWarps - 1 - warp; 16 * t < n_res; t += kStepsWarps) {
+        // tile t goes to warp kGW - 1 - t % kGW of the unit (the page ranges differ by <= 1 batch)
+        for (int t = kGW - 1 - gw; 16 * t < n_res; t += kGW) {
             const int nrows = min(16, n_res - 16 * t);
             uint8_t* tile = ring;  // this warp's page batches are done: its ring holds the tile
             const bool fresh = P.k_new != nullptr && !flushes;  // row n_res - 1 came with this step
@@ -1574,10 +1611,50 @@ __global__ void __launch_bounds__(kStepsThreads, 1) steps_kernel(const StepsPara
                     M = nm;
                 }
             }
-            const float li = 1.0f / L;
-            __half2* o2 = reinterpret_cast<__half2*>(P.out + (size_t)st * P.out_step + ((size_t)i * G + h) * d) + 2 * c4;
-            o2[0] = __floats2half2_rn(a.x * li, a.y * li);
-            o2[1] = __floats2half2_rn(a.z * li, a.w * li);
+            if constexpr (kC == 1) {
+                const float li = 1.0f / L;
+                __half2* o2 = reinterpret_cast<__half2*>(P.out + (size_t)st * P.out_step + ((size_t)i * G + h) * d) + 2 * c4;
+                o2[0] = __floats2half2_rn(a.x * li, a.y * li);
+                o2[1] = __floats2half2_rn(a.z * li, a.w * li);
+            } else {
+                float* cp = cta_part + (size_t)(st & 1) * (2 * kMaxG + kMaxG * kHeadDim);
+                reinterpret_cast<float4*>(cp + 2 * kMaxG + h * d)[c4] = a;
+                if (c4 == 0) { cp[h] = M; cp[kMaxG + h] = L; }
+            }
+        }
+        if constexpr (kC > 1) {
+            // every CTA's partial of this step is in its shared memory; rank 0 merges them.  The
+            // buffers alternate by step: a CTA writes the same buffer again two steps later, after
+            // the next step's barrier, which rank 0 reaches only when this merge is done.
+            cluster_sync_all();
+            if (crank == 0) {
+                const float* cp = cta_part + (size_t)(st & 1) * (2 * kMaxG + kMaxG * kHeadDim);
+                for (int e = tid; e < G * (d / 4); e += kStepsThreads) {
+                    const int h = e / (d / 4), c4 = e % (d / 4);
+                    float M = -INFINITY, L = 0.0f;
+                    float4 a = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+#pragma unroll
+                    for (int r = 0; r < kC; ++r) {
+                        const float lr = ld_dsmem_f(cp + kMaxG + h, (uint32_t)r);
+                        if (lr > 0.0f) {
+                            const float mr = ld_dsmem_f(cp + h, (uint32_t)r);
+                            const float4 v = ld_dsmem_f4(cp + 2 * kMaxG + h * d + 4 * c4, (uint32_t)r);
+                            const float nm = fmaxf(M, mr);
+                            const float f = fast_exp2(M - nm), sc = fast_exp2(mr - nm);
+                            a.x = fmaf(v.x, sc, a.x * f);
+                            a.y = fmaf(v.y, sc, a.y * f);
+                            a.z = fmaf(v.z, sc, a.z * f);
+                            a.w = fmaf(v.w, sc, a.w * f);
+                            L = fmaf(lr, sc, L * f);
+                            M = nm;
+                        }
+                    }
+                    const float li = 1.0f / L;
+                    __half2* o2 = reinterpret_cast<__half2*>(P.out + (size_t)st * P.out_step + ((size_t)i * G + h) * d) + 2 * c4;
+                    o2[0] = __floats2half2_rn(a.x * li, a.y * li);
+                    o2[1] = __floats2half2_rn(a.z * li, a.w * li);
+                }
+            }
         }
         // next step's q into the other buffer; the appended row reaches L2 for later steps
         if (more && tid < G * d / 8) reinterpret_cast<uint4*>(qbuf + ((st + 1) & 1) * (kQBytes / 2))[tid] = q_next;
@@ -1586,23 +1663,56 @@ __global__ void __launch_bounds__(kStepsThreads, 1) steps_kernel(const StepsPara
         __syncthreads();  // partials / q staging are reused by the next step
     }
     if (!ok && lane == 0) atomicOr(P.status, kStatusNonFinite);
-    if (tid == 0) {
+    if constexpr (kC > 1) cluster_sync_all();  // no CTA exits while rank 0 may still read its partials
+    if (crank == 0 && tid == 0) {
         P.meta[u].n_pages = n_pages;
         P.meta[u].n_res = n_res;
         P.meta[u].n_built = n_built;
     }
 }
 
-cudaError_t launch_steps(const StepsParams& p, cudaStream_t s) {
+template <int kC>
+static cudaError_t launch_steps_c(const StepsParams& p, cudaStream_t s) {
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(steps_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStepsSmem);
+        cudaError_t e = cudaFuncSetAttribute(steps_kernel<kC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStepsSmem);
+        if (e == cudaSuccess && kC > 1) e = cudaFuncSetAttribute(steps_kernel<kC>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e != cudaSuccess) return e;
         configured = true;
     }
     count_launch(1);
-    steps_kernel<<<p.n_units, kStepsThreads, kStepsSmem, s>>>(p);
-    return cudaGetLastError();
+    if constexpr (kC == 1) {
+        steps_kernel<1><<<p.n_units, kStepsThreads, kStepsSmem, s>>>(p);
+        return cudaGetLastError();
+    } else {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(p.n_units * kC);
+        cfg.blockDim = dim3(kStepsThreads);
+        cfg.dynamicSmemBytes = kStepsSmem;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = kC;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, steps_kernel<kC>, p);
+    }
+}
+
+// CTAs per unit: as many as fit one CTA per SM (4, 2 or 1); MKV_STEPS_CLUSTER=1|2|4 forces it.
+cudaError_t launch_steps(const StepsParams& p, cudaStream_t s) {
+    static const int forced = [] {
+        const char* e = getenv("MKV_STEPS_CLUSTER");
+        return e ? atoi(e) : 0;
+    }();
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    int c = forced == 1 || forced == 2 || forced == 4 ? forced : (p.n_units * 4 <= sms ? 4 : (p.n_units * 2 <= sms ? 2 : 1));
+    if (c == 4) return launch_steps_c<4>(p, s);
+    if (c == 2) return launch_steps_c<2>(p, s);
+    return launch_steps_c<1>(p, s);
 }
 
 }  // namespace mkv
