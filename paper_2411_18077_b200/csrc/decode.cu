@@ -1701,7 +1701,8 @@ static cudaError_t launch_steps_c(const StepsParams& p, cudaStream_t s) {
     }
 }
 
-// CTAs per unit: as many as fit one CTA per SM (4, 2 or 1); MKV_STEPS_CLUSTER=1|2|4 forces it.
+// CTAs per unit: as many as fit one CTA per SM (4, 2 or 1; 8 measured no faster than 4);
+// MKV_STEPS_CLUSTER=1|2|4|8 forces it.
 cudaError_t launch_steps(const StepsParams& p, cudaStream_t s) {
     static const int forced = [] {
         const char* e = getenv("MKV_STEPS_CLUSTER");
@@ -1709,7 +1710,9 @@ cudaError_t launch_steps(const StepsParams& p, cudaStream_t s) {
     }();
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    int c = forced == 1 || forced == 2 || forced == 4 ? forced : (p.n_units * 4 <= sms ? 4 : (p.n_units * 2 <= sms ? 2 : 1));
+    int c = forced == 1 || forced == 2 || forced == 4 || forced == 8 ? forced
+                                                                     : (p.n_units * 4 <= sms ? 4 : (p.n_units * 2 <= sms ? 2 : 1));
+    if (c == 8) return launch_steps_c<8>(p, s);
     if (c == 4) return launch_steps_c<4>(p, s);
     if (c == 2) return launch_steps_c<2>(p, s);
     return launch_steps_c<1>(p, s);
