@@ -243,7 +243,7 @@ int mkv_decode_step_layers(mkv_cache* cache, int n_layers, const mkv_decode_args
  * and writes out + s * out_step (strides in fp16 ELEMENTS; k_new / v_new may be null: attend
  * only).  Every step's inputs must be written before the call.  Few short units (at most one
  * per SM, <= 1024 pages each by the last step) are served by one launch that keeps each unit on
- * one CTA for all the steps: outputs equal n_steps mkv_decode_step calls up to the fp32
+ * one cluster of CTAs for all the steps: outputs equal n_steps mkv_decode_step calls up to the fp32
  * accumulation order of a different split of the pages, the cache state bit for bit; other
  * calls run the per-step kernels and are bit-identical to mkv_decode_step calls
  * (MKV_STEPS=off forces that path). */

@@ -18,7 +18,12 @@
 //                  (warp, unit) segment.
 //   finish_kernel  one CTA per unit: decode_append (non-flush steps), exact
 //                  attention over the fp16 residual (mma, one warp per 16-token
-//                  tile), and the split-K merge of every partial into out.
+//                  tile), and the split-K merge of every partial into out.  With
+//                  more units than SMs: finish_kernel<true> (persistent, residual
+//                  work beside the page pass) + merge_kernel (per-unit arrival
+//                  counters).
+//   steps_kernel   mkv_decode_steps for few short units: a cluster of CTAs per
+//                  unit runs every step (append, flush, pages, residual, merge).
 //
 // Dequantization never materialises fp16 K/V: each 2-bit code becomes an fp16
 // *subnormal* code * 4^s * 2^-24 with one LOP3 (s = position for the first five codes of a

@@ -338,7 +338,7 @@ class KVCache:
                      scale: float, unit_begin: int = 0, out: Optional[torch.Tensor] = None, stream=None):
         """S consecutive decode steps over a prepared token stream in one call (mkv_decode_steps):
         q fp16 [S, n, G, d], k_new / v_new fp16 [S, n, d] (None: attend only); out [S, n, G, d].
-        Few short units run as one launch (a CTA per unit for all S steps): the cache state is
+        Few short units run as one launch (a cluster of CTAs per unit for all S steps): the cache state is
         that of S decode_step calls bit for bit, outputs equal them up to fp32 accumulation
         order; other calls run the per-step kernels (bit-identical; MKV_STEPS=off forces them)."""
         S, n, G, d = q.shape
