@@ -716,13 +716,38 @@ def config0_gpu():
         e2es.append((time.perf_counter() - t0) * 1e3)
         cache.close()
     e2e_ms = sorted(e2es)[len(e2es) // 2]
+    # the same 256 decode steps as one mkv_decode_step call per step (the form a model's token
+    # loop drives, each step's q known only when it is issued), device-timed after an untimed
+    # prefill; outputs checked against the token-stream kernel's
+    per_step = []
+    outs1 = torch.empty_like(outs)
+    for _ in range(5):  # median of 5
+        cache = new_cache()
+        r1 = mkv.selective_flash_attn(q, k, v, scale, True)
+        cache.prefill(k[0], v[0], r1.a_cumul[0], hh, rw)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        ev[0].record()
+        for s in range(steps):
+            cache.decode_step(qd[s].view(H, 1, d), kd[s], vd[s], scale, out=outs1[s].view(H, 1, d))
+        ev[1].record()
+        torch.cuda.synchronize()
+        per_step.append(ev[0].elapsed_time(ev[1]))
+        cache.close()
+    per_step_ms = sorted(per_step)[len(per_step) // 2]
+    per_step_dev = float((outs1.float() - outs.float()).abs().max().item())
     total_ms = t_attn + t_pack + t_dec
     P = L * (L + 1) / 2
     return {
         "workload": "configs[0]: 1 layer, 8 heads (MHA), d=128, 4K causal prefill (K1) -> 20% budget select (K2, "
                     "409 HH + 409 RW) -> 2-bit pack (K3) -> 256 decode steps (K4, 2 flushes)",
         "gpu_ms": {"prefill_attn": t_attn, "select_pack": t_pack, "decode_256": t_dec, "total": total_ms,
-                   "e2e_total_from_host": e2e_ms, "make_cache_outside_timing": sorted(allocs)[len(allocs) // 2]},
+                   "e2e_total_from_host": e2e_ms, "make_cache_outside_timing": sorted(allocs)[len(allocs) // 2],
+                   "decode_256_per_step_calls": per_step_ms},
+        "per_step_calls": {"how": "256 mkv_decode_step calls (one per step, q of step s issued with step s), "
+                                  "device time after an untimed prefill; the headline chain's decode_256 runs the "
+                                  "same steps as one mkv_decode_steps call over the prepared token stream, as the "
+                                  "reference CLI's loop over its stream does",
+                           "max_abs_vs_decode_steps": per_step_dev},
         "how": "make_cache (the device pool allocation) before the timed region; K1 -> K2+K3 -> "
                "256 decode steps through KVCache.decode_steps (mkv_decode_steps: one FFI crossing); "
                "e2e copies Q/K/V and the decode tokens from pinned host buffers and reads every output back",
