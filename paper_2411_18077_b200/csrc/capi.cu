@@ -358,6 +358,8 @@ int mkv_select(const mkv_select_args* a, void* stream) {
 // ---------------------------------------------------------------------------
 // cache lifecycle
 // ---------------------------------------------------------------------------
+static int plan_reserve(mkv_cache* c, int ub, int n);
+
 int mkv_cache_create(const mkv_cache_config* cfg, mkv_cache** out) {
     if (!cfg || !out) return fail(MKV_ERR_INVALID_ARGUMENT, "make_cache: null argument");
     if (cfg->head_dim < 1) return fail(MKV_ERR_INVALID_ARGUMENT, "make_cache: d must be >= 1");
@@ -417,6 +419,13 @@ int mkv_cache_create(const mkv_cache_config* cfg, mkv_cache** out) {
     if (e != cudaSuccess) {
         delete c;
         return cuda_fail(e, "make_cache: device allocation");
+    }
+    // the page plan of a call over every unit (the usual decode call) is allocated with the pool:
+    // its device buffers, partial slots and pinned staging buffer otherwise cost the first decode
+    // step after a prefill ~3 ms of host time (cudaMalloc / cudaMallocHost)
+    if (int r = plan_reserve(c, 0, n)) {
+        delete c;
+        return r;
     }
     *out = c;
     return MKV_OK;
@@ -636,6 +645,24 @@ static int stage_plan(mkv_cache* c, Plan& pl, const HostPlan& hp, int n, size_t*
     memcpy(pl.h_stage, hp.buf.data(), ib);
     memcpy(static_cast<uint8_t*>(pl.h_stage) + ib, hp.rec.data(), rb);
     *bytes = ib + rb;
+    return MKV_OK;
+}
+
+// Allocates the plan of calls over units [ub, ub + n) ahead of its first use (device buffers,
+// partial slots, upload event, pinned staging buffer); its contents are built by the first call.
+static int plan_reserve(mkv_cache* c, int ub, int n) {
+    const uint64_t key = ((uint64_t)(uint32_t)ub << 32) | (uint32_t)n;
+    Plan& pl = c->plans[key];
+    if (int r = plan_alloc(c, pl, n)) return r;
+    if (!pl.ready) CK(cudaEventCreateWithFlags(&pl.ready, cudaEventDisableTiming));
+    const size_t need = sizeof(int32_t) * plan_ints(c) + sizeof(UnitRec) * n;
+    if (pl.stage_bytes < need) {
+        if (pl.h_stage) cudaFreeHost(pl.h_stage);
+        pl.h_stage = nullptr;
+        pl.stage_bytes = 0;
+        CK(cudaMallocHost(&pl.h_stage, need));
+        pl.stage_bytes = need;
+    }
     return MKV_OK;
 }
 
