@@ -26,8 +26,15 @@ from ._capi import check, lib
 
 
 def _stream_ptr(stream: Optional[torch.cuda.Stream] = None) -> int:
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return int(s.cuda_stream)
+    if stream is not None:
+        return int(stream.cuda_stream)
+    # the raw handle of the current stream without building a torch.cuda.Stream object (a few
+    # us per call: it is on every decode call's host path)
+    return _raw_stream(torch.cuda.current_device())
+
+
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None) or \
+    (lambda dev: int(torch.cuda.current_stream(dev).cuda_stream))
 
 
 def default_scale(d_head: int) -> float:

@@ -90,3 +90,32 @@ for name, fn in (("torch x.add_(1) (reference launch)", lambda: x.add_(1)),
     t2 = time.perf_counter()
     print(f"{name:40s} host {1e6 * (t1 - t0) / N:6.2f} us/call, wall {1e6 * (t2 - t0) / N:6.2f} us/call")
 c.close()
+
+# per-step host and wall times of the 256 append + attend calls (synchronized after each step)
+c = fresh()
+args = [_capi.DecodeArgs(0, H, 1, qd[s].data_ptr(), kd[s].data_ptr(), vd[s].data_ptr(), outs[s].data_ptr(), scale)
+        for s in range(S)]
+hs, ws = [], []
+for s in range(S):
+    t0 = time.perf_counter()
+    _capi.check(L_.mkv_decode_step(c.h, C.byref(args[s]), sp), "decode")
+    t1 = time.perf_counter()
+    torch.cuda.synchronize()
+    t2 = time.perf_counter()
+    hs.append(1e6 * (t1 - t0))
+    ws.append(1e6 * (t2 - t0))
+import numpy as np  # noqa: E402
+hs, ws = np.array(hs), np.array(ws)
+print(f"append+attend per step: host median {np.median(hs):.2f} us, max {hs.max():.1f} us at step {hs.argmax()}; "
+      f"wall median {np.median(ws):.2f} us, max {ws.max():.1f} us at step {ws.argmax()}")
+print("steps with host > 3x median:", [(int(i), round(float(hs[i]), 1)) for i in np.nonzero(hs > 3 * np.median(hs))[0]])
+print("steps with wall > 2x median:", [(int(i), round(float(ws[i]), 1)) for i in np.nonzero(ws > 2 * np.median(ws))[0]])
+c.close()
+
+# the wrapper's current-stream lookup
+for name, fn in (("torch.cuda.current_stream().cuda_stream", lambda: torch.cuda.current_stream().cuda_stream),
+                 ("ops._stream_ptr()", lambda: mkv.ops._stream_ptr())):
+    t0 = time.perf_counter()
+    for _ in range(N):
+        fn()
+    print(f"{name:40s} {1e6 * (time.perf_counter() - t0) / N:6.2f} us/call")
