@@ -146,6 +146,9 @@ typedef struct {
     int keep_fp32_params;       /* also keep fp32 (scale, zero) for bit-exact export */
 } mkv_cache_config;
 
+/* Allocates the page pool, residual rows and the page plan of calls over all n_units (its
+ * device buffers and pinned staging buffer), so the first decode call after a prefill does no
+ * allocation; a call over another unit range allocates that range's plan on first use. */
 int mkv_cache_create(const mkv_cache_config* cfg, mkv_cache** out);
 int mkv_cache_destroy(mkv_cache* cache);
 /* Device bytes held: quantized pages, residual ring, metadata. */
