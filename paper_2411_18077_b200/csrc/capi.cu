@@ -11,6 +11,8 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
+#include <map>
+#include <mutex>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -77,6 +79,39 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 // ---------------------------------------------------------------------------
 // cache object
 // ---------------------------------------------------------------------------
+// Pinned staging buffers of page plans, kept across caches: pinning host memory costs ~1-3 ms
+// per buffer, which would otherwise land on every make_cache.  A freed buffer is parked here and
+// handed to the next request it fits (smallest fit); buffers are never unpinned.
+struct PinnedPool {
+    std::mutex mu;
+    std::multimap<size_t, void*> free_;  // capacity -> buffer
+};
+static PinnedPool& pinned_pool() {
+    static PinnedPool* p = new PinnedPool;  // leaked on purpose: outlives static caches at exit
+    return *p;
+}
+static cudaError_t pinned_get(size_t need, void** out, size_t* cap) {
+    PinnedPool& pp = pinned_pool();
+    {
+        std::lock_guard<std::mutex> g(pp.mu);
+        auto it = pp.free_.lower_bound(need);
+        if (it != pp.free_.end()) {
+            *cap = it->first;
+            *out = it->second;
+            pp.free_.erase(it);
+            return cudaSuccess;
+        }
+    }
+    *cap = need;
+    return cudaMallocHost(out, need);
+}
+static void pinned_put(void* p, size_t cap) {
+    if (!p) return;
+    PinnedPool& pp = pinned_pool();
+    std::lock_guard<std::mutex> g(pp.mu);
+    pp.free_.emplace(cap, p);
+}
+
 struct Plan {
     std::vector<int32_t> sig;  // per unit (pages, prefill rows) the plan was built for
     int total = 0, warps = 0, grid = 0;  // padded pages, workers (balanced ranges), CTAs
@@ -132,7 +167,7 @@ struct mkv_cache {
             cudaFree(kv.second.d_part_ml);
             cudaFree(kv.second.d_part_o);
             if (kv.second.ready) cudaEventDestroy(kv.second.ready);
-            if (kv.second.h_stage) cudaFreeHost(kv.second.h_stage);
+            pinned_put(kv.second.h_stage, kv.second.stage_bytes);
         }
         if (copy_stream) cudaStreamDestroy(copy_stream);
         if (ev_compute) cudaEventDestroy(ev_compute);
@@ -423,10 +458,15 @@ int mkv_cache_create(const mkv_cache_config* cfg, mkv_cache** out) {
     // the page plan of a call over every unit (the usual decode call) is allocated with the pool:
     // its device buffers, partial slots and pinned staging buffer otherwise cost the first decode
     // step after a prefill ~3 ms of host time (cudaMalloc / cudaMallocHost)
-    if (int r = plan_reserve(c, 0, n)) {
-        delete c;
-        return r;
-    }
+    static const bool reserve = [] {
+        const char* e = getenv("MKV_PLAN_RESERVE");
+        return !(e && e[0] == '0');
+    }();
+    if (reserve)
+        if (int r = plan_reserve(c, 0, n)) {
+            delete c;
+            return r;
+        }
     *out = c;
     return MKV_OK;
 }
@@ -636,11 +676,10 @@ static int stage_plan(mkv_cache* c, Plan& pl, const HostPlan& hp, int n, size_t*
     CK(cudaEventSynchronize(pl.ready));
     const size_t ib = sizeof(int32_t) * plan_ints(c), rb = sizeof(UnitRec) * n;
     if (pl.stage_bytes < ib + rb) {
-        if (pl.h_stage) cudaFreeHost(pl.h_stage);
+        pinned_put(pl.h_stage, pl.stage_bytes);
         pl.h_stage = nullptr;
         pl.stage_bytes = 0;
-        CK(cudaMallocHost(&pl.h_stage, ib + rb));
-        pl.stage_bytes = ib + rb;
+        CK(pinned_get(ib + rb, &pl.h_stage, &pl.stage_bytes));
     }
     memcpy(pl.h_stage, hp.buf.data(), ib);
     memcpy(static_cast<uint8_t*>(pl.h_stage) + ib, hp.rec.data(), rb);
@@ -657,11 +696,10 @@ static int plan_reserve(mkv_cache* c, int ub, int n) {
     if (!pl.ready) CK(cudaEventCreateWithFlags(&pl.ready, cudaEventDisableTiming));
     const size_t need = sizeof(int32_t) * plan_ints(c) + sizeof(UnitRec) * n;
     if (pl.stage_bytes < need) {
-        if (pl.h_stage) cudaFreeHost(pl.h_stage);
+        pinned_put(pl.h_stage, pl.stage_bytes);
         pl.h_stage = nullptr;
         pl.stage_bytes = 0;
-        CK(cudaMallocHost(&pl.h_stage, need));
-        pl.stage_bytes = need;
+        CK(pinned_get(need, &pl.h_stage, &pl.stage_bytes));
     }
     return MKV_OK;
 }
